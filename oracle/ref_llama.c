@@ -1,0 +1,484 @@
+/*
+ * oracle/ref_llama.c -- TEST INFRASTRUCTURE ONLY (the CPU oracle).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg load
+ * this file's library (oracle/_lib/libref_llama.so), and only as the checker.
+ * The product (paper_2506_02006_b200/) never links, imports or calls it.
+ *
+ * What it restates:
+ *  - The reference's quantizer (proj/src/toy_model.cpp:40-60,
+ *    quantize_row_scale / quantize_weights): symmetric round-to-nearest,
+ *    scale = max|w| / (2^(b-1) - 1) in fp64, code = std::round(w / scale)
+ *    (half away from zero), all-zero group => scale 1, codes 0.  The group is
+ *    128 consecutive K elements of a row instead of the whole row (SURVEY
+ *    8(c): "g128 grouping").  Pinned against the compiled reference via
+ *    tests/golden (see tests/golden/make_golden.py).
+ *  - The reference's per-layer precision dispatch inside one forward
+ *    (proj/src/toy_model.cpp:139-168, `model.weights(p, config.tags[p])` at
+ *    :153): every layer picks its BF16 or dequantized-W4 weights from its tag.
+ *  - The reference has NO Llama forward (SPEC.md:14 puts kernels out of
+ *    scope).  The Llama-style decoder below is this repo's own definition of
+ *    the math the GPU path must compute: it is
+ *    "parity unpinned" against the reference and pinned only by the frozen
+ *    fixtures under tests/golden.  Rounding points mirror the GPU kernels:
+ *      residual stream fp32; GEMM inputs rounded to bf16; fp64 accumulation;
+ *      RoPE (rotate-half) in fp32 from a host fp64 table; K/V cached as bf16;
+ *      softmax fp32; attention output rounded to bf16; SiLU(g)*u rounded to
+ *      bf16; greedy argmax with ties to the lowest index.
+ *  - A counter-based weight generator (splitmix64 of (seed, tensor, index))
+ *    that the GPU generator reproduces bit for bit.
+ *
+ * Plain C11 + OpenMP, no dependencies.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ------------------------------------------------------------------ bf16 */
+static inline float bf2f(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+static inline uint16_t f2bf(float f) { /* round to nearest even */
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u);
+  uint32_t r = ((u >> 16) & 1u) + 0x7fffu;
+  return (uint16_t)((u + r) >> 16);
+}
+float ref_bf16_to_float(uint16_t b) { return bf2f(b); }
+uint16_t ref_float_to_bf16(float f) { return f2bf(f); }
+
+/* ------------------------------------------------------- weight generator */
+static inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+/* value = offset + scale * u,  u uniform in [-1, 1): fp64 then fp32 then bf16 */
+static inline uint16_t gen_one(uint64_t seed, uint64_t tensor, uint64_t idx, double scale,
+                               double offset) {
+  uint64_t key = seed ^ (tensor * 0xD1B54A32D192ED03ull);
+  uint64_t r = splitmix64(key + idx);
+  double u = (double)(r >> 11) * 0x1.0p-53;
+  double w = 2.0 * u - 1.0;
+  w = w * scale;
+  w = w + offset;
+  return f2bf((float)w);
+}
+void ref_gen_weight(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset,
+                    uint16_t* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = gen_one(seed, tensor, (uint64_t)i, scale, offset);
+}
+
+/* Tensor ids (shared convention with the GPU generator). */
+enum { T_EMBED = 0, T_NORMF = 1, T_LMHEAD = 2 };
+static inline uint64_t t_layer(int l, int which) { return 16u + (uint64_t)l * 8u + (uint64_t)which; }
+enum { W_NORM1 = 0, W_QKV = 1, W_O = 2, W_NORM2 = 3, W_GU = 4, W_DOWN = 5 };
+
+/* ----------------------------------------------------------- quantizer */
+/* Per group of `group` K-elements of each row of a row-major [N][K] bf16
+ * matrix.  Mirrors toy_model.cpp:40-60 (per row there, per group here). */
+void ref_quantize_groups(const uint16_t* w, int64_t N, int64_t K, int group, int bits,
+                         int8_t* codes, double* scales_f64, uint16_t* scales_bf16) {
+  const int64_t G = K / group;
+  const double qmax = (double)((1 << (bits - 1)) - 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    for (int64_t g = 0; g < G; ++g) {
+      const uint16_t* src = w + n * K + g * group;
+      double max_abs = 0.0;
+      for (int i = 0; i < group; ++i) {
+        double a = fabs((double)bf2f(src[i]));
+        if (a > max_abs) max_abs = a;
+      }
+      double scale = 1.0;
+      int8_t* dst = codes + n * K + g * group;
+      if (max_abs == 0.0) {
+        for (int i = 0; i < group; ++i) dst[i] = 0;
+      } else {
+        scale = max_abs / qmax;
+        for (int i = 0; i < group; ++i) dst[i] = (int8_t)round((double)bf2f(src[i]) / scale);
+      }
+      if (scales_f64) scales_f64[n * G + g] = scale;
+      if (scales_bf16) scales_bf16[n * G + g] = f2bf((float)scale);
+    }
+  }
+}
+
+/* W4A16 dequantization contract: bf16(code * float(scale_bf16)), one RNE. */
+void ref_dequant_w4(const int8_t* codes, const uint16_t* scales_bf16, int64_t N, int64_t K,
+                    int group, uint16_t* out) {
+  const int64_t G = K / group;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t k = 0; k < K; ++k)
+      out[n * K + k] = f2bf((float)codes[n * K + k] * bf2f(scales_bf16[n * G + k / group]));
+}
+
+/* ----------------------------------------------- device layout restatement */
+/* BF16 weight chunk layout: chunk (n_tile, kb)
+ * holds rows [128*n_tile, +128) x cols [64*kb, +64) as
+ * [row_group 16][k_chunk 8][row 8][8 elems]; chunks ordered n_tile-major. */
+void ref_pack_bf16(const uint16_t* w, int64_t N, int64_t K, uint16_t* out) {
+  const int64_t KB = K / 64;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    const int64_t nt = n / 128, rr = n % 128, g = rr / 8, r = rr % 8;
+    for (int64_t k = 0; k < K; ++k) {
+      const int64_t kb = k / 64, kk = k % 64, c = kk / 8, e = kk % 8;
+      const int64_t chunk = nt * KB + kb;
+      out[chunk * 8192 + ((g * 8 + c) * 8 + r) * 8 + e] = w[n * K + k];
+    }
+  }
+}
+
+/* W4 chunk layout: chunk (n_tile, group g of 128 K) = 8448 bytes:
+ *   bytes [0, 8192): codes as [j 4][row 128][16 B]; the 16 B of (j,row) hold
+ *   K-elements [32j, 32j+32) of the group, 4 u32 words, word w holds elements
+ *   32j+8w .. +7 with element e at bits 4e..4e+3, stored as (code + 8).
+ *   bytes [8192, 8448): 128 bf16 scales, one per row. */
+void ref_pack_w4(const int8_t* codes, const uint16_t* scales_bf16, int64_t N, int64_t K,
+                 uint8_t* out) {
+  const int64_t G = K / 128;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    const int64_t nt = n / 128, row = n % 128;
+    for (int64_t g = 0; g < G; ++g) {
+      uint8_t* chunk = out + (nt * G + g) * 8448;
+      for (int j = 0; j < 4; ++j) {
+        uint32_t words[4];
+        for (int w = 0; w < 4; ++w) {
+          uint32_t v = 0;
+          for (int e = 0; e < 8; ++e) {
+            int k = g * 128 + j * 32 + w * 8 + e;
+            uint32_t nib = (uint32_t)(codes[n * K + k] + 8) & 0xFu;
+            v |= nib << (4 * e);
+          }
+          words[w] = v;
+        }
+        memcpy(chunk + (j * 128 + row) * 16, words, 16);
+      }
+      uint16_t s = scales_bf16[n * G + g];
+      memcpy(chunk + 8192 + row * 2, &s, 2);
+    }
+  }
+}
+
+/* --------------------------------------------------------------- model */
+typedef struct {
+  int L, d, H, KVH, hd, ffn, V, max_pos;
+  float eps;
+  double theta;
+} ref_cfg;
+
+typedef struct {
+  ref_cfg c;
+  uint64_t seed;
+  uint16_t *embed, *normf, *lm_head;
+  uint16_t **norm1, **norm2;
+  uint16_t **wqkv, **wo, **wgu, **wd;       /* effective bf16 weights */
+  uint16_t **bqkv, **bo, **bgu, **bd;       /* pristine BF16 copies (for restore) */
+  int* tag;                                  /* 0 = BF16, 4 = W4 */
+  float *rope_cos, *rope_sin;                /* [max_pos][hd/2] */
+} ref_model;
+
+typedef struct {
+  int len, cap;
+  uint16_t** k; /* [L] -> [cap][KVH][hd] */
+  uint16_t** v;
+} ref_seq;
+
+static uint16_t* gen_alloc(uint64_t seed, uint64_t tensor, int64_t n, double scale, double off) {
+  uint16_t* p = (uint16_t*)malloc((size_t)n * 2);
+  ref_gen_weight(seed, tensor, n, scale, off, p);
+  return p;
+}
+
+/* RoPE table: angle = pos * theta^(-2i/hd) computed in fp64, stored fp32. */
+void ref_rope_table(int max_pos, int hd, double theta, float* cos_out, float* sin_out) {
+  const int half = hd / 2;
+  for (int p = 0; p < max_pos; ++p)
+    for (int i = 0; i < half; ++i) {
+      double inv = pow(theta, -2.0 * (double)i / (double)hd);
+      double a = (double)p * inv;
+      cos_out[(int64_t)p * half + i] = (float)cos(a);
+      sin_out[(int64_t)p * half + i] = (float)sin(a);
+    }
+}
+
+ref_model* ref_model_create(const ref_cfg* cfg, uint64_t seed) {
+  ref_model* m = (ref_model*)calloc(1, sizeof(ref_model));
+  m->c = *cfg;
+  m->seed = seed;
+  const ref_cfg* c = cfg;
+  const int64_t qkv_n = (int64_t)(c->H + 2 * c->KVH) * c->hd;
+  m->embed = gen_alloc(seed, T_EMBED, (int64_t)c->V * c->d, 1.0, 0.0);
+  m->normf = gen_alloc(seed, T_NORMF, c->d, 0.1, 1.0);
+  m->lm_head = gen_alloc(seed, T_LMHEAD, (int64_t)c->V * c->d, 1.0 / sqrt((double)c->d), 0.0);
+#define ALLOC_L(f) m->f = (uint16_t**)calloc(c->L, sizeof(uint16_t*))
+  ALLOC_L(norm1); ALLOC_L(norm2); ALLOC_L(wqkv); ALLOC_L(wo); ALLOC_L(wgu); ALLOC_L(wd);
+  ALLOC_L(bqkv); ALLOC_L(bo); ALLOC_L(bgu); ALLOC_L(bd);
+#undef ALLOC_L
+  m->tag = (int*)calloc(c->L, sizeof(int));
+  for (int l = 0; l < c->L; ++l) {
+    m->norm1[l] = gen_alloc(seed, t_layer(l, W_NORM1), c->d, 0.1, 1.0);
+    m->norm2[l] = gen_alloc(seed, t_layer(l, W_NORM2), c->d, 0.1, 1.0);
+    m->bqkv[l] = gen_alloc(seed, t_layer(l, W_QKV), qkv_n * c->d, 1.0 / sqrt((double)c->d), 0.0);
+    m->bo[l] = gen_alloc(seed, t_layer(l, W_O), (int64_t)c->d * c->H * c->hd,
+                         1.0 / sqrt((double)(c->H * c->hd)), 0.0);
+    m->bgu[l] = gen_alloc(seed, t_layer(l, W_GU), (int64_t)2 * c->ffn * c->d,
+                          1.0 / sqrt((double)c->d), 0.0);
+    m->bd[l] = gen_alloc(seed, t_layer(l, W_DOWN), (int64_t)c->d * c->ffn,
+                         1.0 / sqrt((double)c->ffn), 0.0);
+    m->wqkv[l] = m->bqkv[l]; m->wo[l] = m->bo[l]; m->wgu[l] = m->bgu[l]; m->wd[l] = m->bd[l];
+  }
+  const int half = c->hd / 2;
+  m->rope_cos = (float*)malloc((size_t)c->max_pos * half * sizeof(float));
+  m->rope_sin = (float*)malloc((size_t)c->max_pos * half * sizeof(float));
+  ref_rope_table(c->max_pos, c->hd, c->theta, m->rope_cos, m->rope_sin);
+  return m;
+}
+
+static uint16_t* dequant_copy(const uint16_t* w, int64_t N, int64_t K) {
+  int8_t* codes = (int8_t*)malloc((size_t)N * K);
+  uint16_t* sc = (uint16_t*)malloc((size_t)N * (K / 128) * 2);
+  ref_quantize_groups(w, N, K, 128, 4, codes, NULL, sc);
+  uint16_t* out = (uint16_t*)malloc((size_t)N * K * 2);
+  ref_dequant_w4(codes, sc, N, K, 128, out);
+  free(codes);
+  free(sc);
+  return out;
+}
+
+/* Per-layer precision dispatch (toy_model.cpp:153): bits 16 or 4. */
+void ref_model_set_precision(ref_model* m, int layer, int bits) {
+  const ref_cfg* c = &m->c;
+  const int64_t qkv_n = (int64_t)(c->H + 2 * c->KVH) * c->hd;
+  if (m->tag[layer] == 4) {
+    free(m->wqkv[layer]); free(m->wo[layer]); free(m->wgu[layer]); free(m->wd[layer]);
+  }
+  if (bits == 4) {
+    m->wqkv[layer] = dequant_copy(m->bqkv[layer], qkv_n, c->d);
+    m->wo[layer] = dequant_copy(m->bo[layer], c->d, (int64_t)c->H * c->hd);
+    m->wgu[layer] = dequant_copy(m->bgu[layer], (int64_t)2 * c->ffn, c->d);
+    m->wd[layer] = dequant_copy(m->bd[layer], c->d, c->ffn);
+    m->tag[layer] = 4;
+  } else {
+    m->wqkv[layer] = m->bqkv[layer]; m->wo[layer] = m->bo[layer];
+    m->wgu[layer] = m->bgu[layer]; m->wd[layer] = m->bd[layer];
+    m->tag[layer] = 0;
+  }
+}
+
+/* Accessors so the harness can hand the exact same weights to the GPU. */
+uint16_t* ref_model_tensor(ref_model* m, int layer, int which) {
+  if (layer < 0) {
+    if (which == T_EMBED) return m->embed;
+    if (which == T_NORMF) return m->normf;
+    return m->lm_head;
+  }
+  switch (which) {
+    case W_NORM1: return m->norm1[layer];
+    case W_QKV: return m->bqkv[layer];
+    case W_O: return m->bo[layer];
+    case W_NORM2: return m->norm2[layer];
+    case W_GU: return m->bgu[layer];
+    default: return m->bd[layer];
+  }
+}
+
+void ref_model_destroy(ref_model* m) {
+  if (!m) return;
+  for (int l = 0; l < m->c.L; ++l) {
+    if (m->tag[l] == 4) ref_model_set_precision(m, l, 16);
+    free(m->norm1[l]); free(m->norm2[l]);
+    free(m->bqkv[l]); free(m->bo[l]); free(m->bgu[l]); free(m->bd[l]);
+  }
+  free(m->norm1); free(m->norm2); free(m->wqkv); free(m->wo); free(m->wgu); free(m->wd);
+  free(m->bqkv); free(m->bo); free(m->bgu); free(m->bd); free(m->tag);
+  free(m->embed); free(m->normf); free(m->lm_head); free(m->rope_cos); free(m->rope_sin);
+  free(m);
+}
+
+ref_seq* ref_seq_create(const ref_model* m, int cap) {
+  ref_seq* s = (ref_seq*)calloc(1, sizeof(ref_seq));
+  s->cap = cap;
+  s->k = (uint16_t**)calloc(m->c.L, sizeof(uint16_t*));
+  s->v = (uint16_t**)calloc(m->c.L, sizeof(uint16_t*));
+  const size_t per = (size_t)cap * m->c.KVH * m->c.hd;
+  for (int l = 0; l < m->c.L; ++l) {
+    s->k[l] = (uint16_t*)calloc(per, 2);
+    s->v[l] = (uint16_t*)calloc(per, 2);
+  }
+  return s;
+}
+void ref_seq_destroy(const ref_model* m, ref_seq* s) {
+  if (!s) return;
+  for (int l = 0; l < m->c.L; ++l) { free(s->k[l]); free(s->v[l]); }
+  free(s->k); free(s->v); free(s);
+}
+int ref_seq_len(const ref_seq* s) { return s->len; }
+/* Direct KV access for kernel-level tests (positions [0,len) of one layer). */
+uint16_t* ref_seq_k(ref_seq* s, int layer) { return s->k[layer]; }
+uint16_t* ref_seq_v(ref_seq* s, int layer) { return s->v[layer]; }
+
+/* y[b][n] = sum_k W[n][k] * x[b][k]   (bf16 inputs, fp64 accumulation, fp32 out) */
+void ref_gemm_bf16(const uint16_t* W, const uint16_t* X, int64_t B, int64_t N, int64_t K,
+                   float* Y) {
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    const uint16_t* wr = W + n * K;
+    for (int64_t b = 0; b < B; ++b) {
+      const uint16_t* xr = X + b * K;
+      double acc = 0.0;
+      for (int64_t k = 0; k < K; ++k) acc += (double)bf2f(wr[k]) * (double)bf2f(xr[k]);
+      Y[b * N + n] = (float)acc;
+    }
+  }
+}
+
+/* xn = bf16((h * inv_rms) * w), inv_rms = 1/sqrt(mean(h^2) + eps) */
+void ref_rmsnorm(const float* h, const uint16_t* w, int64_t B, int64_t d, float eps,
+                 uint16_t* out) {
+  for (int64_t b = 0; b < B; ++b) {
+    double ss = 0.0;
+    for (int64_t i = 0; i < d; ++i) ss += (double)h[b * d + i] * (double)h[b * d + i];
+    const float r = 1.0f / sqrtf((float)(ss / (double)d) + eps);
+    for (int64_t i = 0; i < d; ++i) out[b * d + i] = f2bf((h[b * d + i] * r) * bf2f(w[i]));
+  }
+}
+
+static void rope_inplace(float* x, int hd, const float* cs, const float* sn) {
+  const int half = hd / 2;
+  for (int i = 0; i < half; ++i) {
+    const float x0 = x[i], x1 = x[i + half];
+    x[i] = x0 * cs[i] - x1 * sn[i];
+    x[i + half] = x1 * cs[i] + x0 * sn[i];
+  }
+}
+
+/* One attention query (all heads) against seq positions [0, ctx). */
+void ref_attention(const float* q /*[H][hd]*/, const uint16_t* kc, const uint16_t* vc,
+                   int ctx, int H, int KVH, int hd, uint16_t* out /*[H][hd] bf16*/,
+                   float* out_f32) {
+  const int G = H / KVH;
+  const float scale = 1.0f / sqrtf((float)hd);
+  float* s = (float*)malloc((size_t)ctx * sizeof(float));
+  for (int h = 0; h < H; ++h) {
+    const int kh = h / G;
+    float mx = -INFINITY;
+    for (int t = 0; t < ctx; ++t) {
+      double acc = 0.0;
+      const uint16_t* kr = kc + ((int64_t)t * KVH + kh) * hd;
+      for (int i = 0; i < hd; ++i) acc += (double)q[h * hd + i] * (double)bf2f(kr[i]);
+      s[t] = (float)acc * scale;
+      if (s[t] > mx) mx = s[t];
+    }
+    double l = 0.0;
+    for (int t = 0; t < ctx; ++t) {
+      s[t] = expf(s[t] - mx);
+      l += s[t];
+    }
+    for (int i = 0; i < hd; ++i) {
+      double acc = 0.0;
+      for (int t = 0; t < ctx; ++t)
+        acc += (double)s[t] * (double)bf2f(vc[((int64_t)t * KVH + kh) * hd + i]);
+      const float o = (float)(acc / l);
+      if (out) out[h * hd + i] = f2bf(o);
+      if (out_f32) out_f32[h * hd + i] = o;
+    }
+  }
+  free(s);
+}
+
+static inline float silu(float x) { return x / (1.0f + expf(-x)); }
+
+/* One decode token for each of B sequences: tokens[b] enters at position
+ * seqs[b]->len; its K/V are appended; logits[b][V] (may be NULL) and
+ * next[b] = argmax are returned.  This is also the prefill math: a prefill of
+ * n tokens is n such positions (causal attention makes them identical). */
+void ref_forward(ref_model* m, ref_seq** seqs, const int32_t* tokens, int B, float* logits,
+                 int32_t* next) {
+  const ref_cfg* c = &m->c;
+  const int d = c->d, hd = c->hd, H = c->H, KVH = c->KVH, half = hd / 2;
+  const int qkv_n = (H + 2 * KVH) * hd;
+  float* h = (float*)malloc((size_t)B * d * sizeof(float));
+  uint16_t* xn = (uint16_t*)malloc((size_t)B * (c->ffn > d ? c->ffn : d) * 2);
+  float* y = (float*)malloc((size_t)B * 2 * (c->ffn > qkv_n ? c->ffn : qkv_n) * sizeof(float) +
+                            (size_t)B * c->V * sizeof(float));
+  uint16_t* att = (uint16_t*)malloc((size_t)B * H * hd * 2);
+  float* q = (float*)malloc((size_t)H * hd * sizeof(float));
+  for (int b = 0; b < B; ++b)
+    for (int i = 0; i < d; ++i) h[(int64_t)b * d + i] = bf2f(m->embed[(int64_t)tokens[b] * d + i]);
+
+  for (int l = 0; l < c->L; ++l) {
+    ref_rmsnorm(h, m->norm1[l], B, d, c->eps, xn);
+    ref_gemm_bf16(m->wqkv[l], xn, B, qkv_n, d, y);
+    for (int b = 0; b < B; ++b) {
+      ref_seq* s = seqs[b];
+      const int pos = s->len;
+      float* row = y + (int64_t)b * qkv_n;
+      const float* cs = m->rope_cos + (int64_t)pos * half;
+      const float* sn = m->rope_sin + (int64_t)pos * half;
+      for (int hh = 0; hh < H; ++hh) rope_inplace(row + hh * hd, hd, cs, sn);
+      for (int hh = 0; hh < KVH; ++hh) rope_inplace(row + (H + hh) * hd, hd, cs, sn);
+      for (int hh = 0; hh < KVH; ++hh)
+        for (int i = 0; i < hd; ++i) {
+          s->k[l][((int64_t)pos * KVH + hh) * hd + i] = f2bf(row[(H + hh) * hd + i]);
+          s->v[l][((int64_t)pos * KVH + hh) * hd + i] = f2bf(row[(H + KVH + hh) * hd + i]);
+        }
+      memcpy(q, row, (size_t)H * hd * sizeof(float));
+      ref_attention(q, s->k[l], s->v[l], pos + 1, H, KVH, hd, att + (int64_t)b * H * hd, NULL);
+    }
+    ref_gemm_bf16(m->wo[l], att, B, d, (int64_t)H * hd, y);
+    for (int64_t i = 0; i < (int64_t)B * d; ++i) h[i] = h[i] + y[i];
+    ref_rmsnorm(h, m->norm2[l], B, d, c->eps, xn);
+    ref_gemm_bf16(m->wgu[l], xn, B, 2 * c->ffn, d, y);
+    for (int b = 0; b < B; ++b)
+      for (int j = 0; j < c->ffn; ++j) {
+        const float g = y[(int64_t)b * 2 * c->ffn + j];
+        const float u = y[(int64_t)b * 2 * c->ffn + c->ffn + j];
+        xn[(int64_t)b * c->ffn + j] = f2bf(silu(g) * u);
+      }
+    ref_gemm_bf16(m->wd[l], xn, B, d, c->ffn, y);
+    for (int64_t i = 0; i < (int64_t)B * d; ++i) h[i] = h[i] + y[i];
+  }
+  for (int b = 0; b < B; ++b) seqs[b]->len += 1;
+  ref_rmsnorm(h, m->normf, B, d, c->eps, xn);
+  float* lg = logits ? logits : y;
+  ref_gemm_bf16(m->lm_head, xn, B, c->V, d, lg);
+  for (int b = 0; b < B; ++b) {
+    const float* r = lg + (int64_t)b * c->V;
+    int best = 0;
+    for (int v = 1; v < c->V; ++v)
+      if (r[v] > r[best]) best = v;
+    if (next) next[b] = best;
+  }
+  free(h); free(xn); free(y); free(att); free(q);
+}
+
+/* Prefill helper: runs n positions of one sequence; returns argmax after the
+ * last one (and its logits if requested). */
+int32_t ref_prefill(ref_model* m, ref_seq* s, const int32_t* tokens, int n, float* logits) {
+  int32_t nxt = -1;
+  for (int i = 0; i < n; ++i) ref_forward(m, &s, tokens + i, 1, (i == n - 1) ? logits : NULL, &nxt);
+  return nxt;
+}
+
+int ref_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

@@ -1,0 +1,366 @@
+// elementwise.cu -- the row-wise kernels around the GEMMs and attention:
+// embedding + RMSNorm, QKV split-K reduction + RoPE + paged KV append,
+// residual add + RMSNorm, SiLU*up, logits reduction + greedy argmax, and the
+// offline weight tools (synthetic generator, BF16 tile packer, g128 W4
+// quantiser/packer).  Each output is written directly in the layout its
+// consumer wants (packed activation images for the next GEMM, KV pages for
+// attention) so no separate layout pass runs per step.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace ms {
+
+template <int kThreads>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// ------------------------------------------------ embedding + RMSNorm (layer 0)
+__global__ void __launch_bounds__(256) embed_norm_kernel(const uint16_t* __restrict__ embed,
+                                                         const int32_t* __restrict__ tokens,
+                                                         const int32_t* __restrict__ hist,
+                                                         const int32_t* __restrict__ slot,
+                                                         const int32_t* __restrict__ pos, int hist_stride, int d,
+                                                         const uint16_t* __restrict__ w, float eps,
+                                                         float* __restrict__ h, uint16_t* __restrict__ x, int TM) {
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const int tok = tokens ? tokens[m] : hist[(size_t)slot[m] * hist_stride + pos[m]];
+  const uint16_t* e = embed + (size_t)tok * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += 256) {
+    const float v = bf2f(e[i]);
+    h[(size_t)m * d + i] = v;
+    ss += v * v;
+  }
+  ss = block_sum<256>(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int i = threadIdx.x; i < d; i += 256) {
+    const float v = h[(size_t)m * d + i];
+    x[act_off(m, i, d, TM)] = f2bf((v * r) * bf2f(w[i]));
+  }
+}
+
+cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, const int32_t* hist,
+                              const int32_t* slot, const int32_t* pos, int hist_stride, int M, int d,
+                              const uint16_t* norm_w, float eps, float* h, uint16_t* x_packed, int TM,
+                              cudaStream_t s) {
+  embed_norm_kernel<<<M, 256, 0, s>>>(embed, tokens, hist, slot, pos, hist_stride, d, norm_w, eps, h, x_packed,
+                                      TM);
+  return cudaGetLastError();
+}
+
+// --------------------------------- QKV: split-K sum, RoPE, q out, K/V -> KV pages
+__global__ void __launch_bounds__(256) qkv_post_kernel(const float* __restrict__ part, int splits, int M, int H,
+                                                       int KVH, int hd, const float* __restrict__ rc,
+                                                       const float* __restrict__ rs, const int32_t* __restrict__ pos,
+                                                       KvGeom kv, int layer, const int32_t* __restrict__ pages,
+                                                       const int32_t* __restrict__ page_row, int page_stride,
+                                                       float* __restrict__ q_out) {
+  const int m = blockIdx.x;
+  const int N = (H + 2 * KVH) * hd;
+  const int half = hd / 2;
+  const int p = pos[m];
+  const int prow = page_row ? page_row[m] : m;
+  const int32_t page = pages[(size_t)prow * page_stride + p / kv.block_tokens];
+  const int slot = p % kv.block_tokens;
+  char* kvbase = kv.arena + (int64_t)page * kv.page_bytes + kv.layer_off(layer);
+  const float* cs = rc + (size_t)p * half;
+  const float* sn = rs + (size_t)p * half;
+  const size_t stride = (size_t)M * N;
+  const float* prow_part = part + (size_t)m * N;
+  // rotated pairs: q heads and k heads
+  const int npairs = (H + KVH) * half;
+  for (int idx = threadIdx.x; idx < npairs; idx += 256) {
+    const int hs = idx / half, i = idx - hs * half;
+    const int c0 = hs * hd + i, c1 = c0 + half;
+    float x0 = 0.f, x1 = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      x0 += prow_part[s * stride + c0];
+      x1 += prow_part[s * stride + c1];
+    }
+    const float y0 = x0 * cs[i] - x1 * sn[i];
+    const float y1 = x1 * cs[i] + x0 * sn[i];
+    if (hs < H) {
+      q_out[((size_t)m * H + hs) * hd + i] = y0;
+      q_out[((size_t)m * H + hs) * hd + i + half] = y1;
+    } else {
+      uint16_t* kp = reinterpret_cast<uint16_t*>(kvbase + (int64_t)(hs - H) * 2 * kv.head_bytes()) + slot * hd;
+      kp[i] = f2bf(y0);
+      kp[i + half] = f2bf(y1);
+    }
+  }
+  for (int idx = threadIdx.x; idx < KVH * hd; idx += 256) {
+    const int kh = idx / hd, dim = idx - kh * hd;
+    const int c = (H + KVH) * hd + idx;
+    float v = 0.f;
+    for (int s = 0; s < splits; ++s) v += prow_part[s * stride + c];
+    uint16_t* vp = reinterpret_cast<uint16_t*>(kvbase + (int64_t)kh * 2 * kv.head_bytes() + kv.head_bytes()) +
+                   slot * hd;
+    vp[dim] = f2bf(v);
+  }
+}
+
+cudaError_t qkv_post_launch(const float* part, int splits, int M, int H, int KVH, int hd, const float* rope_cos,
+                            const float* rope_sin, const int32_t* pos, const KvGeom& kv, int layer,
+                            const int32_t* pages, const int32_t* page_row, int page_stride, float* q_out,
+                            cudaStream_t s) {
+  qkv_post_kernel<<<M, 256, 0, s>>>(part, splits, M, H, KVH, hd, rope_cos, rope_sin, pos, kv, layer, pages,
+                                    page_row, page_stride, q_out);
+  return cudaGetLastError();
+}
+
+// ----------------------------------- residual add (split-K sum) + RMSNorm + pack
+__global__ void __launch_bounds__(256) residual_norm_kernel(const float* __restrict__ part, int splits, int M,
+                                                            int d, float* __restrict__ h,
+                                                            const uint16_t* __restrict__ w, float eps,
+                                                            uint16_t* __restrict__ x, int TM, int norm_row_begin) {
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const size_t stride = (size_t)M * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += 256) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += part[s * stride + (size_t)m * d + i];
+    const float v = h[(size_t)m * d + i] + acc;
+    h[(size_t)m * d + i] = v;
+    ss += v * v;
+  }
+  if (w == nullptr || m < norm_row_begin) return;  // uniform per block
+  ss = block_sum<256>(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  const int mo = m - norm_row_begin;
+  for (int i = threadIdx.x; i < d; i += 256) {
+    const float v = h[(size_t)m * d + i];
+    x[act_off(mo, i, d, TM)] = f2bf((v * r) * bf2f(w[i]));
+  }
+}
+
+cudaError_t residual_norm_launch(const float* part, int splits, int M, int d, float* h, const uint16_t* norm_w,
+                                 float eps, uint16_t* x_packed, int TM, cudaStream_t s) {
+  residual_norm_kernel<<<M, 256, 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t residual_norm_rows_launch(const float* part, int splits, int M, int d, float* h,
+                                      const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
+                                      int norm_row_begin, cudaStream_t s) {
+  residual_norm_kernel<<<M, 256, 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM, norm_row_begin);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- SiLU(gate)*up
+__global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int M, int ffn,
+                                uint16_t* __restrict__ x, int TM) {
+  const size_t total = (size_t)M * ffn;
+  const size_t stride = (size_t)M * 2 * ffn;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(idx / ffn), j = (int)(idx - (size_t)m * ffn);
+    float g = 0.f, u = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      g += part[s * stride + (size_t)m * 2 * ffn + j];
+      u += part[s * stride + (size_t)m * 2 * ffn + ffn + j];
+    }
+    const float a = (g / (1.0f + expf(-g))) * u;
+    x[act_off(m, j, ffn, TM)] = f2bf(a);
+  }
+}
+
+cudaError_t silu_mul_launch(const float* part, int splits, int M, int ffn, uint16_t* x_packed, int TM,
+                            cudaStream_t s) {
+  const size_t total = (size_t)M * ffn;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  silu_mul_kernel<<<blocks, 256, 0, s>>>(part, splits, M, ffn, x_packed, TM);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------ logits + greedy argmax
+__global__ void __launch_bounds__(512) argmax_kernel(const float* __restrict__ part, int splits, int M, int V,
+                                                     float* __restrict__ logits_out, int32_t* __restrict__ next_out,
+                                                     int32_t* __restrict__ hist, const int32_t* __restrict__ slot,
+                                                     const int32_t* __restrict__ pos, int hist_stride) {
+  __shared__ float bv[16];
+  __shared__ int bi[16];
+  const int m = blockIdx.x;
+  const size_t stride = (size_t)M * V;
+  float best = -INFINITY;
+  int besti = 0x7fffffff;
+  for (int v = threadIdx.x; v < V; v += 512) {
+    float x = 0.f;
+    for (int s = 0; s < splits; ++s) x += part[s * stride + (size_t)m * V + v];
+    if (logits_out) logits_out[(size_t)m * V + v] = x;
+    if (x > best || (x == best && v < besti)) {
+      best = x;
+      besti = v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+    if (ov > best || (ov == best && oi < besti)) {
+      best = ov;
+      besti = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    bv[w] = best;
+    bi[w] = besti;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 16; ++i)
+      if (bv[i] > best || (bv[i] == best && bi[i] < besti)) {
+        best = bv[i];
+        besti = bi[i];
+      }
+    if (next_out) next_out[m] = besti;
+    if (hist) hist[(size_t)slot[m] * hist_stride + pos[m] + 1] = besti;
+  }
+}
+
+cudaError_t argmax_launch(const float* part, int splits, int M, int V, float* logits_out, int32_t* next_out,
+                          int32_t* hist, const int32_t* slot, const int32_t* pos, int hist_stride,
+                          cudaStream_t s) {
+  argmax_kernel<<<M, 512, 0, s>>>(part, splits, M, V, logits_out, next_out, hist, slot, pos, hist_stride);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ synthetic weight generator
+// Bit-identical to oracle/ref_llama.c gen_one(): splitmix64 counter RNG,
+// fp64 (explicitly rounded, no FMA contraction) -> fp32 -> bf16 RNE.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void gen_weight_kernel(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset,
+                                  uint16_t* __restrict__ out) {
+  const uint64_t key = seed ^ (tensor * 0xD1B54A32D192ED03ull);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = splitmix64(key + (uint64_t)i);
+    const double u = __dmul_rn((double)(r >> 11), 0x1.0p-53);
+    double w = __dadd_rn(__dmul_rn(2.0, u), -1.0);
+    w = __dmul_rn(w, scale);
+    w = __dadd_rn(w, offset);
+    out[i] = f2bf(__double2float_rn(w));
+  }
+}
+cudaError_t gen_weight_launch(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset,
+                              uint16_t* out, cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  gen_weight_kernel<<<(int)blocks, 256, 0, s>>>(seed, tensor, n, scale, offset, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ BF16 tile packer
+__global__ void pack_bf16_kernel(const uint16_t* __restrict__ w, int N, int K, uint16_t* __restrict__ out) {
+  const int64_t total = (int64_t)N * K;
+  const int KB = K / 64;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(idx / K), k = (int)(idx - (int64_t)n * K);
+    const int nt = n >> 7, rr = n & 127, g = rr >> 3, r = rr & 7;
+    const int kb = k >> 6, kk = k & 63, c = kk >> 3, e = kk & 7;
+    const int64_t chunk = (int64_t)nt * KB + kb;
+    out[chunk * 8192 + ((g * 8 + c) * 8 + r) * 8 + e] = w[idx];
+  }
+}
+cudaError_t pack_bf16_launch(const uint16_t* w, int N, int K, uint16_t* out, cudaStream_t s) {
+  pack_bf16_kernel<<<148 * 16, 256, 0, s>>>(w, N, K, out);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------- g128 W4 quantiser + chunk packer
+// One thread per (row, group).  Reference semantics (toy_model.cpp:40-60):
+// scale = max|w| / 7 in fp64, code = round(w / scale) (half away from zero),
+// all-zero group -> scale 1, codes 0.  Stored: nibble (code + 8), bf16 scale.
+__global__ void quant_w4_kernel(const uint16_t* __restrict__ w, int N, int K, uint8_t* __restrict__ out,
+                                int8_t* __restrict__ codes_out) {
+  const int G = K / 128;
+  const int64_t total = (int64_t)N * G;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(idx / G), g = (int)(idx - (int64_t)n * G);
+    const uint16_t* src = w + (size_t)n * K + (size_t)g * 128;
+    double mx = 0.0;
+    for (int i = 0; i < 128; ++i) mx = fmax(mx, fabs((double)bf2f(src[i])));
+    const double scale = mx == 0.0 ? 1.0 : __ddiv_rn(mx, 7.0);
+    uint8_t* chunk = out + ((int64_t)(n >> 7) * G + g) * 8448;
+    const int row = n & 127;
+    for (int j = 0; j < 4; ++j) {
+      uint32_t words[4];
+      for (int q = 0; q < 4; ++q) {
+        uint32_t v = 0;
+        for (int e = 0; e < 8; ++e) {
+          const int kk = j * 32 + q * 8 + e;
+          const int code = mx == 0.0 ? 0 : (int)round(__ddiv_rn((double)bf2f(src[kk]), scale));
+          if (codes_out) codes_out[(size_t)n * K + (size_t)g * 128 + kk] = (int8_t)code;
+          v |= ((uint32_t)(code + 8) & 0xFu) << (4 * e);
+        }
+        words[q] = v;
+      }
+      *reinterpret_cast<uint4*>(chunk + (j * 128 + row) * 16) = make_uint4(words[0], words[1], words[2], words[3]);
+    }
+    *reinterpret_cast<uint16_t*>(chunk + 8192 + row * 2) = f2bf(__double2float_rn(scale));
+  }
+}
+cudaError_t quant_w4_launch(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, cudaStream_t s) {
+  const int64_t total = (int64_t)N * (K / 128);
+  int64_t blocks = (total + 127) / 128;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  quant_w4_kernel<<<(int)blocks, 128, 0, s>>>(w, N, K, out, codes_out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ activation packer (tests / e2e)
+__global__ void pack_act_kernel(const uint16_t* __restrict__ x, int M, int K, int TM, uint16_t* __restrict__ out) {
+  const int64_t total = (int64_t)M * K;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(idx / K), k = (int)(idx - (int64_t)m * K);
+    out[act_off(m, k, K, TM)] = x[idx];
+  }
+}
+cudaError_t pack_act_launch(const uint16_t* x, int M, int K, int TM, uint16_t* out, cudaStream_t s) {
+  pack_act_kernel<<<148 * 8, 256, 0, s>>>(x, M, K, TM, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------- synthetic KV fill (bench "prefilled" context)
+__global__ void fill_kv_kernel(KvGeom kv, const int32_t* __restrict__ page_list, int n_pages, uint64_t seed) {
+  const int64_t per_page = kv.page_bytes / 2;
+  const int64_t total = per_page * n_pages;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pi = idx / per_page, off = idx - pi * per_page;
+    const uint64_t r = splitmix64(seed + (uint64_t)idx);
+    const float u = (float)(r >> 40) * (1.0f / 16777216.0f) * 2.0f - 1.0f;
+    reinterpret_cast<uint16_t*>(kv.arena + (int64_t)page_list[pi] * kv.page_bytes)[off] = f2bf(u);
+  }
+}
+cudaError_t fill_kv_launch(const KvGeom& kv, const int32_t* page_list, int n_pages, uint64_t seed, cudaStream_t s) {
+  fill_kv_kernel<<<148 * 32, 256, 0, s>>>(kv, page_list, n_pages, seed);
+  return cudaGetLastError();
+}
+
+}  // namespace ms

@@ -1,0 +1,79 @@
+// kernels.h -- internal launch interface between the runtime (runtime.cu) and
+// the CUDA kernels.  Not part of the public C ABI (include/morphserve.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ms {
+
+// A weight matrix as the GEMM sees it: chunk c of the matrix lives in page
+// (first_chunk + c) / chunks_per_page of its variant image.
+struct GemmWeights {
+  const uint64_t* pages;  // device array of page base addresses
+  int64_t first_chunk;
+  int64_t chunks_per_page;
+  int N, K;
+};
+
+cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, int splits, float* out,
+                        cudaStream_t stream);
+int gemm_pick_splits(int n_tiles, int m_tiles, int nk, int num_sms, int ctas_per_sm);
+int gemm_ctas_per_sm(bool w4, int TM);
+
+// Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
+// every layer): [layer][kv_head][K|V][token][head_dim] bf16.
+struct KvGeom {
+  char* arena;
+  int64_t page_bytes;
+  int layers, kv_heads, head_dim, block_tokens;
+  __host__ __device__ int64_t head_bytes() const { return (int64_t)block_tokens * head_dim * 2; }
+  __host__ __device__ int64_t layer_off(int l) const { return (int64_t)l * kv_heads * 2 * head_bytes(); }
+};
+
+struct AttnArgs {
+  const float* q;           // [rows][H][hd] fp32, RoPE applied
+  KvGeom kv;
+  int layer;
+  const int32_t* pages;     // page index table, row r uses pages + page_row[r] * page_stride
+  const int32_t* page_row;  // nullptr => identity
+  int page_stride;
+  const int32_t* ctx_len;   // [rows] tokens attended (current token included)
+  int rows, H, KVH;
+  float scale_log2;         // log2(e) / sqrt(hd)
+  int splits;               // split-KV slices (1 => write the final output directly)
+  float* part_o;            // [splits][rows][H][hd] (splits > 1)
+  float* part_ml;           // [splits][rows][H][2]
+  uint16_t* out;            // bf16 output
+  int out_packed;           // 1: packed activation image (K = H*hd, TM), 0: row-major [rows][H*hd]
+  int TM;
+};
+cudaError_t attn_decode_launch(const AttnArgs& a, cudaStream_t stream);
+
+// elementwise / row kernels (elementwise.cu)
+cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, const int32_t* hist,
+                              const int32_t* slot, const int32_t* pos, int hist_stride, int M, int d,
+                              const uint16_t* norm_w, float eps, float* h, uint16_t* x_packed, int TM,
+                              cudaStream_t s);
+cudaError_t qkv_post_launch(const float* part, int splits, int M, int H, int KVH, int hd, const float* rope_cos,
+                            const float* rope_sin, const int32_t* pos, const KvGeom& kv, int layer,
+                            const int32_t* pages, const int32_t* page_row, int page_stride, float* q_out,
+                            cudaStream_t s);
+cudaError_t residual_norm_launch(const float* part, int splits, int M, int d, float* h, const uint16_t* norm_w,
+                                 float eps, uint16_t* x_packed, int TM, cudaStream_t s);
+cudaError_t residual_norm_rows_launch(const float* part, int splits, int M, int d, float* h,
+                                      const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
+                                      int norm_row_begin, cudaStream_t s);
+cudaError_t silu_mul_launch(const float* part, int splits, int M, int ffn, uint16_t* x_packed, int TM,
+                            cudaStream_t s);
+cudaError_t argmax_launch(const float* part, int splits, int M, int V, float* logits_out, int32_t* next_out,
+                          int32_t* hist, const int32_t* slot, const int32_t* pos, int hist_stride,
+                          cudaStream_t s);
+cudaError_t gen_weight_launch(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset,
+                              uint16_t* out, cudaStream_t s);
+cudaError_t pack_bf16_launch(const uint16_t* w, int N, int K, uint16_t* out, cudaStream_t s);
+cudaError_t quant_w4_launch(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, cudaStream_t s);
+cudaError_t pack_act_launch(const uint16_t* x, int M, int K, int TM, uint16_t* out, cudaStream_t s);
+cudaError_t fill_kv_launch(const KvGeom& kv, const int32_t* page_list, int n_pages, uint64_t seed,
+                           cudaStream_t s);
+
+}  // namespace ms

@@ -1,0 +1,1041 @@
+// runtime.cu -- the device context behind include/morphserve.h.
+//
+// Owns: the page arena (KV blocks and layer weight images share one pool of
+// page_bytes pages), the per-layer dispatch table (committed precision +
+// double-buffered device page tables), the pinned-host variant store the
+// LayerSwapper uploads from, the compute/copy streams, the token history, and
+// the per-step driver that strings the kernels together.
+//
+// Reference seams replaced (see include/morphserve.h for the per-function map):
+//   CostModel::decode_step_ms        proj/src/sim_config.cpp:23-27  -> ms_decode_step
+//   tokens * prefill_ms_per_token    proj/src/engine.cpp:477-478    -> ms_prefill
+//   CostModel::swap_duration_ms      proj/src/sim_config.cpp:29-33  -> ms_swap_begin (+ copy stream)
+//   MorphState::complete_swap        proj/src/engine.cpp:30-38      -> ms_swap_commit (pointer flip)
+//   KvBlockPool::attach/detach       proj/src/kv_pool.cpp:77-100    -> ms_kv_attach / ms_kv_detach
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/morphserve.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct MsError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw MsError{code, msg}; }
+
+#define CK(x)                                                                                      \
+  do {                                                                                             \
+    cudaError_t e_ = (x);                                                                          \
+    if (e_ != cudaSuccess) fail(MS_ERUNTIME, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MS_OK;
+  } catch (const MsError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MS_ERUNTIME;
+  }
+}
+
+constexpr int kMats = 4;  // qkv, o, gate_up, down
+constexpr int kRing = 3;  // staging ring depth (host may run this many steps ahead)
+
+struct MatShape {
+  int N, K;
+};
+
+struct ImageGeom {
+  int bits = 16;
+  int64_t chunk_bytes = 0, cpp = 0, total_chunks = 0, pages = 0;
+  int64_t first_chunk[kMats] = {0, 0, 0, 0};
+  MatShape mat[kMats];
+};
+
+int64_t page_bytes_of(const ms_model_desc& d) {
+  return (int64_t)d.block_tokens * d.num_layers * d.num_kv_heads * 2 * d.head_dim * 2;
+}
+
+void validate_desc(const ms_model_desc& d) {
+  auto bad = [](const char* m) { fail(MS_EVALIDATION, std::string("model desc: ") + m); };
+  if (d.num_layers < 1 || d.hidden < 128 || d.num_heads < 1 || d.num_kv_heads < 1) bad("bad sizes");
+  if (d.num_heads % d.num_kv_heads) bad("num_heads must be a multiple of num_kv_heads");
+  const int G = d.num_heads / d.num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) bad("GQA group must be 1, 2, 4 or 8");
+  if (d.head_dim != 64 && d.head_dim != 128) bad("head_dim must be 64 or 128");
+  if (d.block_tokens != 16) bad("block_tokens must be 16");
+  if (d.hidden % 128 || d.ffn % 128 || d.vocab % 128 || (d.num_heads * d.head_dim) % 128 ||
+      ((d.num_heads + 2 * d.num_kv_heads) * d.head_dim) % 128)
+    bad("hidden, ffn, vocab and projection widths must be multiples of 128");
+  if (d.max_batch < 1 || d.max_batch > 4096 || d.max_prefill_tokens < 1 || d.max_pos < 1) bad("bad capacities");
+  if (d.arena_pages < 1) bad("arena_pages must be >= 1");
+}
+
+ImageGeom image_geom(const ms_model_desc& d, int bits) {
+  ImageGeom g;
+  g.bits = bits;
+  g.mat[0] = {(d.num_heads + 2 * d.num_kv_heads) * d.head_dim, d.hidden};
+  g.mat[1] = {d.hidden, d.num_heads * d.head_dim};
+  g.mat[2] = {2 * d.ffn, d.hidden};
+  g.mat[3] = {d.hidden, d.ffn};
+  g.chunk_bytes = bits == 16 ? 16384 : 8448;
+  const int64_t pb = page_bytes_of(d);
+  g.cpp = pb / g.chunk_bytes;
+  if (g.cpp < 1) fail(MS_EVALIDATION, "page smaller than one weight chunk");
+  int64_t c = 0;
+  for (int i = 0; i < kMats; ++i) {
+    g.first_chunk[i] = c;
+    c += (int64_t)(g.mat[i].N / 128) * (g.mat[i].K / (bits == 16 ? 64 : 128));
+  }
+  g.total_chunks = c;
+  g.pages = (c + g.cpp - 1) / g.cpp;
+  return g;
+}
+
+struct FreePage {
+  int32_t page;
+  cudaEvent_t fence;  // compute-stream event that must complete before reuse (may be null)
+};
+
+struct Layer {
+  int bits = 16;
+  int slot = 0;
+  uint64_t* d_table[2] = {nullptr, nullptr};
+  uint64_t* h_table[2] = {nullptr, nullptr};  // pinned staging
+  std::vector<int32_t> pages;
+  cudaEvent_t last_release = nullptr;
+  // in-flight swap
+  bool in_flight = false;
+  int to_bits = 0;
+  uint64_t ticket = 0;
+  std::vector<int32_t> new_pages;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  // pinned host variant store
+  uint8_t* host_img[2] = {nullptr, nullptr};  // [0] bf16, [1] w4
+};
+
+struct Staging {  // one slot of the per-step H2D ring
+  int32_t* h = nullptr;   // pinned
+  int32_t* d = nullptr;   // device
+  size_t words = 0;
+  cudaEvent_t used = nullptr;
+  bool armed = false;
+};
+
+}  // namespace
+
+struct ms_ctx {
+  ms_model_desc desc{};
+  int device = 0;
+  int num_sms = 148;
+  int64_t page_bytes = 0;
+  ImageGeom geom16, geom4;
+  cudaStream_t compute = nullptr, copy = nullptr;
+  char* arena = nullptr;
+  ms::KvGeom kv{};
+  std::vector<FreePage> free_pages;
+  std::vector<cudaEvent_t> events;  // all fence events (destroyed at the end)
+  std::vector<int32_t> id_page;     // logical KV block id -> page (-1 unmapped)
+  std::vector<Layer> layers;
+  uint64_t next_ticket = 1;
+
+  // resident non-morphable weights
+  uint16_t* embed = nullptr;     // [V][d] row-major
+  uint16_t* normf = nullptr;     // [d]
+  uint16_t* norms = nullptr;     // [L][2][d]
+  uint16_t* lm_packed = nullptr; // packed [V/128][d/64] chunks
+  uint64_t* lm_table = nullptr;  // 1-entry page table
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  bool weights_ready = false;
+  // raw uploads awaiting finalize
+  std::vector<uint16_t*> raw;  // [L*6 + 3]
+
+  // activations
+  int max_rows = 0;
+  float* h = nullptr;
+  uint16_t* x = nullptr;
+  float* part = nullptr;
+  size_t part_elems = 0;
+  float* q = nullptr;
+  float* attn_ws = nullptr;
+  size_t attn_ws_elems = 0;
+  int32_t* next = nullptr;
+  float* logits = nullptr;
+  int max_blocks = 0;
+  Staging ring[kRing];
+  int ring_i = 0;
+  int32_t* h_next = nullptr;   // pinned
+  float* h_logits = nullptr;   // pinned
+  cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
+
+  int32_t* hist = nullptr;
+  int32_t hist_slots = 0, hist_len = 0;
+};
+
+namespace {
+
+cudaEvent_t new_event(ms_ctx* c, bool timing = false) {
+  cudaEvent_t e;
+  CK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  c->events.push_back(e);
+  return e;
+}
+
+std::vector<int32_t> take_pages(ms_ctx* c, int64_t n, cudaStream_t user) {
+  if ((int64_t)c->free_pages.size() < n)
+    fail(MS_ERUNTIME, "arena exhausted: need " + std::to_string(n) + " pages, " +
+                          std::to_string(c->free_pages.size()) + " free");
+  std::vector<int32_t> out;
+  out.reserve(n);
+  cudaEvent_t last = nullptr;
+  for (int64_t i = 0; i < n; ++i) {
+    FreePage fp = c->free_pages.back();
+    c->free_pages.pop_back();
+    if (fp.fence && fp.fence != last && user != c->compute) {
+      CK(cudaStreamWaitEvent(user, fp.fence, 0));
+      last = fp.fence;
+    }
+    out.push_back(fp.page);
+  }
+  return out;
+}
+
+void give_pages(ms_ctx* c, const std::vector<int32_t>& pages, cudaEvent_t fence) {
+  for (auto it = pages.rbegin(); it != pages.rend(); ++it) c->free_pages.push_back({*it, fence});
+}
+
+cudaEvent_t compute_fence(ms_ctx* c) {
+  cudaEvent_t e = new_event(c);
+  CK(cudaEventRecord(e, c->compute));
+  return e;
+}
+
+const ImageGeom& geom_of(ms_ctx* c, int bits) { return bits == 16 ? c->geom16 : c->geom4; }
+
+// Write the page-address table of `pages` into layer slot `slot` (on stream s).
+void write_table(ms_ctx* c, Layer& L, int slot, const std::vector<int32_t>& pages, cudaStream_t s) {
+  for (size_t i = 0; i < pages.size(); ++i)
+    L.h_table[slot][i] = (uint64_t)(c->arena + (int64_t)pages[i] * c->page_bytes);
+  CK(cudaMemcpyAsync(L.d_table[slot], L.h_table[slot], pages.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+}
+
+void upload_image(ms_ctx* c, const uint8_t* img, const ImageGeom& g, const std::vector<int32_t>& pages,
+                  cudaStream_t s) {
+  const int64_t used = g.cpp * g.chunk_bytes;
+  for (int64_t p = 0; p < g.pages; ++p) {
+    const int64_t chunks = std::min<int64_t>(g.cpp, g.total_chunks - p * g.cpp);
+    const int64_t bytes = chunks * g.chunk_bytes;
+    (void)used;
+    CK(cudaMemcpyAsync(c->arena + (int64_t)pages[p] * c->page_bytes, img + p * c->page_bytes, bytes,
+                       cudaMemcpyHostToDevice, s));
+  }
+}
+
+// Scatter a contiguous packed matrix (device) into a pinned host image.
+void scatter_to_image(ms_ctx* c, const ImageGeom& g, int mat, const uint8_t* packed_dev, uint8_t* img) {
+  const int64_t n = (int64_t)(g.mat[mat].N / 128) * (g.mat[mat].K / (g.bits == 16 ? 64 : 128));
+  int64_t ci = 0;
+  while (ci < n) {
+    const int64_t c_abs = g.first_chunk[mat] + ci;
+    const int64_t page = c_abs / g.cpp, inpage = c_abs % g.cpp;
+    const int64_t run = std::min<int64_t>(n - ci, g.cpp - inpage);
+    CK(cudaMemcpyAsync(img + page * c->page_bytes + inpage * g.chunk_bytes, packed_dev + ci * g.chunk_bytes,
+                       run * g.chunk_bytes, cudaMemcpyDeviceToHost, c->compute));
+    ci += run;
+  }
+}
+
+int round16(int m) { return (m + 15) / 16 * 16; }
+
+void build_images(ms_ctx* c, int l, uint16_t* w_dev[kMats], uint8_t* tmp) {
+  Layer& L = c->layers[l];
+  for (int bi = 0; bi < 2; ++bi) {
+    const ImageGeom& g = bi == 0 ? c->geom16 : c->geom4;
+    if (!L.host_img[bi]) {
+      CK(cudaHostAlloc(&L.host_img[bi], g.pages * c->page_bytes, cudaHostAllocPortable));
+      std::memset(L.host_img[bi], 0, g.pages * c->page_bytes);
+    }
+    for (int m = 0; m < kMats; ++m) {
+      if (bi == 0)
+        CK(ms::pack_bf16_launch(w_dev[m], g.mat[m].N, g.mat[m].K, reinterpret_cast<uint16_t*>(tmp), c->compute));
+      else
+        CK(ms::quant_w4_launch(w_dev[m], g.mat[m].N, g.mat[m].K, tmp, nullptr, c->compute));
+      scatter_to_image(c, g, m, tmp, L.host_img[bi]);
+      CK(cudaStreamSynchronize(c->compute));  // tmp reused
+    }
+  }
+}
+
+void make_resident_bf16(ms_ctx* c) {
+  for (int l = 0; l < c->desc.num_layers; ++l) {
+    Layer& L = c->layers[l];
+    if (!L.pages.empty()) give_pages(c, L.pages, nullptr);
+    L.pages = take_pages(c, c->geom16.pages, c->compute);
+    L.bits = 16;
+    L.slot = 0;
+    upload_image(c, L.host_img[0], c->geom16, L.pages, c->compute);
+    write_table(c, L, 0, L.pages, c->compute);
+  }
+  CK(cudaStreamSynchronize(c->compute));
+  c->weights_ready = true;
+}
+
+ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
+  Layer& L = c->layers[l];
+  const ImageGeom& g = geom_of(c, L.bits);
+  return ms::GemmWeights{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
+}
+
+int pick_splits(ms_ctx* c, bool w4, int N, int K, int M, int TM) {
+  const int m_tiles = (M + TM - 1) / TM;
+  const int nk = K / (w4 ? 128 : 64);
+  int s = ms::gemm_pick_splits(N / 128, m_tiles, nk, c->num_sms, ms::gemm_ctas_per_sm(w4, TM));
+  while (s > 1 && (size_t)s * M * N > c->part_elems) --s;
+  return s;
+}
+
+int gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
+  if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
+  const int s = pick_splits(c, w4, w.N, w.K, M, TM);
+  CK(ms::gemm_launch(w, w4, c->x, M, TM, s, c->part, c->compute));
+  return s;
+}
+
+int attn_splits(ms_ctx* c, int rows, int max_ctx) {
+  const int ctas = rows * c->desc.num_kv_heads;
+  const int target = c->num_sms * 4;
+  int s = 1;
+  const int nb = (max_ctx + 15) / 16;
+  while (ctas * s < target && s < 32 && nb / (s * 2) >= 8) s *= 2;
+  while (s > 1 && (size_t)s * rows * c->desc.num_heads * (c->desc.head_dim + 2) > c->attn_ws_elems) s /= 2;
+  return s;
+}
+
+// The decoder over M rows whose per-row metadata already sits in device memory.
+void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_pos, const int32_t* d_ctx,
+             const int32_t* d_tokens, const int32_t* d_pages, const int32_t* d_page_row, int page_stride,
+             int max_ctx, int final_row_begin, bool want_logits) {
+  const ms_model_desc& D = c->desc;
+  const int d = D.hidden, H = D.num_heads, KVH = D.num_kv_heads, hd = D.head_dim;
+  CK(ms::embed_norm_launch(c->embed, d_tokens, c->hist, d_slot, d_pos, c->hist_len, M, d, c->norms, D.rms_eps,
+                           c->h, c->x, TM, c->compute));
+  const int asplits = attn_splits(c, M, max_ctx);
+  for (int l = 0; l < D.num_layers; ++l) {
+    const bool w4 = c->layers[l].bits == 4;
+    int s = gemm(c, mat_weights(c, l, 0), w4, M, TM);
+    CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
+                           d_page_row, page_stride, c->q, c->compute));
+    ms::AttnArgs a{};
+    a.q = c->q;
+    a.kv = c->kv;
+    a.layer = l;
+    a.pages = d_pages;
+    a.page_row = d_page_row;
+    a.page_stride = page_stride;
+    a.ctx_len = d_ctx;
+    a.rows = M;
+    a.H = H;
+    a.KVH = KVH;
+    a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    a.splits = asplits;
+    a.part_o = c->attn_ws;
+    a.part_ml = c->attn_ws + (size_t)asplits * M * H * hd;
+    a.out = c->x;
+    a.out_packed = 1;
+    a.TM = TM;
+    CK(ms::attn_decode_launch(a, c->compute));
+    s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
+    CK(ms::residual_norm_launch(c->part, s, M, d, c->h, c->norms + ((size_t)l * 2 + 1) * d, D.rms_eps, c->x, TM,
+                                c->compute));
+    s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
+    CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
+    s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
+    const bool last = l == D.num_layers - 1;
+    const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
+    const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
+    CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out,
+                                     last ? final_row_begin : 0, c->compute));
+  }
+  const int Mo = M - final_row_begin;
+  const int TMo = round16(Mo) > 256 ? 256 : round16(Mo);
+  ms::GemmWeights lw{c->lm_table, 0, (int64_t)1 << 40, D.vocab, d};
+  const int s = gemm(c, lw, false, Mo, TMo);
+  CK(ms::argmax_launch(c->part, s, Mo, D.vocab, want_logits ? c->logits : nullptr, c->next, c->hist,
+                       d_slot + final_row_begin, d_pos + final_row_begin, c->hist_len, c->compute));
+}
+
+Staging& next_staging(ms_ctx* c, size_t words) {
+  Staging& st = c->ring[c->ring_i];
+  c->ring_i = (c->ring_i + 1) % kRing;
+  if (st.armed) CK(cudaEventSynchronize(st.used));
+  if (st.words < words) {
+    if (st.h) cudaFreeHost(st.h);
+    if (st.d) cudaFree(st.d);
+    st.words = words * 2;
+    CK(cudaHostAlloc(&st.h, st.words * 4, cudaHostAllocDefault));
+    CK(cudaMalloc(&st.d, st.words * 4));
+  }
+  return st;
+}
+
+int32_t page_of(ms_ctx* c, int64_t id) {
+  if (id < 0 || id >= (int64_t)c->id_page.size() || c->id_page[id] < 0)
+    fail(MS_EVALIDATION, "block id " + std::to_string(id) + " is not mapped to a page");
+  return c->id_page[id];
+}
+
+void check_ready(ms_ctx* c) {
+  if (!c->weights_ready) fail(MS_EVALIDATION, "weights not initialised");
+  if (!c->hist) fail(MS_EVALIDATION, "token history not reserved (ms_hist_reserve)");
+}
+
+__global__ void hist_scatter_kernel(int32_t* hist, int stride, const int32_t* slot, const int32_t* pos,
+                                    const int32_t* tok, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) hist[(size_t)slot[i] * stride + pos[i]] = tok[i];
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* ms_last_error(void) { return g_err.c_str(); }
+
+int64_t ms_page_bytes(const ms_model_desc* desc) { return desc ? page_bytes_of(*desc) : -1; }
+
+int64_t ms_layer_pages(const ms_model_desc* desc, int bits) {
+  int64_t out = -1;
+  guard([&] {
+    if (!desc || (bits != 16 && bits != 4)) fail(MS_EVALIDATION, "bits must be 16 or 4");
+    out = image_geom(*desc, bits).pages;
+  });
+  return out;
+}
+
+int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
+  return guard([&] {
+    if (!desc || !out) fail(MS_EVALIDATION, "null argument");
+    validate_desc(*desc);
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) fail(MS_EVALIDATION, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    auto* c = new ms_ctx();
+    try {
+      c->desc = *desc;
+      c->device = device;
+      cudaDeviceProp prop;
+      CK(cudaGetDeviceProperties(&prop, device));
+      c->num_sms = prop.multiProcessorCount;
+      if (prop.major != 10) fail(MS_ERUNTIME, "libmorphserve is built for sm_100a (B200) only");
+      c->page_bytes = page_bytes_of(*desc);
+      c->geom16 = image_geom(*desc, 16);
+      c->geom4 = image_geom(*desc, 4);
+      CK(cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+      CK(cudaMalloc(&c->arena, (size_t)desc->arena_pages * c->page_bytes));
+      c->kv = ms::KvGeom{c->arena, c->page_bytes, desc->num_layers, desc->num_kv_heads, desc->head_dim,
+                         desc->block_tokens};
+      c->free_pages.reserve(desc->arena_pages);
+      for (int64_t p = desc->arena_pages - 1; p >= 0; --p) c->free_pages.push_back({(int32_t)p, nullptr});
+      c->layers.resize(desc->num_layers);
+      const int64_t max_img_pages = std::max(c->geom16.pages, c->geom4.pages);
+      for (auto& L : c->layers) {
+        for (int s = 0; s < 2; ++s) {
+          CK(cudaMalloc(&L.d_table[s], max_img_pages * sizeof(uint64_t)));
+          CK(cudaHostAlloc(&L.h_table[s], max_img_pages * sizeof(uint64_t), cudaHostAllocDefault));
+        }
+        CK(cudaEventCreateWithFlags(&L.ev_start, cudaEventDefault));
+        CK(cudaEventCreateWithFlags(&L.ev_done, cudaEventDefault));
+      }
+      const int d = desc->hidden, H = desc->num_heads, hd = desc->head_dim;
+      const int qkv_n = (H + 2 * desc->num_kv_heads) * hd;
+      c->max_rows = std::max(desc->max_batch, desc->max_prefill_tokens);
+      const int rows_pad = (c->max_rows + 255) / 256 * 256;
+      const int kmax = std::max(std::max(d, H * hd), desc->ffn);
+      const int nmax = std::max(std::max(qkv_n, 2 * desc->ffn), std::max(d, desc->vocab));
+      CK(cudaMalloc(&c->h, (size_t)c->max_rows * d * sizeof(float)));
+      CK(cudaMalloc(&c->x, (size_t)rows_pad * kmax * sizeof(uint16_t)));
+      CK(cudaMemset(c->x, 0, (size_t)rows_pad * kmax * sizeof(uint16_t)));
+      c->part_elems = std::max((size_t)desc->max_prefill_tokens * std::max(qkv_n, 2 * desc->ffn),
+                               (size_t)std::min(desc->max_batch * 16, 4096) * nmax);
+      c->part_elems = std::max(c->part_elems, (size_t)std::min(desc->max_prefill_tokens, 256) * desc->vocab);
+      CK(cudaMalloc(&c->part, c->part_elems * sizeof(float)));
+      CK(cudaMalloc(&c->q, (size_t)c->max_rows * H * hd * sizeof(float)));
+      c->attn_ws_elems = (size_t)16 * desc->max_batch * H * (hd + 2);
+      CK(cudaMalloc(&c->attn_ws, c->attn_ws_elems * sizeof(float)));
+      CK(cudaMalloc(&c->next, (size_t)c->max_rows * sizeof(int32_t)));
+      CK(cudaMalloc(&c->logits, (size_t)desc->max_batch * desc->vocab * sizeof(float)));
+      CK(cudaHostAlloc(&c->h_next, (size_t)c->max_rows * sizeof(int32_t), cudaHostAllocDefault));
+      CK(cudaHostAlloc(&c->h_logits, (size_t)desc->max_batch * desc->vocab * sizeof(float), cudaHostAllocDefault));
+      c->max_blocks = (desc->max_pos + desc->block_tokens - 1) / desc->block_tokens;
+      for (auto& st : c->ring) CK(cudaEventCreateWithFlags(&st.used, cudaEventDisableTiming));
+      CK(cudaEventCreate(&c->ev_step0));
+      CK(cudaEventCreate(&c->ev_step1));
+      // RoPE table (fp64 -> fp32), same formula as oracle/ref_llama.c ref_rope_table
+      const int half = hd / 2;
+      std::vector<float> cs((size_t)desc->max_pos * half), sn((size_t)desc->max_pos * half);
+      for (int p = 0; p < desc->max_pos; ++p)
+        for (int i = 0; i < half; ++i) {
+          const double inv = std::pow(desc->rope_theta, -2.0 * (double)i / (double)hd);
+          const double a = (double)p * inv;
+          cs[(size_t)p * half + i] = (float)std::cos(a);
+          sn[(size_t)p * half + i] = (float)std::sin(a);
+        }
+      CK(cudaMalloc(&c->rope_cos, cs.size() * sizeof(float)));
+      CK(cudaMalloc(&c->rope_sin, sn.size() * sizeof(float)));
+      CK(cudaMemcpy(c->rope_cos, cs.data(), cs.size() * sizeof(float), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->rope_sin, sn.data(), sn.size() * sizeof(float), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&c->embed, (size_t)desc->vocab * d * 2));
+      CK(cudaMalloc(&c->normf, (size_t)d * 2));
+      CK(cudaMalloc(&c->norms, (size_t)desc->num_layers * 2 * d * 2));
+      CK(cudaMalloc(&c->lm_packed, (size_t)desc->vocab * d * 2));
+      CK(cudaMalloc(&c->lm_table, sizeof(uint64_t)));
+      const uint64_t lm_addr = (uint64_t)c->lm_packed;
+      CK(cudaMemcpy(c->lm_table, &lm_addr, sizeof(uint64_t), cudaMemcpyHostToDevice));
+      c->raw.assign((size_t)desc->num_layers * 6 + 3, nullptr);
+    } catch (...) {
+      ms_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int ms_ctx_destroy(ms_ctx* c) {
+  if (!c) return MS_OK;
+  cudaSetDevice(c->device);
+  if (c->compute) cudaStreamSynchronize(c->compute);
+  if (c->copy) cudaStreamSynchronize(c->copy);
+  for (auto& L : c->layers) {
+    for (int s = 0; s < 2; ++s) {
+      cudaFree(L.d_table[s]);
+      cudaFreeHost(L.h_table[s]);
+      cudaFreeHost(L.host_img[s]);
+    }
+    if (L.ev_start) cudaEventDestroy(L.ev_start);
+    if (L.ev_done) cudaEventDestroy(L.ev_done);
+  }
+  for (auto* p : c->raw) cudaFree(p);
+  for (auto& st : c->ring) {
+    cudaFreeHost(st.h);
+    cudaFree(st.d);
+    if (st.used) cudaEventDestroy(st.used);
+  }
+  for (auto e : c->events) cudaEventDestroy(e);
+  if (c->ev_step0) cudaEventDestroy(c->ev_step0);
+  if (c->ev_step1) cudaEventDestroy(c->ev_step1);
+  void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
+                 c->h, c->x, c->part, c->q, c->attn_ws, c->next, c->logits, c->hist};
+  for (void* p : dev) cudaFree(p);
+  cudaFreeHost(c->h_next);
+  cudaFreeHost(c->h_logits);
+  if (c->compute) cudaStreamDestroy(c->compute);
+  if (c->copy) cudaStreamDestroy(c->copy);
+  delete c;
+  return MS_OK;
+}
+
+int ms_sync(ms_ctx* c) {
+  return guard([&] {
+    CK(cudaStreamSynchronize(c->compute));
+    CK(cudaStreamSynchronize(c->copy));
+  });
+}
+
+int ms_num_sms(ms_ctx* c) { return c ? c->num_sms : 0; }
+
+// ------------------------------------------------------------------ weights
+namespace {
+struct TensorSpec {
+  int64_t n;
+  double scale, offset;
+};
+TensorSpec layer_tensor(const ms_model_desc& D, int which) {
+  const int64_t d = D.hidden, qkv_n = (int64_t)(D.num_heads + 2 * D.num_kv_heads) * D.head_dim;
+  switch (which) {
+    case 0: case 3: return {d, 0.1, 1.0};
+    case 1: return {qkv_n * d, 1.0 / std::sqrt((double)d), 0.0};
+    case 2: return {d * D.num_heads * D.head_dim, 1.0 / std::sqrt((double)(D.num_heads * D.head_dim)), 0.0};
+    case 4: return {2LL * D.ffn * d, 1.0 / std::sqrt((double)d), 0.0};
+    default: return {d * D.ffn, 1.0 / std::sqrt((double)D.ffn), 0.0};
+  }
+}
+int64_t expected_count(const ms_model_desc& D, int layer, int which) {
+  if (layer < 0) return which == 1 ? D.hidden : (int64_t)D.vocab * D.hidden;
+  return layer_tensor(D, which).n;
+}
+void finalize_weights(ms_ctx* c, bool synthetic, uint64_t seed) {
+  const ms_model_desc& D = c->desc;
+  const int d = D.hidden;
+  const int64_t tmp_elems = std::max<int64_t>((int64_t)2 * D.ffn * d,
+                                              (int64_t)(D.num_heads + 2 * D.num_kv_heads) * D.head_dim * d);
+  uint16_t* wtmp[kMats] = {nullptr, nullptr, nullptr, nullptr};
+  uint8_t* ptmp = nullptr;
+  try {
+    if (synthetic) {
+      CK(ms::gen_weight_launch(seed, 0, (int64_t)D.vocab * d, 1.0, 0.0, c->embed, c->compute));
+      CK(ms::gen_weight_launch(seed, 1, d, 0.1, 1.0, c->normf, c->compute));
+      uint16_t* lm = nullptr;
+      CK(cudaMalloc(&lm, (size_t)D.vocab * d * 2));
+      CK(ms::gen_weight_launch(seed, 2, (int64_t)D.vocab * d, 1.0 / std::sqrt((double)d), 0.0, lm, c->compute));
+      CK(ms::pack_bf16_launch(lm, D.vocab, d, c->lm_packed, c->compute));
+      CK(cudaStreamSynchronize(c->compute));
+      cudaFree(lm);
+    } else {
+      for (int w = 0; w < 3; ++w)
+        if (!c->raw[(size_t)D.num_layers * 6 + w]) fail(MS_EVALIDATION, "missing global tensor upload");
+      CK(cudaMemcpyAsync(c->embed, c->raw[(size_t)D.num_layers * 6 + 0], (size_t)D.vocab * d * 2,
+                         cudaMemcpyDeviceToDevice, c->compute));
+      CK(cudaMemcpyAsync(c->normf, c->raw[(size_t)D.num_layers * 6 + 1], (size_t)d * 2, cudaMemcpyDeviceToDevice,
+                         c->compute));
+      CK(ms::pack_bf16_launch(c->raw[(size_t)D.num_layers * 6 + 2], D.vocab, d, c->lm_packed, c->compute));
+    }
+    for (int m = 0; m < kMats; ++m) CK(cudaMalloc(&wtmp[m], (size_t)tmp_elems * 2));
+    CK(cudaMalloc(&ptmp, (size_t)tmp_elems * 2));
+    static const int mat_which[kMats] = {1, 2, 4, 5};
+    for (int l = 0; l < D.num_layers; ++l) {
+      for (int nrm = 0; nrm < 2; ++nrm) {
+        uint16_t* dst = c->norms + ((size_t)l * 2 + nrm) * d;
+        const int which = nrm == 0 ? 0 : 3;
+        if (synthetic) {
+          CK(ms::gen_weight_launch(seed, 16 + (uint64_t)l * 8 + which, d, 0.1, 1.0, dst, c->compute));
+        } else {
+          uint16_t* r = c->raw[(size_t)l * 6 + which];
+          if (!r) fail(MS_EVALIDATION, "missing norm upload");
+          CK(cudaMemcpyAsync(dst, r, (size_t)d * 2, cudaMemcpyDeviceToDevice, c->compute));
+        }
+      }
+      for (int m = 0; m < kMats; ++m) {
+        const int which = mat_which[m];
+        if (synthetic) {
+          const TensorSpec t = layer_tensor(D, which);
+          CK(ms::gen_weight_launch(seed, 16 + (uint64_t)l * 8 + which, t.n, t.scale, t.offset, wtmp[m],
+                                   c->compute));
+        } else {
+          uint16_t* r = c->raw[(size_t)l * 6 + which];
+          if (!r) fail(MS_EVALIDATION, "missing layer tensor upload");
+          CK(cudaMemcpyAsync(wtmp[m], r, (size_t)layer_tensor(D, which).n * 2, cudaMemcpyDeviceToDevice,
+                             c->compute));
+        }
+      }
+      build_images(c, l, wtmp, ptmp);
+    }
+    make_resident_bf16(c);
+  } catch (...) {
+    for (auto* p : wtmp) cudaFree(p);
+    cudaFree(ptmp);
+    throw;
+  }
+  for (auto* p : wtmp) cudaFree(p);
+  cudaFree(ptmp);
+  for (auto*& p : c->raw) {
+    cudaFree(p);
+    p = nullptr;
+  }
+}
+}  // namespace
+
+int ms_weights_synthetic(ms_ctx* c, uint64_t seed) {
+  return guard([&] {
+    CK(cudaSetDevice(c->device));
+    finalize_weights(c, true, seed);
+  });
+}
+
+int ms_weights_upload(ms_ctx* c, int layer, int which, const uint16_t* host_bf16, int64_t count) {
+  return guard([&] {
+    const ms_model_desc& D = c->desc;
+    if (layer < -1 || layer >= D.num_layers) fail(MS_EVALIDATION, "layer out of range");
+    if (layer < 0 ? (which < 0 || which > 2) : (which < 0 || which > 5)) fail(MS_EVALIDATION, "bad tensor id");
+    if (count != expected_count(D, layer, which)) fail(MS_EVALIDATION, "tensor element count mismatch");
+    const size_t idx = layer < 0 ? (size_t)D.num_layers * 6 + which : (size_t)layer * 6 + which;
+    if (!c->raw[idx]) CK(cudaMalloc(&c->raw[idx], (size_t)count * 2));
+    CK(cudaMemcpy(c->raw[idx], host_bf16, (size_t)count * 2, cudaMemcpyHostToDevice));
+  });
+}
+
+int ms_weights_finalize(ms_ctx* c) {
+  return guard([&] {
+    CK(cudaSetDevice(c->device));
+    finalize_weights(c, false, 0);
+  });
+}
+
+int64_t ms_variant_bytes(ms_ctx* c, int bits) {
+  return (bits == 16 ? c->geom16.pages : c->geom4.pages) * c->page_bytes;
+}
+
+int ms_variant_export(ms_ctx* c, int layer, int bits, void* host_out, int64_t bytes) {
+  return guard([&] {
+    if (layer < 0 || layer >= c->desc.num_layers) fail(MS_EVALIDATION, "layer out of range");
+    if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "bits must be 16 or 4");
+    const Layer& L = c->layers[layer];
+    const uint8_t* img = L.host_img[bits == 16 ? 0 : 1];
+    if (!img) fail(MS_EVALIDATION, "variant store not built");
+    const int64_t n = std::min<int64_t>(bytes, ms_variant_bytes(c, bits));
+    std::memcpy(host_out, img, (size_t)n);
+  });
+}
+
+// ------------------------------------------------------------- LayerSwapper
+int ms_swap_begin(ms_ctx* c, int layer, int bits, uint64_t* ticket) {
+  return guard([&] {
+    if (layer < 0 || layer >= c->desc.num_layers) fail(MS_EVALIDATION, "begin_swap: layer out of range");
+    Layer& L = c->layers[layer];
+    if (L.in_flight) fail(MS_EVALIDATION, "begin_swap: swap already in flight on layer");
+    if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "begin_swap: bits must be 16 or 4");
+    if (L.bits == bits) fail(MS_EVALIDATION, "begin_swap: layer already at target precision");
+    if (!c->weights_ready) fail(MS_EVALIDATION, "weights not initialised");
+    const ImageGeom& g = geom_of(c, bits);
+    CK(cudaSetDevice(c->device));
+    // the inactive table slot may still be read by steps launched before the
+    // previous commit of this layer
+    if (L.last_release) CK(cudaStreamWaitEvent(c->copy, L.last_release, 0));
+    L.new_pages = take_pages(c, g.pages, c->copy);
+    CK(cudaEventRecord(L.ev_start, c->copy));
+    write_table(c, L, L.slot ^ 1, L.new_pages, c->copy);
+    upload_image(c, L.host_img[bits == 16 ? 0 : 1], g, L.new_pages, c->copy);
+    CK(cudaEventRecord(L.ev_done, c->copy));
+    L.in_flight = true;
+    L.to_bits = bits;
+    L.ticket = (c->next_ticket++ << 16) | (uint64_t)layer;
+    *ticket = L.ticket;
+  });
+}
+
+namespace {
+Layer& ticket_layer(ms_ctx* c, uint64_t ticket) {
+  const int layer = (int)(ticket & 0xFFFF);
+  if (layer >= c->desc.num_layers) fail(MS_EVALIDATION, "bad swap ticket");
+  Layer& L = c->layers[layer];
+  if (!L.in_flight || L.ticket != ticket) fail(MS_ELOGIC, "complete_swap: no swap in flight on layer");
+  return L;
+}
+}  // namespace
+
+int ms_swap_poll(ms_ctx* c, uint64_t ticket, int* done) {
+  return guard([&] {
+    Layer& L = ticket_layer(c, ticket);
+    const cudaError_t e = cudaEventQuery(L.ev_done);
+    if (e == cudaErrorNotReady) {
+      *done = 0;
+      return;
+    }
+    CK(e);
+    *done = 1;
+  });
+}
+
+int ms_swap_wait(ms_ctx* c, uint64_t ticket, float* upload_ms) {
+  return guard([&] {
+    Layer& L = ticket_layer(c, ticket);
+    CK(cudaEventSynchronize(L.ev_done));
+    if (upload_ms) CK(cudaEventElapsedTime(upload_ms, L.ev_start, L.ev_done));
+  });
+}
+
+int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
+  return guard([&] {
+    Layer& L = ticket_layer(c, ticket);
+    CK(cudaSetDevice(c->device));
+    // Token-boundary flip: steps launched from now on use the new image; the
+    // compute stream orders them after the upload (no host sync, no flush).
+    CK(cudaStreamWaitEvent(c->compute, L.ev_done, 0));
+    cudaEvent_t fence = compute_fence(c);  // after every step that read the old image
+    const int64_t freed = (int64_t)L.pages.size();
+    give_pages(c, L.pages, fence);
+    L.pages = std::move(L.new_pages);
+    L.new_pages.clear();
+    L.slot ^= 1;
+    L.bits = L.to_bits;
+    L.in_flight = false;
+    L.last_release = fence;
+    if (pages_freed) *pages_freed = freed;
+  });
+}
+
+int ms_layer_bits(ms_ctx* c, int layer) {
+  if (!c || layer < 0 || layer >= c->desc.num_layers) return -1;
+  return c->layers[layer].bits;
+}
+
+// ---------------------------------------------------------------- KV resizer
+int ms_kv_attach(ms_ctx* c, int64_t first_id, int64_t n) {
+  return guard([&] {
+    if (n < 1) fail(MS_EVALIDATION, "kv attach: count must be >= 1");
+    if (first_id < 0) fail(MS_EVALIDATION, "kv attach: negative id");
+    for (int64_t id = first_id; id < first_id + n; ++id)
+      if (id < (int64_t)c->id_page.size() && c->id_page[id] >= 0) fail(MS_EVALIDATION, "kv attach: id already mapped");
+    std::vector<int32_t> pages = take_pages(c, n, c->compute);
+    if ((int64_t)c->id_page.size() < first_id + n) c->id_page.resize(first_id + n, -1);
+    for (int64_t i = 0; i < n; ++i) c->id_page[first_id + i] = pages[i];
+  });
+}
+
+int ms_kv_detach(ms_ctx* c, const int64_t* ids, int64_t n) {
+  return guard([&] {
+    std::vector<int32_t> pages;
+    pages.reserve(n);
+    for (int64_t i = 0; i < n; ++i) {
+      pages.push_back(page_of(c, ids[i]));
+      c->id_page[ids[i]] = -1;
+    }
+    give_pages(c, pages, compute_fence(c));
+  });
+}
+
+int64_t ms_free_pages(ms_ctx* c) { return c ? (int64_t)c->free_pages.size() : -1; }
+
+int64_t ms_kv_page_of(ms_ctx* c, int64_t id) {
+  if (!c || id < 0 || id >= (int64_t)c->id_page.size()) return -1;
+  return c->id_page[id];
+}
+
+// ------------------------------------------------------------ token history
+int ms_hist_reserve(ms_ctx* c, int32_t slots, int32_t max_len) {
+  return guard([&] {
+    if (slots < 1 || max_len < 2) fail(MS_EVALIDATION, "bad history shape");
+    if (max_len > c->desc.max_pos + 1) fail(MS_EVALIDATION, "history longer than max_pos");
+    CK(cudaStreamSynchronize(c->compute));
+    if (c->hist) cudaFree(c->hist);
+    c->hist = nullptr;
+    CK(cudaMalloc(&c->hist, (size_t)slots * max_len * sizeof(int32_t)));
+    CK(cudaMemset(c->hist, 0, (size_t)slots * max_len * sizeof(int32_t)));
+    c->hist_slots = slots;
+    c->hist_len = max_len;
+  });
+}
+
+int ms_hist_write(ms_ctx* c, int32_t slot, int32_t offset, const int32_t* host_tokens, int32_t n) {
+  return guard([&] {
+    if (!c->hist || slot < 0 || slot >= c->hist_slots || offset < 0 || offset + n > c->hist_len)
+      fail(MS_EVALIDATION, "history write out of range");
+    for (int i = 0; i < n; ++i)
+      if (host_tokens[i] < 0 || host_tokens[i] >= c->desc.vocab) fail(MS_EVALIDATION, "token id out of vocab");
+    Staging& st = next_staging(c, (size_t)n);
+    std::memcpy(st.h, host_tokens, (size_t)n * 4);
+    CK(cudaMemcpyAsync(c->hist + (size_t)slot * c->hist_len + offset, st.h, (size_t)n * 4, cudaMemcpyHostToDevice,
+                       c->compute));
+    CK(cudaEventRecord(st.used, c->compute));
+    st.armed = true;
+  });
+}
+
+int ms_hist_read(ms_ctx* c, int32_t slot, int32_t offset, int32_t* host_out, int32_t n) {
+  return guard([&] {
+    if (!c->hist || slot < 0 || slot >= c->hist_slots || offset < 0 || offset + n > c->hist_len)
+      fail(MS_EVALIDATION, "history read out of range");
+    CK(cudaMemcpyAsync(host_out, c->hist + (size_t)slot * c->hist_len + offset, (size_t)n * 4,
+                       cudaMemcpyDeviceToHost, c->compute));
+    CK(cudaStreamSynchronize(c->compute));
+  });
+}
+
+// -------------------------------------------------------------------- steps
+int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float* logits_out) {
+  return guard([&] {
+    check_ready(c);
+    const int n = b->n;
+    if (n < 1 || n > c->desc.max_batch) fail(MS_EVALIDATION, "decode batch size out of range");
+    const int mb = c->max_blocks;
+    // staging: slot[n] pos[n] ctx[n] tok[n] pages[n][mb]
+    Staging& st = next_staging(c, (size_t)n * (4 + mb));
+    int32_t* hs = st.h;
+    int max_ctx = 0;
+    for (int i = 0; i < n; ++i) {
+      const int slot = b->slots[i], pos = b->positions[i];
+      if (slot < 0 || slot >= c->hist_slots) fail(MS_EVALIDATION, "slot out of range");
+      if (pos < 0 || pos + 1 >= c->hist_len || pos >= c->desc.max_pos) fail(MS_EVALIDATION, "position out of range");
+      hs[i] = slot;
+      hs[n + i] = pos;
+      hs[2 * n + i] = pos + 1;
+      hs[3 * n + i] = b->tokens ? b->tokens[i] : 0;
+      if (b->tokens && (b->tokens[i] < 0 || b->tokens[i] >= c->desc.vocab)) fail(MS_EVALIDATION, "token out of vocab");
+      max_ctx = std::max(max_ctx, pos + 1);
+      const int nb = pos / c->desc.block_tokens + 1;
+      if (nb > b->max_blocks) fail(MS_EVALIDATION, "block table narrower than the context");
+      int32_t* row = hs + 4 * n + (size_t)i * mb;
+      for (int j = 0; j < nb; ++j) row[j] = page_of(c, b->block_ids[(size_t)i * b->max_blocks + j]);
+    }
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventRecord(c->ev_step0, c->compute));
+    CK(cudaMemcpyAsync(st.d, st.h, (size_t)n * (4 + mb) * 4, cudaMemcpyHostToDevice, c->compute));
+    CK(cudaEventRecord(st.used, c->compute));
+    st.armed = true;
+    const int32_t* d_slot = st.d;
+    const int32_t* d_pos = st.d + n;
+    const int32_t* d_ctx = st.d + 2 * n;
+    const int32_t* d_tok = st.d + 3 * n;
+    const int32_t* d_pages = st.d + 4 * n;
+    if (b->tokens) {
+      hist_scatter_kernel<<<(n + 127) / 128, 128, 0, c->compute>>>(c->hist, c->hist_len, d_slot, d_pos, d_tok, n);
+      CK(cudaGetLastError());
+    }
+    const int TM = std::min(256, round16(n));
+    forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, logits_out != nullptr);
+    CK(cudaEventRecord(c->ev_step1, c->compute));
+    if (next_out || logits_out) {
+      if (next_out) CK(cudaMemcpyAsync(c->h_next, c->next, (size_t)n * 4, cudaMemcpyDeviceToHost, c->compute));
+      if (logits_out)
+        CK(cudaMemcpyAsync(c->h_logits, c->logits, (size_t)n * c->desc.vocab * 4, cudaMemcpyDeviceToHost,
+                           c->compute));
+      CK(cudaStreamSynchronize(c->compute));
+      if (next_out) std::memcpy(next_out, c->h_next, (size_t)n * 4);
+      if (logits_out) std::memcpy(logits_out, c->h_logits, (size_t)n * c->desc.vocab * 4);
+    }
+  });
+}
+
+int ms_prefill(ms_ctx* c, int32_t slot, int32_t n_tokens, const int64_t* block_ids, int32_t n_blocks,
+               int32_t* next_out, float* logits_out) {
+  return guard([&] {
+    check_ready(c);
+    const int n = n_tokens;
+    if (n < 1 || n > c->desc.max_prefill_tokens) fail(MS_EVALIDATION, "prefill length out of range");
+    if (slot < 0 || slot >= c->hist_slots || n + 1 > c->hist_len) fail(MS_EVALIDATION, "prefill slot/length");
+    const int nb = (n + c->desc.block_tokens - 1) / c->desc.block_tokens;
+    if (n_blocks < nb) fail(MS_EVALIDATION, "prefill needs more blocks");
+    const int mb = c->max_blocks;
+    Staging& st = next_staging(c, (size_t)n * 4 + mb);
+    int32_t* hs = st.h;
+    for (int i = 0; i < n; ++i) {
+      hs[i] = slot;
+      hs[n + i] = i;
+      hs[2 * n + i] = i + 1;
+      hs[3 * n + i] = 0;  // page_row
+    }
+    int32_t* row = hs + 4 * n;
+    for (int j = 0; j < nb; ++j) row[j] = page_of(c, block_ids[j]);
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventRecord(c->ev_step0, c->compute));
+    CK(cudaMemcpyAsync(st.d, st.h, ((size_t)n * 4 + mb) * 4, cudaMemcpyHostToDevice, c->compute));
+    CK(cudaEventRecord(st.used, c->compute));
+    st.armed = true;
+    const int TM = std::min(256, round16(n));
+    forward(c, n, TM, st.d, st.d + n, st.d + 2 * n, nullptr, st.d + 4 * n, st.d + 3 * n, 0, n, n - 1,
+            logits_out != nullptr);
+    CK(cudaEventRecord(c->ev_step1, c->compute));
+    if (next_out || logits_out) {
+      if (next_out) CK(cudaMemcpyAsync(c->h_next, c->next, 4, cudaMemcpyDeviceToHost, c->compute));
+      if (logits_out)
+        CK(cudaMemcpyAsync(c->h_logits, c->logits, (size_t)c->desc.vocab * 4, cudaMemcpyDeviceToHost, c->compute));
+      CK(cudaStreamSynchronize(c->compute));
+      if (next_out) *next_out = c->h_next[0];
+      if (logits_out) std::memcpy(logits_out, c->h_logits, (size_t)c->desc.vocab * 4);
+    }
+  });
+}
+
+int ms_last_step_ms(ms_ctx* c, float* ms_out) {
+  return guard([&] {
+    CK(cudaEventSynchronize(c->ev_step1));
+    CK(cudaEventElapsedTime(ms_out, c->ev_step0, c->ev_step1));
+  });
+}
+
+int ms_kv_fill_synthetic(ms_ctx* c, const int64_t* ids, int64_t n, uint64_t seed) {
+  return guard([&] {
+    std::vector<int32_t> pages(n);
+    for (int64_t i = 0; i < n; ++i) pages[i] = page_of(c, ids[i]);
+    int32_t* d = nullptr;
+    CK(cudaMalloc(&d, (size_t)n * 4));
+    CK(cudaMemcpyAsync(d, pages.data(), (size_t)n * 4, cudaMemcpyHostToDevice, c->compute));
+    CK(ms::fill_kv_launch(c->kv, d, (int)n, seed, c->compute));
+    CK(cudaStreamSynchronize(c->compute));
+    cudaFree(d);
+  });
+}
+
+// ------------------------------------------------------ kernel-level (tests)
+int ms_k_gen_weight(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset, uint16_t* out,
+                    void* stream) {
+  return guard([&] { CK(ms::gen_weight_launch(seed, tensor, n, scale, offset, out, (cudaStream_t)stream)); });
+}
+int ms_k_pack_bf16(const uint16_t* w, int N, int K, uint16_t* out, void* stream) {
+  return guard([&] {
+    if (N % 128 || K % 64) fail(MS_EVALIDATION, "pack_bf16: N%128, K%64");
+    CK(ms::pack_bf16_launch(w, N, K, out, (cudaStream_t)stream));
+  });
+}
+int ms_k_quant_w4(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, void* stream) {
+  return guard([&] {
+    if (N % 128 || K % 128) fail(MS_EVALIDATION, "quant_w4: N%128, K%128");
+    CK(ms::quant_w4_launch(w, N, K, out, codes_out, (cudaStream_t)stream));
+  });
+}
+int ms_k_pack_act(const uint16_t* x, int M, int K, int TM, uint16_t* out, void* stream) {
+  return guard([&] {
+    if (K % 64 || TM % 16 || TM < 16 || TM > 256) fail(MS_EVALIDATION, "pack_act: K%64, TM in 16..256 step 16");
+    CK(ms::pack_act_launch(x, M, K, TM, out, (cudaStream_t)stream));
+  });
+}
+int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_packed, int M, int TM, int splits,
+              float* out, int* splits_used, void* stream) {
+  return guard([&] {
+    if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "gemm: bits must be 16 or 4");
+    if (N % 128 || K % 128 || M < 1 || TM % 16 || TM < 16 || TM > 256) fail(MS_EVALIDATION, "gemm: bad shape");
+    static thread_local uint64_t* table = nullptr;
+    if (!table) CK(cudaMalloc(&table, sizeof(uint64_t)));
+    const uint64_t addr = (uint64_t)w_packed;
+    CK(cudaMemcpyAsync(table, &addr, sizeof(addr), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    ms::GemmWeights w{table, 0, (int64_t)1 << 40, N, K};
+    const bool w4 = bits == 4;
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int nk = K / (w4 ? 128 : 64);
+    int s = splits > 0 ? std::min(splits, nk)
+                       : ms::gemm_pick_splits(N / 128, (M + TM - 1) / TM, nk, sms, ms::gemm_ctas_per_sm(w4, TM));
+    CK(ms::gemm_launch(w, w4, x_packed, M, TM, s, out, (cudaStream_t)stream));
+    if (splits_used) *splits_used = s;
+  });
+}
+int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int layers, int layer, int H, int KVH,
+                     int hd, const int32_t* pages, int max_blocks, const int32_t* ctx_len, int rows, int splits,
+                     float* workspace, uint16_t* out, void* stream) {
+  return guard([&] {
+    ms::AttnArgs a{};
+    a.q = q;
+    a.kv = ms::KvGeom{(char*)arena, page_bytes, layers, KVH, hd, 16};
+    a.layer = layer;
+    a.pages = pages;
+    a.page_row = nullptr;
+    a.page_stride = max_blocks;
+    a.ctx_len = ctx_len;
+    a.rows = rows;
+    a.H = H;
+    a.KVH = KVH;
+    a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    a.splits = splits < 1 ? 1 : splits;
+    a.part_o = workspace;
+    a.part_ml = workspace ? workspace + (size_t)a.splits * rows * H * hd : nullptr;
+    a.out = out;
+    a.out_packed = 0;
+    a.TM = 16;
+    if (a.splits > 1 && !workspace) fail(MS_EVALIDATION, "attn: split-KV needs a workspace");
+    CK(ms::attn_decode_launch(a, (cudaStream_t)stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+"""Python handle on one B200 device context (libmorphserve.so, include/morphserve.h).
+
+This is the model-runner / LayerSwapper / KV-resizer surface the host runtime
+drives; every method is one C-ABI call.  Shapes follow the
+BASELINE.json configs:
+
+    TINY      Llama-style L=4, d=256, H=4, KVH=2, hd=64, ffn=768, V=1024 (config 1)
+    LLAMA2_7B L=32, d=4096, H=KVH=32, hd=128, ffn=11008, V=32000      (config 2)
+    LLAMA3_8B L=32, d=4096, H=32, KVH=8, hd=128, ffn=14336, V=128256  (config 3/5)
+    LLAMA2_13B L=40, d=5120, H=KVH=40, hd=128, ffn=13824, V=32000     (config 4)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+TINY = dict(L=4, d=256, H=4, KVH=2, hd=64, ffn=768, V=1024)
+LLAMA2_7B = dict(L=32, d=4096, H=32, KVH=32, hd=128, ffn=11008, V=32000)
+LLAMA3_8B = dict(L=32, d=4096, H=32, KVH=8, hd=128, ffn=14336, V=128256, theta=500000.0)
+LLAMA2_13B = dict(L=40, d=5120, H=40, KVH=40, hd=128, ffn=13824, V=32000)
+
+
+def model_desc(shape: dict, *, max_batch: int, max_prefill_tokens: int, max_pos: int,
+               arena_pages: int, eps: float = 1e-5) -> N.ModelDesc:
+    return N.ModelDesc(shape["L"], shape["d"], shape["H"], shape["KVH"], shape["hd"], shape["ffn"],
+                       shape["V"], 16, max_batch, max_prefill_tokens, max_pos, eps,
+                       float(shape.get("theta", 10000.0)), arena_pages)
+
+
+def page_bytes(shape: dict) -> int:
+    return 16 * shape["L"] * shape["KVH"] * 2 * shape["hd"] * 2
+
+
+def layer_pages(shape: dict, bits: int) -> int:
+    d = model_desc(shape, max_batch=1, max_prefill_tokens=1, max_pos=16, arena_pages=1)
+    return N.lib().ms_layer_pages(C.byref(d), bits)
+
+
+@dataclass
+class SwapTicket:
+    layer: int
+    bits: int
+    ticket: int
+
+
+class DeviceModel:
+    """One device context: arena, layer table, variant store, streams, steps."""
+
+    def __init__(self, shape: dict, *, device: int = 0, max_batch: int = 64, max_prefill_tokens: int = 2048,
+                 max_pos: int = 4096, arena_pages: int, eps: float = 1e-5):
+        self.shape = dict(shape)
+        self.desc = model_desc(shape, max_batch=max_batch, max_prefill_tokens=max_prefill_tokens,
+                               max_pos=max_pos, arena_pages=arena_pages, eps=eps)
+        self.lib = N.lib()
+        h = C.c_void_p()
+        N.check(self.lib.ms_ctx_create(device, C.byref(self.desc), C.byref(h)))
+        self.h = h
+        self.max_blocks = (max_pos + 15) // 16
+        self.page_bytes = self.lib.ms_page_bytes(C.byref(self.desc))
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ms_ctx_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        N.check(self.lib.ms_sync(self.h))
+
+    # -- weights
+    def weights_synthetic(self, seed: int):
+        N.check(self.lib.ms_weights_synthetic(self.h, seed))
+
+    def upload(self, layer: int, which: int, arr_bf16: np.ndarray):
+        a = np.ascontiguousarray(arr_bf16, np.uint16)
+        N.check(self.lib.ms_weights_upload(self.h, layer, which, a.ctypes.data, a.size))
+
+    def finalize(self):
+        N.check(self.lib.ms_weights_finalize(self.h))
+
+    def variant_image(self, layer: int, bits: int) -> np.ndarray:
+        n = self.lib.ms_variant_bytes(self.h, bits)
+        out = np.empty(n, np.uint8)
+        N.check(self.lib.ms_variant_export(self.h, layer, bits, out.ctypes.data, n))
+        return out
+
+    # -- LayerSwapper
+    def swap_begin(self, layer: int, bits: int) -> SwapTicket:
+        t = C.c_uint64()
+        N.check(self.lib.ms_swap_begin(self.h, layer, bits, C.byref(t)))
+        return SwapTicket(layer, bits, t.value)
+
+    def swap_done(self, t: SwapTicket) -> bool:
+        d = C.c_int()
+        N.check(self.lib.ms_swap_poll(self.h, t.ticket, C.byref(d)))
+        return bool(d.value)
+
+    def swap_wait(self, t: SwapTicket) -> float:
+        ms = C.c_float()
+        N.check(self.lib.ms_swap_wait(self.h, t.ticket, C.byref(ms)))
+        return ms.value
+
+    def swap_commit(self, t: SwapTicket) -> int:
+        freed = C.c_int64()
+        N.check(self.lib.ms_swap_commit(self.h, t.ticket, C.byref(freed)))
+        return freed.value
+
+    def layer_bits(self, layer: int) -> int:
+        return self.lib.ms_layer_bits(self.h, layer)
+
+    # -- KV resizer
+    def kv_attach(self, first_id: int, n: int):
+        N.check(self.lib.ms_kv_attach(self.h, first_id, n))
+
+    def kv_detach(self, ids):
+        a = np.ascontiguousarray(ids, np.int64)
+        N.check(self.lib.ms_kv_detach(self.h, N.i64p(a), a.size))
+
+    def free_pages(self) -> int:
+        return self.lib.ms_free_pages(self.h)
+
+    def page_of(self, block_id: int) -> int:
+        return self.lib.ms_kv_page_of(self.h, block_id)
+
+    # -- token history
+    def hist_reserve(self, slots: int, max_len: int):
+        N.check(self.lib.ms_hist_reserve(self.h, slots, max_len))
+
+    def hist_write(self, slot: int, offset: int, tokens):
+        a = np.ascontiguousarray(tokens, np.int32)
+        N.check(self.lib.ms_hist_write(self.h, slot, offset, N.i32p(a), a.size))
+
+    def hist_read(self, slot: int, offset: int, n: int) -> np.ndarray:
+        out = np.empty(n, np.int32)
+        N.check(self.lib.ms_hist_read(self.h, slot, offset, N.i32p(out), n))
+        return out
+
+    # -- steps
+    def prefill(self, slot: int, n_tokens: int, block_ids, want_logits: bool = False):
+        ids = np.ascontiguousarray(block_ids, np.int64)
+        nxt = C.c_int32()
+        logits = np.empty(self.shape["V"], np.float32) if want_logits else None
+        N.check(self.lib.ms_prefill(self.h, slot, n_tokens, N.i64p(ids), ids.size, C.byref(nxt),
+                                    N.f32p(logits)))
+        return nxt.value, logits
+
+    def decode(self, slots, positions, block_table, tokens=None, want_next: bool = True,
+               want_logits: bool = False):
+        slots = np.ascontiguousarray(slots, np.int32)
+        pos = np.ascontiguousarray(positions, np.int32)
+        bt = np.ascontiguousarray(block_table, np.int64)
+        n = slots.size
+        tok = np.ascontiguousarray(tokens, np.int32) if tokens is not None else None
+        b = N.DecodeBatch(n, N.i32p(slots), N.i32p(pos), N.i32p(tok), N.i64p(bt), bt.shape[1])
+        nxt = np.empty(n, np.int32) if want_next else None
+        logits = np.empty((n, self.shape["V"]), np.float32) if want_logits else None
+        N.check(self.lib.ms_decode_step(self.h, C.byref(b), N.i32p(nxt), N.f32p(logits)))
+        return nxt, logits
+
+    def last_step_ms(self) -> float:
+        ms = C.c_float()
+        N.check(self.lib.ms_last_step_ms(self.h, C.byref(ms)))
+        return ms.value
+
+    def kv_fill_synthetic(self, block_ids, seed: int):
+        a = np.ascontiguousarray(block_ids, np.int64)
+        N.check(self.lib.ms_kv_fill_synthetic(self.h, N.i64p(a), a.size, seed))

@@ -1,0 +1,164 @@
+"""Kernel-level parity: every CUDA kernel on the hot path against the CPU oracle
+(oracle/ref_llama.c) on the same seeded inputs.  Integer / byte work is
+bit-exact; floating point within the tolerance stated in each test.
+Runs only on a B200 (-m gpu), through the C ABI (include/morphserve.h).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _native():
+    from paper_2506_02006_b200 import _native as N
+    return N
+
+
+def dev_u16(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda()
+
+
+def to_np_u16(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint16)
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def test_generator_bit_exact():
+    N = _native()
+    for tensor, n, scale, off in [(0, 1 << 16, 1.0, 0.0), (17, 4096, 0.1, 1.0), (99, 123457, 1 / 64.0, 0.0)]:
+        out = torch.empty(n, dtype=torch.int16, device="cuda")
+        N.check(N.lib().ms_k_gen_weight(7, tensor, n, scale, off, C.c_void_p(out.data_ptr()), stream()))
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np_u16(out), O.gen_weight(7, tensor, n, scale, off))
+
+
+@pytest.mark.parametrize("N_,K", [(128, 64), (256, 256), (512, 768), (1536, 256)])
+def test_pack_bf16_bit_exact(N_, K):
+    N = _native()
+    w = O.gen_weight(3, 5, N_ * K, 0.05).reshape(N_, K)
+    dw = dev_u16(w)
+    out = torch.empty(N_ * K, dtype=torch.int16, device="cuda")
+    N.check(N.lib().ms_k_pack_bf16(C.c_void_p(dw.data_ptr()), N_, K, C.c_void_p(out.data_ptr()), stream()))
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np_u16(out), O.pack_bf16(w))
+
+
+@pytest.mark.parametrize("N_,K", [(128, 128), (256, 768), (512, 256)])
+def test_quant_w4_codes_and_image_bit_exact(N_, K):
+    N = _native()
+    w = O.gen_weight(11, 6, N_ * K, 0.02).reshape(N_, K).copy()
+    w[3, :128] = 0          # all-zero group -> scale 1, codes 0 (toy_model.cpp:43,53)
+    w[5, 128 - 1] = w[5, 0]  # ties are fine, exercise equal maxima
+    dw = dev_u16(w)
+    img = torch.empty((N_ // 128) * (K // 128) * 8448, dtype=torch.uint8, device="cuda")
+    codes = torch.empty(N_ * K, dtype=torch.int8, device="cuda")
+    N.check(N.lib().ms_k_quant_w4(C.c_void_p(dw.data_ptr()), N_, K, C.c_void_p(img.data_ptr()),
+                                  C.c_void_p(codes.data_ptr()), stream()))
+    torch.cuda.synchronize()
+    rc, _, rs = O.quantize_groups(w)
+    assert np.array_equal(codes.cpu().numpy().reshape(N_, K), rc)
+    assert np.array_equal(img.cpu().numpy(), O.pack_w4(rc, rs))
+
+
+def _run_gemm(bits, W, X, TM, splits=0):
+    """W [N,K] bf16 (np u16), X [M,K] bf16 -> fp32 [M,N] (sum of split partials)."""
+    N = _native()
+    Nn, K = W.shape
+    M = X.shape[0]
+    dw = dev_u16(W)
+    if bits == 16:
+        wp = torch.empty(Nn * K, dtype=torch.int16, device="cuda")
+        N.check(N.lib().ms_k_pack_bf16(C.c_void_p(dw.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), stream()))
+    else:
+        wp = torch.empty((Nn // 128) * (K // 128) * 8448, dtype=torch.uint8, device="cuda")
+        N.check(N.lib().ms_k_quant_w4(C.c_void_p(dw.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), None, stream()))
+    m_tiles = (M + TM - 1) // TM
+    xp = torch.zeros(m_tiles * TM * K, dtype=torch.int16, device="cuda")
+    dx = dev_u16(X)
+    N.check(N.lib().ms_k_pack_act(C.c_void_p(dx.data_ptr()), M, K, TM, C.c_void_p(xp.data_ptr()), stream()))
+    out = torch.empty(16 * M * Nn, dtype=torch.float32, device="cuda")
+    used = C.c_int()
+    N.check(N.lib().ms_k_gemm(bits, C.c_void_p(wp.data_ptr()), Nn, K, C.c_void_p(xp.data_ptr()), M, TM, splits,
+                              C.c_void_p(out.data_ptr()), C.byref(used), stream()))
+    torch.cuda.synchronize()
+    s = used.value
+    return out[: s * M * Nn].view(s, M, Nn).sum(0).cpu().numpy(), s
+
+
+@pytest.mark.parametrize("Nn,K,M,TM,splits", [
+    (128, 128, 1, 16, 1), (256, 256, 4, 16, 0), (512, 768, 33, 48, 3), (1024, 4096, 64, 64, 0),
+    (384, 1024, 300, 256, 1), (128, 128, 16, 16, 2)])
+def test_gemm_bf16(Nn, K, M, TM, splits):
+    W = O.gen_weight(21, 1, Nn * K, 1 / np.sqrt(K)).reshape(Nn, K)
+    X = O.gen_weight(21, 2, M * K, 1.0).reshape(M, K)
+    got, _ = _run_gemm(16, W, X, TM, splits)
+    ref = O.gemm_bf16(W, X)
+    # fp32 tensor-core accumulation vs fp64: |err| <= 1e-5 * sum|w x| (K <= 4096)
+    bound = 1e-5 * (np.abs(O.bf16_to_f32(X)) @ np.abs(O.bf16_to_f32(W)).T) + 1e-6
+    assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
+
+
+@pytest.mark.parametrize("Nn,K,M,TM,splits", [
+    (128, 128, 1, 16, 1), (256, 768, 4, 16, 0), (512, 1024, 64, 64, 0), (256, 256, 200, 208, 1)])
+def test_gemm_w4(Nn, K, M, TM, splits):
+    W = O.gen_weight(22, 1, Nn * K, 1 / np.sqrt(K)).reshape(Nn, K)
+    X = O.gen_weight(22, 2, M * K, 1.0).reshape(M, K)
+    got, _ = _run_gemm(4, W, X, TM, splits)
+    codes, _, s16 = O.quantize_groups(W)
+    Wq = O.dequant_w4(codes, s16)
+    ref = O.gemm_bf16(Wq, X)
+    bound = 1e-5 * (np.abs(O.bf16_to_f32(X)) @ np.abs(O.bf16_to_f32(Wq)).T) + 1e-6
+    assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
+
+
+@pytest.mark.parametrize("H,KVH,hd,ctxs,splits", [
+    (4, 2, 64, [1, 5, 16, 17, 100], 1),
+    (8, 8, 128, [1, 33, 250], 1),
+    (32, 8, 128, [2048, 7, 300], 4),
+    (8, 1, 128, [64, 129], 2)])
+def test_paged_attention(H, KVH, hd, ctxs, splits):
+    N = _native()
+    L, layer = 3, 1
+    rows = len(ctxs)
+    page_bytes = 16 * L * KVH * 2 * hd * 2
+    max_blocks = max((c + 15) // 16 for c in ctxs)
+    n_pages = rows * max_blocks + 5
+    rng = np.random.default_rng(0)
+    arena = O.f32_to_bf16(rng.uniform(-1, 1, n_pages * page_bytes // 2).astype(np.float32))
+    perm = rng.permutation(n_pages).astype(np.int32)  # scattered pages
+    pages = perm[: rows * max_blocks].reshape(rows, max_blocks)
+    q = rng.uniform(-1, 1, (rows, H, hd)).astype(np.float32)
+    d_arena = dev_u16(arena)
+    d_q = torch.from_numpy(q).cuda()
+    d_pages = torch.from_numpy(pages.copy()).cuda()
+    d_ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    out = torch.empty(rows * H * hd, dtype=torch.int16, device="cuda")
+    ws = torch.empty(splits * rows * H * (hd + 2) + 16, dtype=torch.float32, device="cuda")
+    N.check(N.lib().ms_k_attn_decode(C.c_void_p(d_q.data_ptr()), C.c_void_p(d_arena.data_ptr()), page_bytes, L,
+                                     layer, H, KVH, hd, C.c_void_p(d_pages.data_ptr()), max_blocks,
+                                     C.c_void_p(d_ctx.data_ptr()), rows, splits, C.c_void_p(ws.data_ptr()),
+                                     C.c_void_p(out.data_ptr()), stream()))
+    torch.cuda.synchronize()
+    got = O.bf16_to_f32(to_np_u16(out)).reshape(rows, H * hd)
+    head_elems = 16 * hd
+    for r, ctx in enumerate(ctxs):
+        k = np.empty((ctx, KVH, hd), np.uint16)
+        v = np.empty((ctx, KVH, hd), np.uint16)
+        for t in range(ctx):
+            base = pages[r, t // 16] * (page_bytes // 2) + layer * KVH * 2 * head_elems
+            for kh in range(KVH):
+                off = base + kh * 2 * head_elems + (t % 16) * hd
+                k[t, kh] = arena[off: off + hd]
+                v[t, kh] = arena[off + head_elems: off + head_elems + hd]
+        _, ref32 = O.attention(q[r].reshape(-1), k, v, H, KVH, hd)
+        # bf16 output rounding (2^-8 relative) + fp32 softmax/accumulation
+        np.testing.assert_allclose(got[r], ref32, rtol=1e-2, atol=2e-3)
