@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Headline benchmark: decode tok/s on Llama-2-7B-shaped mixed W4A16/BF16
+serving on B200 (BASELINE.json metric, configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): Llama-2-7B shape, random-init BF16
+weights, 64 sequences whose KV context is prefilled to 2048 tokens (synthetic
+KV values written into the paged arena), 16-token blocks; one "step" = one
+continuous-batching decode step of all 64 sequences (every layer, attention
+over the growing context, lm_head, greedy argmax).  Timed with 8 of the 32
+layers swapped to W4A16 g128 through the LayerSwapper (layers order[0..7] of
+the reference LIS profile); the all-BF16 step is reported beside it.
+
+N > 1: independent replicas (the path has no exchange step), one
+process per GPU under torchrun; value = sum over ranks of tokens / max-over-ranks
+time.  --impl reference: the CPU oracle port of the same decode step
+(oracle/ref_llama.c; the reference simulator has no decode math),
+a bounded sample (one layer-step + lm_head, extrapolated x L) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPE = dict(L=32, d=4096, H=32, KVH=32, hd=128, ffn=11008, V=32000)
+BATCH = 64
+CTX = 2048
+W4_LAYERS = [24, 14, 10, 20, 4, 19, 11, 5]  # reference LIS order[0..7]
+METRIC = "decode tok/s/GPU + P95 TTFT, 7B mixed W4A16/BF16, bursty trace, 1-8 B200"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 6 for i in range(4)
+                          if s[2 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- CPU oracle
+def cpu_sample(batch: int, ctx: int, w4: bool):
+    """One layer-step + lm_head of the 7B decode on the host (oracle port)."""
+    import oracle as O
+    L = O.lib()
+    L.ref_bench_decode_sample.restype = C.c_double
+    L.ref_bench_decode_sample.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                                          C.POINTER(C.c_double)]
+    cfg = O._Cfg(SHAPE["L"], SHAPE["d"], SHAPE["H"], SHAPE["KVH"], SHAPE["hd"], SHAPE["ffn"], SHAPE["V"],
+                 ctx + 1, 1e-5, 10000.0)
+    lm = C.c_double()
+    layer_s = L.ref_bench_decode_sample(C.byref(cfg), batch, ctx, 1 if w4 else 0, 7, C.byref(lm))
+    return layer_s, lm.value, L.ref_num_threads()
+
+
+def cpu_baseline():
+    ls16, lm, threads = cpu_sample(BATCH, CTX, False)
+    ls4, _, _ = cpu_sample(BATCH, CTX, True)
+    step_s = (SHAPE["L"] - len(W4_LAYERS)) * ls16 + len(W4_LAYERS) * ls4 + lm
+    return {"value": BATCH / step_s, "unit": "tok/s", "cores": threads, "kind": "port",
+            "sample": f"one BF16 and one W4 layer-step + lm_head of the B={BATCH} ctx={CTX} 7B decode step, "
+                      f"extrapolated to {SHAPE['L'] - len(W4_LAYERS)} BF16 + {len(W4_LAYERS)} W4 layers "
+                      f"(oracle/ref_llama.c, fp64 accumulation, OpenMP)"}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    O.build()
+    for _ in range(args.warmup):
+        cpu_sample(8, 256, False)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ls, lm, threads = cpu_sample(BATCH, CTX, False)
+        wall = time.perf_counter() - t0
+        times.append(SHAPE["L"] * ls + lm)
+    step_s = float(np.mean(times))
+    v = BATCH / step_s
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights/activations, fp64 accumulate",
+            "data": "synthetic", "config": {"workload": "llama2-7b-shape decode, batch 64, ctx 2048, BF16",
+                                           "global_batch": BATCH, "seq_len": CTX, "parallelism": "cpu"},
+            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "port",
+                             "sample": "each step: one layer-step + lm_head of the B=64 ctx=2048 7B decode "
+                                       "on all host threads, extrapolated x32 layers (the reference simulator "
+                                       "prices this step instead of computing it, SPEC.md:14)"},
+            "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def build_model(local_rank: int, extra_steps: int):
+    from paper_2506_02006_b200.device import DeviceModel, layer_pages
+    blocks_per_seq = (CTX + extra_steps + 16) // 16 + 1
+    kv_pages = BATCH * blocks_per_seq
+    w_pages = SHAPE["L"] * layer_pages(SHAPE, 16)
+    staging = len(W4_LAYERS) * layer_pages(SHAPE, 4) + 64
+    dev = DeviceModel(SHAPE, device=local_rank, max_batch=BATCH, max_prefill_tokens=256,
+                      max_pos=CTX + extra_steps + 32, arena_pages=kv_pages + w_pages + staging)
+    dev.weights_synthetic(7)
+    dev.hist_reserve(BATCH, CTX + extra_steps + 33)
+    dev.kv_attach(0, kv_pages)
+    table = np.arange(kv_pages, dtype=np.int64).reshape(BATCH, blocks_per_seq)
+    # scatter each sequence's blocks across the arena (interleaved ids)
+    table = np.arange(kv_pages, dtype=np.int64).reshape(blocks_per_seq, BATCH).T.copy()
+    dev.kv_fill_synthetic(table.reshape(-1), seed=11)
+    rng = np.random.default_rng(3)
+    for b in range(BATCH):
+        dev.hist_write(b, CTX - 1, rng.integers(0, SHAPE["V"], size=1).astype(np.int32))
+    return dev, table
+
+
+def attn_bytes_per_launch(pos: np.ndarray) -> float:
+    """sum_b ctx_b*KVH*hd*2*2 + sum_b ceil(ctx_b/16)*4 + B*H*hd*2*2 (q in, o out)."""
+    ctx = pos + 1
+    return float(np.sum(ctx) * SHAPE["KVH"] * SHAPE["hd"] * 4 + np.sum((ctx + 15) // 16) * 4 +
+                 BATCH * SHAPE["H"] * SHAPE["hd"] * 4)
+
+
+def run_ours(args):
+    rank, local_rank, world = dist_env()
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    total_steps = 2 * (args.warmup + args.steps) + args.e2e_steps + 8
+    dev, table = build_model(local_rank, total_steps)
+    slots = np.arange(BATCH, dtype=np.int32)
+    pos = np.full(BATCH, CTX - 1, dtype=np.int32)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def timed(k, prof=False):
+        nonlocal pos
+        dev.prof_attention(prof)
+        launches0 = dev.launch_count()
+        barrier()
+        dev.sync()
+        attn_bytes = 0.0
+        dev.timer_start()
+        for _ in range(k):
+            dev.decode(slots, pos, table, want_next=False)
+            attn_bytes += SHAPE["L"] * attn_bytes_per_launch(pos)
+            pos = pos + 1
+        ms = dev.timer_stop()
+        dev.sync()
+        barrier()
+        attn_ms, attn_n = dev.prof_attention_read() if prof else (0.0, 0)
+        dev.prof_attention(False)
+        return ms, dev.launch_count() - launches0, attn_bytes, attn_ms, attn_n
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- all-BF16 step
+    for _ in range(args.warmup):
+        dev.decode(slots, pos, table, want_next=False)
+        pos = pos + 1
+    ms16, _, _, _, _ = timed(args.steps)
+    ms16 = max_over_ranks(ms16)
+    # ---- LayerSwapper: 8 layers -> W4A16 (uploads overlap decode steps)
+    swap_ms = []
+    tickets = [dev.swap_begin(l, 4) for l in W4_LAYERS]
+    for t in tickets:
+        swap_ms.append(dev.swap_wait(t))
+        dev.swap_commit(t)
+    for _ in range(args.warmup):
+        dev.decode(slots, pos, table, want_next=False)
+        pos = pos + 1
+    with ClockSampler(local_rank) as clk:
+        ms, launches, attn_bytes, attn_ms, attn_n = timed(args.steps, prof=True)
+    ms = max_over_ranks(ms)
+    # ---- e2e through the C ABI with host buffers: H2D of the step inputs
+    # (tokens, slots, positions, block table) and D2H of the next tokens.
+    tokens = np.zeros(BATCH, np.int32)
+    barrier()
+    dev.sync()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        tokens, _ = dev.decode(slots, pos, table, tokens=tokens, want_next=True)
+        pos = pos + 1
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    max_blocks = dev.max_blocks
+    h2d = BATCH * (4 + max_blocks) * 4
+    d2h = BATCH * 4
+
+    hbm, peak_kind = peaks()
+    attn_avg_ms = attn_ms / max(attn_n, 1)
+    achieved = (attn_bytes / max(attn_n, 1)) / (attn_avg_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": BATCH * args.steps * world / (ms * 1e-3),
+        "unit": "tok/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16 activations, mixed W4A16-g128 / BF16 weights, fp32 accumulate",
+        "data": "synthetic (random-init weights, synthetic 2048-token KV context)",
+        "config": {"workload": "llama2-7b-shape decode, batch 64, ctx 2048->2048+steps, 8/32 layers W4A16 "
+                               "(LIS order[0..7]), 16-token paged KV",
+                   "global_batch": BATCH * world, "seq_len": CTX,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single replica",
+                   "l2": "inputs larger than L2 (13.2 GB weights + 68.7 GB KV per step)"},
+        "value_bf16_only": BATCH * args.steps * world / (ms16 * 1e-3),
+        "ms_per_step_bf16_only": ms16 / args.steps,
+        "p95_ttft_ms": None,
+        "swap_upload_ms": {"w4_layer_mean": float(np.mean(swap_ms))},
+        "e2e": {"value": BATCH * args.e2e_steps * world / e2e_s, "unit": "tok/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "attn_decode_kernel (paged GQA decode attention)",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "peak_kind": peak_kind, "traffic": None,
+                     "share_of_step": attn_ms / ms if ms > 0 else None},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dev.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

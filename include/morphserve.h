@@ -137,6 +137,16 @@ int ms_last_step_ms(ms_ctx* ctx, float* ms);
 /* Fill the listed blocks' KV with synthetic values (bench: "prefilled" context). */
 int ms_kv_fill_synthetic(ms_ctx* ctx, const int64_t* block_ids, int64_t n, uint64_t seed);
 
+/* ------------------------------------------------------- instrumentation
+ * Launch counter (every kernel this context launched), CUDA-event timer on the
+ * compute stream, and per-launch timing of the paged attention kernel (events
+ * bracketing each attention launch on its own stream). */
+int64_t ms_launch_count(ms_ctx* ctx);
+int ms_timer_start(ms_ctx* ctx);
+int ms_timer_stop(ms_ctx* ctx, float* ms);
+int ms_prof_attention(ms_ctx* ctx, int enable);
+int ms_prof_attention_read(ms_ctx* ctx, float* total_ms, int64_t* launches);
+
 /* ------------------------------------------ kernel-level entry points (tests)
  * Device pointers, caller-owned memory, caller stream. */
 int ms_k_gen_weight(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset, uint16_t* out,

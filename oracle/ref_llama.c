@@ -482,3 +482,95 @@ int ref_num_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------------ CPU baseline sample */
+/* Times one decoder-layer decode step for B sequences at context `ctx`
+ * (weights from the shared generator, KV filled with random bf16) plus the
+ * final norm + lm_head + argmax for B rows.  Used by bench.py's cpu_baseline
+ * and --impl reference legs as a BOUNDED sample of the 7B decode step (the
+ * full step is L layer-steps + one lm_head).  Returns layer seconds. */
+#include <time.h>
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+double ref_bench_decode_sample(const ref_cfg* c, int B, int ctx, int w4, uint64_t seed, double* lm_seconds) {
+  const int d = c->d, hd = c->hd, H = c->H, KVH = c->KVH, half = hd / 2, ffn = c->ffn;
+  const int64_t qkv_n = (int64_t)(H + 2 * KVH) * hd;
+  uint16_t* n1 = gen_alloc(seed, t_layer(0, W_NORM1), d, 0.1, 1.0);
+  uint16_t* n2 = gen_alloc(seed, t_layer(0, W_NORM2), d, 0.1, 1.0);
+  uint16_t* wqkv = gen_alloc(seed, t_layer(0, W_QKV), qkv_n * d, 1.0 / sqrt((double)d), 0.0);
+  uint16_t* wo = gen_alloc(seed, t_layer(0, W_O), (int64_t)d * H * hd, 1.0 / sqrt((double)(H * hd)), 0.0);
+  uint16_t* wgu = gen_alloc(seed, t_layer(0, W_GU), (int64_t)2 * ffn * d, 1.0 / sqrt((double)d), 0.0);
+  uint16_t* wd = gen_alloc(seed, t_layer(0, W_DOWN), (int64_t)d * ffn, 1.0 / sqrt((double)ffn), 0.0);
+  if (w4) {
+    uint16_t* t;
+    t = dequant_copy(wqkv, qkv_n, d); free(wqkv); wqkv = t;
+    t = dequant_copy(wo, d, (int64_t)H * hd); free(wo); wo = t;
+    t = dequant_copy(wgu, (int64_t)2 * ffn, d); free(wgu); wgu = t;
+    t = dequant_copy(wd, d, ffn); free(wd); wd = t;
+  }
+  const size_t per_seq = (size_t)ctx * KVH * hd;
+  uint16_t* kc = gen_alloc(seed ^ 0x55, 1000, (int64_t)(per_seq * B), 1.0, 0.0);
+  uint16_t* vc = gen_alloc(seed ^ 0xAA, 1001, (int64_t)(per_seq * B), 1.0, 0.0);
+  float* h = (float*)malloc((size_t)B * d * sizeof(float));
+  uint16_t* embed_row = gen_alloc(seed, T_EMBED, (int64_t)B * d, 1.0, 0.0);
+  for (int64_t i = 0; i < (int64_t)B * d; ++i) h[i] = bf2f(embed_row[i]);
+  uint16_t* xn = (uint16_t*)malloc((size_t)B * (ffn > d ? ffn : d) * 2);
+  float* y = (float*)malloc((size_t)B * (2 * ffn > qkv_n ? 2 * ffn : qkv_n) * sizeof(float));
+  uint16_t* att = (uint16_t*)malloc((size_t)B * H * hd * 2);
+  float* cs = (float*)malloc((size_t)half * sizeof(float));
+  float* sn = (float*)malloc((size_t)half * sizeof(float));
+  for (int i = 0; i < half; ++i) {
+    double a = (double)(ctx - 1) * pow(c->theta, -2.0 * (double)i / (double)hd);
+    cs[i] = (float)cos(a);
+    sn[i] = (float)sin(a);
+  }
+  const double t0 = now_s();
+  ref_rmsnorm(h, n1, B, d, c->eps, xn);
+  ref_gemm_bf16(wqkv, xn, B, qkv_n, d, y);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int b = 0; b < B; ++b) {
+    float* row = y + (int64_t)b * qkv_n;
+    for (int hh = 0; hh < H + KVH; ++hh) rope_inplace(row + hh * hd, hd, cs, sn);
+    uint16_t* kb = kc + (size_t)b * per_seq;
+    uint16_t* vb = vc + (size_t)b * per_seq;
+    for (int hh = 0; hh < KVH; ++hh)
+      for (int i = 0; i < hd; ++i) {
+        kb[((size_t)(ctx - 1) * KVH + hh) * hd + i] = f2bf(row[(H + hh) * hd + i]);
+        vb[((size_t)(ctx - 1) * KVH + hh) * hd + i] = f2bf(row[(H + KVH + hh) * hd + i]);
+      }
+    ref_attention(row, kb, vb, ctx, H, KVH, hd, att + (int64_t)b * H * hd, NULL);
+  }
+  ref_gemm_bf16(wo, att, B, d, (int64_t)H * hd, y);
+  for (int64_t i = 0; i < (int64_t)B * d; ++i) h[i] += y[i];
+  ref_rmsnorm(h, n2, B, d, c->eps, xn);
+  ref_gemm_bf16(wgu, xn, B, 2 * ffn, d, y);
+  for (int b = 0; b < B; ++b)
+    for (int j = 0; j < ffn; ++j)
+      xn[(int64_t)b * ffn + j] = f2bf(silu(y[(int64_t)b * 2 * ffn + j]) * y[(int64_t)b * 2 * ffn + ffn + j]);
+  ref_gemm_bf16(wd, xn, B, d, ffn, y);
+  for (int64_t i = 0; i < (int64_t)B * d; ++i) h[i] += y[i];
+  const double t1 = now_s();
+  if (lm_seconds) {
+    uint16_t* lm = gen_alloc(seed, T_LMHEAD, (int64_t)c->V * d, 1.0 / sqrt((double)d), 0.0);
+    uint16_t* nf = gen_alloc(seed, T_NORMF, d, 0.1, 1.0);
+    float* lg = (float*)malloc((size_t)B * c->V * sizeof(float));
+    const double t2 = now_s();
+    ref_rmsnorm(h, nf, B, d, c->eps, xn);
+    ref_gemm_bf16(lm, xn, B, c->V, d, lg);
+    volatile int sink = 0;
+    for (int b = 0; b < B; ++b) {
+      int best = 0;
+      for (int v = 1; v < c->V; ++v)
+        if (lg[(int64_t)b * c->V + v] > lg[(int64_t)b * c->V + best]) best = v;
+      sink += best;
+    }
+    *lm_seconds = now_s() - t2;
+    free(lm); free(nf); free(lg);
+  }
+  free(n1); free(n2); free(wqkv); free(wo); free(wgu); free(wd); free(kc); free(vc); free(h);
+  free(embed_row); free(xn); free(y); free(att); free(cs); free(sn);
+  return t1 - t0;
+}

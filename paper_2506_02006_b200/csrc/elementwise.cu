@@ -66,124 +66,155 @@ cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, cons
 }
 
 // --------------------------------- QKV: split-K sum, RoPE, q out, K/V -> KV pages
-__global__ void __launch_bounds__(256) qkv_post_kernel(const float* __restrict__ part, int splits, int M, int H,
-                                                       int KVH, int hd, const float* __restrict__ rc,
-                                                       const float* __restrict__ rs, const int32_t* __restrict__ pos,
-                                                       KvGeom kv, int layer, const int32_t* __restrict__ pages,
-                                                       const int32_t* __restrict__ page_row, int page_stride,
-                                                       float* __restrict__ q_out) {
-  const int m = blockIdx.x;
+// grid (rows, H + 2*KVH heads), one thread per rotation pair (i, i + hd/2).
+__global__ void qkv_post_kernel(const float* __restrict__ part, int splits, int M, int H, int KVH, int hd,
+                                const float* __restrict__ rc, const float* __restrict__ rs,
+                                const int32_t* __restrict__ pos, KvGeom kv, int layer,
+                                const int32_t* __restrict__ pages, const int32_t* __restrict__ page_row,
+                                int page_stride, float* __restrict__ q_out) {
+  const int m = blockIdx.x, hs = blockIdx.y, i = threadIdx.x;
   const int N = (H + 2 * KVH) * hd;
-  const int half = hd / 2;
+  const int half = hd >> 1;
   const int p = pos[m];
+  const size_t stride = (size_t)M * N;
+  const float* src = part + (size_t)m * N + (size_t)hs * hd + i;
+  float x0 = 0.f, x1 = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    x0 += src[s * stride];
+    x1 += src[s * stride + half];
+  }
+  if (hs < H + KVH) {  // q and k heads are rotated
+    const float c = rc[(size_t)p * half + i], sn = rs[(size_t)p * half + i];
+    const float y0 = x0 * c - x1 * sn;
+    const float y1 = x1 * c + x0 * sn;
+    x0 = y0;
+    x1 = y1;
+  }
+  if (hs < H) {
+    float* q = q_out + ((size_t)m * H + hs) * hd;
+    q[i] = x0;
+    q[i + half] = x1;
+    return;
+  }
   const int prow = page_row ? page_row[m] : m;
   const int32_t page = pages[(size_t)prow * page_stride + p / kv.block_tokens];
   const int slot = p % kv.block_tokens;
-  char* kvbase = kv.arena + (int64_t)page * kv.page_bytes + kv.layer_off(layer);
-  const float* cs = rc + (size_t)p * half;
-  const float* sn = rs + (size_t)p * half;
-  const size_t stride = (size_t)M * N;
-  const float* prow_part = part + (size_t)m * N;
-  // rotated pairs: q heads and k heads
-  const int npairs = (H + KVH) * half;
-  for (int idx = threadIdx.x; idx < npairs; idx += 256) {
-    const int hs = idx / half, i = idx - hs * half;
-    const int c0 = hs * hd + i, c1 = c0 + half;
-    float x0 = 0.f, x1 = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      x0 += prow_part[s * stride + c0];
-      x1 += prow_part[s * stride + c1];
-    }
-    const float y0 = x0 * cs[i] - x1 * sn[i];
-    const float y1 = x1 * cs[i] + x0 * sn[i];
-    if (hs < H) {
-      q_out[((size_t)m * H + hs) * hd + i] = y0;
-      q_out[((size_t)m * H + hs) * hd + i + half] = y1;
-    } else {
-      uint16_t* kp = reinterpret_cast<uint16_t*>(kvbase + (int64_t)(hs - H) * 2 * kv.head_bytes()) + slot * hd;
-      kp[i] = f2bf(y0);
-      kp[i + half] = f2bf(y1);
-    }
-  }
-  for (int idx = threadIdx.x; idx < KVH * hd; idx += 256) {
-    const int kh = idx / hd, dim = idx - kh * hd;
-    const int c = (H + KVH) * hd + idx;
-    float v = 0.f;
-    for (int s = 0; s < splits; ++s) v += prow_part[s * stride + c];
-    uint16_t* vp = reinterpret_cast<uint16_t*>(kvbase + (int64_t)kh * 2 * kv.head_bytes() + kv.head_bytes()) +
-                   slot * hd;
-    vp[dim] = f2bf(v);
-  }
+  const bool is_v = hs >= H + KVH;
+  const int kh = is_v ? hs - H - KVH : hs - H;
+  uint16_t* dst = reinterpret_cast<uint16_t*>(kv.arena + (int64_t)page * kv.page_bytes + kv.layer_off(layer) +
+                                              (int64_t)kh * 2 * kv.head_bytes() + (is_v ? kv.head_bytes() : 0)) +
+                  slot * hd;
+  dst[i] = f2bf(x0);
+  dst[i + half] = f2bf(x1);
 }
 
 cudaError_t qkv_post_launch(const float* part, int splits, int M, int H, int KVH, int hd, const float* rope_cos,
                             const float* rope_sin, const int32_t* pos, const KvGeom& kv, int layer,
                             const int32_t* pages, const int32_t* page_row, int page_stride, float* q_out,
                             cudaStream_t s) {
-  qkv_post_kernel<<<M, 256, 0, s>>>(part, splits, M, H, KVH, hd, rope_cos, rope_sin, pos, kv, layer, pages,
-                                    page_row, page_stride, q_out);
+  qkv_post_kernel<<<dim3(M, H + 2 * KVH), hd / 2, 0, s>>>(part, splits, M, H, KVH, hd, rope_cos, rope_sin, pos, kv,
+                                                          layer, pages, page_row, page_stride, q_out);
   return cudaGetLastError();
 }
 
 // ----------------------------------- residual add (split-K sum) + RMSNorm + pack
-__global__ void __launch_bounds__(256) residual_norm_kernel(const float* __restrict__ part, int splits, int M,
-                                                            int d, float* __restrict__ h,
-                                                            const uint16_t* __restrict__ w, float eps,
-                                                            uint16_t* __restrict__ x, int TM, int norm_row_begin) {
+// One CTA per row, float4 per thread; the normalised row is written straight
+// into the packed activation image of the next GEMM.
+__global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __restrict__ part, int splits, int M,
+                                                             int d, float* __restrict__ h,
+                                                             const uint16_t* __restrict__ w, float eps,
+                                                             uint16_t* __restrict__ x, int TM, int norm_row_begin) {
   __shared__ float red[32];
   const int m = blockIdx.x;
   const size_t stride = (size_t)M * d;
+  const int d4 = d >> 2;
+  float4* hr = reinterpret_cast<float4*>(h + (size_t)m * d);
+  const float4* pr = reinterpret_cast<const float4*>(part + (size_t)m * d);
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += 256) {
-    float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += part[s * stride + (size_t)m * d + i];
-    const float v = h[(size_t)m * d + i] + acc;
-    h[(size_t)m * d + i] = v;
-    ss += v * v;
+  for (int i4 = threadIdx.x; i4 < d4; i4 += blockDim.x) {
+    float4 v = hr[i4];
+    for (int s = 0; s < splits; ++s) {
+      const float4 a = pr[(s * stride) / 4 + i4];
+      v.x += a.x;
+      v.y += a.y;
+      v.z += a.z;
+      v.w += a.w;
+    }
+    hr[i4] = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   if (w == nullptr || m < norm_row_begin) return;  // uniform per block
-  ss = block_sum<256>(ss, red);
-  const float r = 1.0f / sqrtf(ss / (float)d + eps);
-  const int mo = m - norm_row_begin;
-  for (int i = threadIdx.x; i < d; i += 256) {
-    const float v = h[(size_t)m * d + i];
-    x[act_off(mo, i, d, TM)] = f2bf((v * r) * bf2f(w[i]));
+  // block reduction
+  ss = warp_sum(ss);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[wid] = ss;
+  __syncthreads();
+  if (wid == 0) {
+    float t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.f;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
   }
+  __syncthreads();
+  const float r = 1.0f / sqrtf(red[0] / (float)d + eps);
+  const int mo = m - norm_row_begin;
+  const uint2* w4 = reinterpret_cast<const uint2*>(w);
+  for (int i4 = threadIdx.x; i4 < d4; i4 += blockDim.x) {
+    const float4 v = hr[i4];
+    const uint2 wv = w4[i4];
+    uint2 o;
+    o.x = pack_bf2((v.x * r) * __uint_as_float(wv.x << 16), (v.y * r) * __uint_as_float(wv.x & 0xFFFF0000u));
+    o.y = pack_bf2((v.z * r) * __uint_as_float(wv.y << 16), (v.w * r) * __uint_as_float(wv.y & 0xFFFF0000u));
+    *reinterpret_cast<uint2*>(x + act_off(mo, i4 * 4, d, TM)) = o;
+  }
+}
+
+static int norm_threads(int d) {
+  int t = d / 4;
+  if (t > 1024) t = 1024;
+  return (t + 31) / 32 * 32;
 }
 
 cudaError_t residual_norm_launch(const float* part, int splits, int M, int d, float* h, const uint16_t* norm_w,
                                  float eps, uint16_t* x_packed, int TM, cudaStream_t s) {
-  residual_norm_kernel<<<M, 256, 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM, 0);
+  residual_norm_kernel<<<M, norm_threads(d), 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM, 0);
   return cudaGetLastError();
 }
 
 cudaError_t residual_norm_rows_launch(const float* part, int splits, int M, int d, float* h,
                                       const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
                                       int norm_row_begin, cudaStream_t s) {
-  residual_norm_kernel<<<M, 256, 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM, norm_row_begin);
+  residual_norm_kernel<<<M, norm_threads(d), 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM,
+                                                     norm_row_begin);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------- SiLU(gate)*up
 __global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int M, int ffn,
                                 uint16_t* __restrict__ x, int TM) {
-  const size_t total = (size_t)M * ffn;
-  const size_t stride = (size_t)M * 2 * ffn;
+  const int f4 = ffn >> 2;
+  const size_t total = (size_t)M * f4;
+  const size_t stride4 = (size_t)M * 2 * ffn / 4;
+  const float4* p4 = reinterpret_cast<const float4*>(part);
   for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-    const int m = (int)(idx / ffn), j = (int)(idx - (size_t)m * ffn);
-    float g = 0.f, u = 0.f;
+    const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f), u = g;
+    const size_t base = (size_t)m * 2 * f4 + j4;
     for (int s = 0; s < splits; ++s) {
-      g += part[s * stride + (size_t)m * 2 * ffn + j];
-      u += part[s * stride + (size_t)m * 2 * ffn + ffn + j];
+      const float4 a = p4[s * stride4 + base];
+      const float4 b = p4[s * stride4 + base + f4];
+      g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
+      u.x += b.x; u.y += b.y; u.z += b.z; u.w += b.w;
     }
-    const float a = (g / (1.0f + expf(-g))) * u;
-    x[act_off(m, j, ffn, TM)] = f2bf(a);
+    uint2 o;
+    o.x = pack_bf2((g.x / (1.0f + expf(-g.x))) * u.x, (g.y / (1.0f + expf(-g.y))) * u.y);
+    o.y = pack_bf2((g.z / (1.0f + expf(-g.z))) * u.z, (g.w / (1.0f + expf(-g.w))) * u.w);
+    *reinterpret_cast<uint2*>(x + act_off(m, j4 * 4, ffn, TM)) = o;
   }
 }
 
 cudaError_t silu_mul_launch(const float* part, int splits, int M, int ffn, uint16_t* x_packed, int TM,
                             cudaStream_t s) {
-  const size_t total = (size_t)M * ffn;
+  const size_t total = (size_t)M * ffn / 4;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   silu_mul_kernel<<<blocks, 256, 0, s>>>(part, splits, M, ffn, x_packed, TM);

@@ -188,6 +188,13 @@ struct ms_ctx {
 
   int32_t* hist = nullptr;
   int32_t hist_slots = 0, hist_len = 0;
+
+  // instrumentation: launch counter and per-launch attention timing
+  int64_t launches = 0;
+  bool prof_attn = false;
+  std::vector<cudaEvent_t> prof_ev;  // pairs
+  size_t prof_used = 0;
+  cudaEvent_t tm0 = nullptr, tm1 = nullptr;
 };
 
 namespace {
@@ -316,7 +323,18 @@ int gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
   const int s = pick_splits(c, w4, w.N, w.K, M, TM);
   CK(ms::gemm_launch(w, w4, c->x, M, TM, s, c->part, c->compute));
+  c->launches += 1;
   return s;
+}
+
+void prof_mark(ms_ctx* c) {
+  if (!c->prof_attn) return;
+  if (c->prof_used == c->prof_ev.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->prof_ev.push_back(e);
+  }
+  CK(cudaEventRecord(c->prof_ev[c->prof_used++], c->compute));
 }
 
 int attn_splits(ms_ctx* c, int rows, int max_ctx) {
@@ -337,12 +355,14 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   const int d = D.hidden, H = D.num_heads, KVH = D.num_kv_heads, hd = D.head_dim;
   CK(ms::embed_norm_launch(c->embed, d_tokens, c->hist, d_slot, d_pos, c->hist_len, M, d, c->norms, D.rms_eps,
                            c->h, c->x, TM, c->compute));
+  c->launches += 1;
   const int asplits = attn_splits(c, M, max_ctx);
   for (int l = 0; l < D.num_layers; ++l) {
     const bool w4 = c->layers[l].bits == 4;
     int s = gemm(c, mat_weights(c, l, 0), w4, M, TM);
     CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
                            d_page_row, page_stride, c->q, c->compute));
+    c->launches += 1;
     ms::AttnArgs a{};
     a.q = c->q;
     a.kv = c->kv;
@@ -361,18 +381,24 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     a.out = c->x;
     a.out_packed = 1;
     a.TM = TM;
+    prof_mark(c);
     CK(ms::attn_decode_launch(a, c->compute));
+    prof_mark(c);
+    c->launches += asplits > 1 ? 2 : 1;
     s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
     CK(ms::residual_norm_launch(c->part, s, M, d, c->h, c->norms + ((size_t)l * 2 + 1) * d, D.rms_eps, c->x, TM,
                                 c->compute));
+    c->launches += 1;
     s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
     CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
+    c->launches += 1;
     s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
     const bool last = l == D.num_layers - 1;
     const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
     const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
     CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out,
                                      last ? final_row_begin : 0, c->compute));
+    c->launches += 1;
   }
   const int Mo = M - final_row_begin;
   const int TMo = round16(Mo) > 256 ? 256 : round16(Mo);
@@ -380,6 +406,7 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   const int s = gemm(c, lw, false, Mo, TMo);
   CK(ms::argmax_launch(c->part, s, Mo, D.vocab, want_logits ? c->logits : nullptr, c->next, c->hist,
                        d_slot + final_row_begin, d_pos + final_row_begin, c->hist_len, c->compute));
+  c->launches += 1;
 }
 
 Staging& next_staging(ms_ctx* c, size_t words) {
@@ -542,6 +569,9 @@ int ms_ctx_destroy(ms_ctx* c) {
     if (st.used) cudaEventDestroy(st.used);
   }
   for (auto e : c->events) cudaEventDestroy(e);
+  for (auto e : c->prof_ev) cudaEventDestroy(e);
+  if (c->tm0) cudaEventDestroy(c->tm0);
+  if (c->tm1) cudaEventDestroy(c->tm1);
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
@@ -890,6 +920,7 @@ int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float
     if (b->tokens) {
       hist_scatter_kernel<<<(n + 127) / 128, 128, 0, c->compute>>>(c->hist, c->hist_len, d_slot, d_pos, d_tok, n);
       CK(cudaGetLastError());
+      c->launches += 1;
     }
     const int TM = std::min(256, round16(n));
     forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, logits_out != nullptr);
@@ -963,6 +994,48 @@ int ms_kv_fill_synthetic(ms_ctx* c, const int64_t* ids, int64_t n, uint64_t seed
     CK(ms::fill_kv_launch(c->kv, d, (int)n, seed, c->compute));
     CK(cudaStreamSynchronize(c->compute));
     cudaFree(d);
+  });
+}
+
+// ------------------------------------------------------------ instrumentation
+int64_t ms_launch_count(ms_ctx* c) { return c ? c->launches : -1; }
+
+int ms_timer_start(ms_ctx* c) {
+  return guard([&] {
+    if (!c->tm0) {
+      CK(cudaEventCreate(&c->tm0));
+      CK(cudaEventCreate(&c->tm1));
+    }
+    CK(cudaEventRecord(c->tm0, c->compute));
+  });
+}
+
+int ms_timer_stop(ms_ctx* c, float* ms_out) {
+  return guard([&] {
+    CK(cudaEventRecord(c->tm1, c->compute));
+    CK(cudaEventSynchronize(c->tm1));
+    CK(cudaEventElapsedTime(ms_out, c->tm0, c->tm1));
+  });
+}
+
+int ms_prof_attention(ms_ctx* c, int enable) {
+  return guard([&] {
+    c->prof_attn = enable != 0;
+    c->prof_used = 0;
+  });
+}
+
+int ms_prof_attention_read(ms_ctx* c, float* total_ms, int64_t* launches) {
+  return guard([&] {
+    CK(cudaStreamSynchronize(c->compute));
+    double t = 0.0;
+    for (size_t i = 0; i + 1 < c->prof_used; i += 2) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->prof_ev[i], c->prof_ev[i + 1]));
+      t += ms;
+    }
+    *total_ms = (float)t;
+    *launches = (int64_t)(c->prof_used / 2);
   });
 }
 

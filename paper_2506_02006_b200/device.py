@@ -181,3 +181,24 @@ class DeviceModel:
     def kv_fill_synthetic(self, block_ids, seed: int):
         a = np.ascontiguousarray(block_ids, np.int64)
         N.check(self.lib.ms_kv_fill_synthetic(self.h, N.i64p(a), a.size, seed))
+
+    # -- instrumentation
+    def launch_count(self) -> int:
+        return self.lib.ms_launch_count(self.h)
+
+    def timer_start(self):
+        N.check(self.lib.ms_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_float()
+        N.check(self.lib.ms_timer_stop(self.h, C.byref(ms)))
+        return ms.value
+
+    def prof_attention(self, enable: bool):
+        N.check(self.lib.ms_prof_attention(self.h, int(enable)))
+
+    def prof_attention_read(self):
+        ms = C.c_float()
+        n = C.c_int64()
+        N.check(self.lib.ms_prof_attention_read(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
