@@ -91,6 +91,8 @@ int ms_swap_poll(ms_ctx* ctx, uint64_t ticket, int* done);
 int ms_swap_wait(ms_ctx* ctx, uint64_t ticket, float* upload_ms);
 int ms_swap_commit(ms_ctx* ctx, uint64_t ticket, int64_t* pages_freed);
 int ms_layer_bits(ms_ctx* ctx, int layer);
+/* Between runs: restore every layer to BF16 and unmap every KV block id. */
+int ms_reset_state(ms_ctx* ctx);
 
 /* ------------------------------------------------------ KV resizer (a7,a9)
  * Logical block ids stay owned by the host KvBlockPool (bit-exact with

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("ms_swap_wait", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_float)]),
     ("ms_swap_commit", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int64)]),
     ("ms_layer_bits", C.c_int, [_P, C.c_int]),
+    ("ms_reset_state", C.c_int, [_P]),
     ("ms_kv_attach", C.c_int, [_P, C.c_int64, C.c_int64]),
     ("ms_kv_detach", C.c_int, [_P, C.POINTER(C.c_int64), C.c_int64]),
     ("ms_free_pages", C.c_int64, [_P]),

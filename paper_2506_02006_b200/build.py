@@ -62,8 +62,46 @@ def build_device_lib(verbose: bool = False) -> str:
     return out
 
 
+HOST_SOURCES = ["core.cpp", "engine.cpp", "device_backend.cpp"]
+CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter"]
+
+
+def build_host_lib(verbose: bool = False) -> str:
+    """libmorphserve_host.so: the C++ engine / KV pool / controller (links libmorphserve.so)."""
+    host = os.path.join(CSRC, "host")
+    srcs = [os.path.join(host, s) for s in HOST_SOURCES]
+    deps = srcs + [os.path.join(host, h) for h in os.listdir(host) if h.endswith(".hpp")]
+    deps.append(os.path.join(ROOT, "include", "morphserve.h"))
+    out = os.path.join(LIB, "libmorphserve_host.so")
+    if _stale(out, deps + [os.path.join(LIB, "libmorphserve.so")]):
+        r = _run(["g++", *CXXFLAGS, "-shared", "-o", out, *srcs, "-L" + LIB, "-lmorphserve",
+                  "-Wl,-rpath,$ORIGIN"])
+        if verbose and r.stderr:
+            print(r.stderr, file=sys.stderr)
+    return out
+
+
+def build_pymodule(verbose: bool = False) -> str:
+    import sysconfig
+
+    import pybind11
+    host = os.path.join(CSRC, "host")
+    src = os.path.join(host, "bindings.cpp")
+    out = os.path.join(PKG, "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
+    deps = [src] + [os.path.join(host, h) for h in os.listdir(host) if h.endswith(".hpp")]
+    if _stale(out, deps + [os.path.join(LIB, "libmorphserve_host.so")]):
+        r = _run(["g++", *CXXFLAGS, "-shared", "-o", out, src, "-I" + pybind11.get_include(),
+                  "-I" + sysconfig.get_paths()["include"], "-L" + LIB, "-lmorphserve_host", "-lmorphserve",
+                  "-Wl,-rpath,$ORIGIN/lib"])
+        if verbose and r.stderr:
+            print(r.stderr, file=sys.stderr)
+    return out
+
+
 def build_all(verbose: bool = False) -> None:
     build_device_lib(verbose)
+    build_host_lib(verbose)
+    build_pymodule(verbose)
 
 
 if __name__ == "__main__":

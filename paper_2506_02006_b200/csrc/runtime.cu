@@ -804,6 +804,31 @@ int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
   });
 }
 
+int ms_reset_state(ms_ctx* c) {
+  return guard([&] {
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->compute));
+    CK(cudaStreamSynchronize(c->copy));
+    for (int l = 0; l < c->desc.num_layers; ++l) {
+      Layer& L = c->layers[l];
+      if (L.in_flight) fail(MS_ELOGIC, "reset: swap in flight");
+      if (L.bits == 16) continue;
+      uint64_t t = 0;
+      if (ms_swap_begin(c, l, 16, &t) != MS_OK) fail(MS_ERUNTIME, g_err);
+      CK(cudaStreamSynchronize(c->copy));
+      if (ms_swap_commit(c, t, nullptr) != MS_OK) fail(MS_ERUNTIME, g_err);
+    }
+    std::vector<int32_t> pages;
+    for (auto& p : c->id_page)
+      if (p >= 0) {
+        pages.push_back(p);
+        p = -1;
+      }
+    give_pages(c, pages, compute_fence(c));
+    CK(cudaStreamSynchronize(c->compute));
+  });
+}
+
 int ms_layer_bits(ms_ctx* c, int layer) {
   if (!c || layer < 0 || layer >= c->desc.num_layers) return -1;
   return c->layers[layer].bits;

@@ -1,0 +1,132 @@
+"""The serving engine driving the B200 (virtual clock): the event log / block
+tables must be byte-identical to the CPU-only run (and to the reference when
+oracle/_ref is built), and every token the GPU generated -- across prefills,
+re-prefills after preemption, continuous-batching decode steps, layer swaps to
+W4 and back, KV attach/detach -- must be what the CPU oracle predicts when it
+replays the same launches with the same per-layer precision (teacher forced;
+near ties within the bf16 logit tolerance are allowed and counted).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TINY = dict(L=4, d=256, H=4, KVH=2, hd=64, ffn=768, V=1024)
+PB = 16 * 4 * 2 * 2 * 64 * 2  # page = one KV block (all layers) = 32 KiB
+
+
+def tiny_config(trace_path, seq_path, static_blocks=40):
+    return {
+        "seed": 11,
+        "model": {"num_layers": 4, "layer_bytes": {"full": 48 * PB, "q8": 16 * PB, "q4": 16 * PB, "q3": 16 * PB}},
+        "kv": {"block_tokens": 16, "block_bytes": PB, "static_capacity_blocks": static_blocks},
+        "budget": {"device_bytes": (4 * 48 + static_blocks + 40) * PB, "reserve_bytes": 40 * PB},
+        "cost": {"prefill_ms_per_token": 0.05, "attn_ms_per_kv_block": 0.0001},
+        "controller": {"performance": {"kv_trigger": 0.6, "kv_low": 0.4, "hold_ms": 50.0, "max_swapped_layers": 2,
+                                       "swap_step": 1},
+                       "accuracy": {"kv_trigger": 0.9, "max_swapped_layers": 1}},
+        "toy": {"num_layers": 4},
+        "workload": {"trace_file": trace_path},
+        "sequence_file": seq_path,
+    }
+
+
+@pytest.fixture(scope="module")
+def setup(tmp_path_factory):
+    from paper_2506_02006_b200 import morphsim as M
+    from paper_2506_02006_b200.device import DeviceModel, layer_pages
+    assert layer_pages(TINY, 16) == 48 and layer_pages(TINY, 4) == 16
+    d = tmp_path_factory.mktemp("eng")
+    trace = d / "trace.csv"
+    trace.write_text("".join(f"{i * 3},{40 + (i % 3) * 8},{24 + (i % 4) * 4}\n" for i in range(14)) +
+                     "".join(f"{400 + i * 40},{32},{16}\n" for i in range(6)))
+    seq = str(d / "seq.json")
+    M.save_sequence(M.baseline_sequence("back_to_front", 4), seq)
+    cfg = tiny_config(str(trace), seq)
+    dev = DeviceModel(TINY, max_batch=32, max_prefill_tokens=128, max_pos=128, arena_pages=(4 * 48 + 40 + 40) + 32)
+    dev.weights_synthetic(7)
+    yield M, cfg, dev
+    dev.close()
+
+
+def test_device_backed_run_is_bit_exact_and_tokens_match_oracle(setup):
+    M, cfg, dev = setup
+    rep_cpu, log_cpu, tl_cpu = M.run_arm_full(cfg, "morph-performance")
+    rep, log, tl = M.run_arm_full(cfg, "morph-performance", device=dev, record=True)
+    assert log == log_cpu and tl == tl_cpu
+    calls = rep.pop("device_calls")
+    for r in (rep, rep_cpu):
+        r.pop("device")
+    assert rep == rep_cpu
+    assert rep["morph"]["swap_events"] >= 1 and rep["kv"]["peak_capacity_blocks"] > 40
+    assert "KV_ATTACH" in log
+    if O.have_ref_core():
+        ref = O.ref_core()
+        import tempfile
+        with tempfile.TemporaryDirectory() as td:
+            r_ref = json.loads(ref.run_arm(json.dumps(cfg), "morph-performance", td))
+            assert open(os.path.join(td, "events_morph-performance.log")).read() == log
+        rep.pop("fingerprint")
+        r_ref.pop("fingerprint")
+        assert rep == r_ref
+
+    # ---- replay every device launch on the CPU oracle
+    from paper_2506_02006_b200 import _core
+    from paper_2506_02006_b200.morphsim import resolve_workload
+    trace = resolve_workload(M.config_from_json(cfg))
+    n_req = len(trace.events)
+    hist = {r: dev.hist_read(r, 0, trace.events[r].prompt_tokens + trace.events[r].output_tokens)
+            for r in range(n_req)}
+    for r in range(n_req):
+        P = trace.events[r].prompt_tokens
+        assert np.array_equal(hist[r][:P], np.array(_core.synthetic_prompt(cfg["seed"], r, P, TINY["V"])))
+    model = O.RefModel(dict(TINY, max_pos=256), 7)
+    seqs, checked, ties = {}, 0, []
+    bits_now = [16] * 4
+
+    def set_bits(bits):
+        for l, b in enumerate(bits):
+            if bits_now[l] != b:
+                model.set_precision(l, b)
+                bits_now[l] = b
+
+    for c in calls:
+        set_bits(c["bits"])
+        if c["kind"] == "P":
+            r, n = c["reqs"][0], c["pos"][0]
+            seqs[r] = model.new_seq(256)  # (re-)prefill rebuilds the whole KV
+            nxt, lg = model.prefill(seqs[r], hist[r][:n])
+            pairs = [(r, n, nxt, lg)]
+        else:
+            toks = [hist[r][p] for r, p in zip(c["reqs"], c["pos"])]
+            for r, p in zip(c["reqs"], c["pos"]):
+                assert O.lib().ref_seq_len(seqs[r]) == p  # KV footprint = position of the input token
+            nxt, lg = model.forward([seqs[r] for r in c["reqs"]], toks)
+            pairs = [(r, p + 1, nxt[i], lg[i]) for i, (r, p) in enumerate(zip(c["reqs"], c["pos"]))]
+        for r, at, rtok, rlog in pairs:
+            if at >= len(hist[r]):
+                continue
+            g = int(hist[r][at])
+            checked += 1
+            if g != int(rtok):
+                margin = float(rlog[rtok] - rlog[g])
+                assert margin <= 2e-3 * float(np.max(np.abs(rlog))), (c, r, at, margin)
+                ties.append((r, at, margin))
+    assert checked >= 300
+    assert len(ties) <= 0.02 * checked, ties
+    model.close()
+
+
+def test_device_clock_run_measures_real_time(setup):
+    M, cfg, dev = setup
+    rep, log, _ = M.run_arm_full(cfg, "morph-performance", device=dev, clock="device")
+    assert rep["requests"]["completed"] == rep["requests"]["total"]
+    d = rep["device"]
+    assert d["decode_steps"] > 0 and d["decode_ms"] > 0 and d["prefill_ms"] > 0
+    # durations in the log are the measured GPU times, not the cost model's
+    assert rep["ttft_ms"]["p95"] is not None
