@@ -135,8 +135,7 @@ def test_validation_errors_are_value_errors():
     with pytest.raises(ValueError):
         M.config_from_json(bad)
     with pytest.raises(ValueError):
-        M.run_arm(dict(cfg, sequence_file=None) if False else {k: v for k, v in cfg.items() if k != "sequence_file"},
-                  "morph-performance")
+        M.run_arm({k: v for k, v in cfg.items() if k != "sequence_file"}, "morph-performance")
 
 
 def test_morph_without_pressure_equals_static_full(tmp_path):
