@@ -156,8 +156,11 @@ int ms_k_gen_weight(uint64_t seed, uint64_t tensor, int64_t n, double scale, dou
 int ms_k_pack_bf16(const uint16_t* w, int N, int K, uint16_t* out, void* stream);
 int ms_k_quant_w4(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, void* stream);
 int ms_k_pack_act(const uint16_t* x, int M, int K, int TM, uint16_t* out, void* stream);
-/* out[s][m][n] fp32 partials of W(packed, bits) x X(packed, TM); splits<=0 = auto.
- * Returns the split count used through *splits_used. */
+/* out[s][m][n] fp32 partials of W(packed, bits) x X(packed, TM) from the
+ * persistent stream-K kernel; `splits` > 0 caps the CTA count (<= 0: one per
+ * SM).  *splits_used = partial slots the plan may write; `out` must hold that
+ * many [M][N] slots and be zeroed (a tile writes only the slots it uses), the
+ * result is the sum over slots. */
 int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_packed, int M, int TM, int splits,
               float* out, int* splits_used, void* stream);
 /* Paged decode attention on a caller-provided arena (page_bytes per page,

@@ -145,7 +145,9 @@ void ref_pack_bf16(const uint16_t* w, int64_t N, int64_t K, uint16_t* out) {
 /* W4 chunk layout: chunk (n_tile, group g of 128 K) = 8448 bytes:
  *   bytes [0, 8192): codes as [j 4][row 128][16 B]; the 16 B of (j,row) hold
  *   K-elements [32j, 32j+32) of the group, 4 u32 words, word w holds elements
- *   32j+8w .. +7 with element e at bits 4e..4e+3, stored as (code + 8).
+ *   32j+8w .. +7 stored as (code + 8): even elements e=2i in the low half at
+ *   bits 4i, odd elements e=2i+1 in the high half at bits 16+4i (so that
+ *   (word >> 4i) & 0x000F000F is the bf16x2 pair (e_2i, e_2i+1)).
  *   bytes [8192, 8448): 128 bf16 scales, one per row. */
 void ref_pack_w4(const int8_t* codes, const uint16_t* scales_bf16, int64_t N, int64_t K,
                  uint8_t* out) {
@@ -162,7 +164,7 @@ void ref_pack_w4(const int8_t* codes, const uint16_t* scales_bf16, int64_t N, in
           for (int e = 0; e < 8; ++e) {
             int k = g * 128 + j * 32 + w * 8 + e;
             uint32_t nib = (uint32_t)(codes[n * K + k] + 8) & 0xFu;
-            v |= nib << (4 * e);
+            v |= nib << ((e & 1) * 16 + (e >> 1) * 4);
           }
           words[w] = v;
         }

@@ -36,6 +36,8 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
   uint64_t* empty = full + kAttnStages;
   float* scratch = reinterpret_cast<float*>(empty + kAttnStages);  // [4][G][HD] acc + [4][G][2] m,l
 
+  pdl_wait();
+  pdl_trigger();
   const int kvh = blockIdx.x, row = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ctx = a.ctx_len[row];
@@ -204,6 +206,8 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
 
 template <int HD>
 __global__ void attn_combine_kernel(AttnArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x, h = blockIdx.y, dim = threadIdx.x;
   float M = -INFINITY;
   for (int s = 0; s < a.splits; ++s) M = fmaxf(M, a.part_ml[(((size_t)s * a.rows + row) * a.H + h) * 2]);
@@ -234,11 +238,9 @@ static cudaError_t launch_g(const AttnArgs& a, cudaStream_t stream) {
     attr = true;
   }
   dim3 grid(a.KVH, a.rows, a.splits);
-  attn_decode_kernel<HD, G, BT><<<grid, 160, smem, stream>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(attn_decode_kernel<HD, G, BT>, grid, dim3(160), smem, stream, a);
   if (e != cudaSuccess || a.splits == 1) return e;
-  attn_combine_kernel<HD><<<dim3(a.rows, a.H), HD, 0, stream>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(attn_combine_kernel<HD>, dim3(a.rows, a.H), dim3(HD), 0, stream, a);
 }
 
 template <int HD>

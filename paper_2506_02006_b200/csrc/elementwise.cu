@@ -39,6 +39,8 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const uint16_t* __restr
                                                          const uint16_t* __restrict__ w, float eps,
                                                          float* __restrict__ h, uint16_t* __restrict__ x, int TM) {
   __shared__ float red[32];
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int tok = tokens ? tokens[m] : hist[(size_t)slot[m] * hist_stride + pos[m]];
   const uint16_t* e = embed + (size_t)tok * d;
@@ -60,29 +62,30 @@ cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, cons
                               const int32_t* slot, const int32_t* pos, int hist_stride, int M, int d,
                               const uint16_t* norm_w, float eps, float* h, uint16_t* x_packed, int TM,
                               cudaStream_t s) {
-  embed_norm_kernel<<<M, 256, 0, s>>>(embed, tokens, hist, slot, pos, hist_stride, d, norm_w, eps, h, x_packed,
-                                      TM);
-  return cudaGetLastError();
+  return launch_pdl(embed_norm_kernel, dim3(M), dim3(256), 0, s, embed, tokens, hist, slot, pos, hist_stride, d,
+                    norm_w, eps, h, x_packed, TM);
 }
 
 // --------------------------------- QKV: split-K sum, RoPE, q out, K/V -> KV pages
 // grid (rows, H + 2*KVH heads), one thread per rotation pair (i, i + hd/2).
-__global__ void qkv_post_kernel(const float* __restrict__ part, int splits, int M, int H, int KVH, int hd,
+__global__ void qkv_post_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int H, int KVH, int hd,
                                 const float* __restrict__ rc, const float* __restrict__ rs,
                                 const int32_t* __restrict__ pos, KvGeom kv, int layer,
                                 const int32_t* __restrict__ pages, const int32_t* __restrict__ page_row,
                                 int page_stride, float* __restrict__ q_out) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x, hs = blockIdx.y, i = threadIdx.x;
   const int N = (H + 2 * KVH) * hd;
   const int half = hd >> 1;
   const int p = pos[m];
   const size_t stride = (size_t)M * N;
-  const float* src = part + (size_t)m * N + (size_t)hs * hd + i;
+  const int c0 = hs * hd + i;
+  const float* src = part + (size_t)m * N + c0;
   float x0 = 0.f, x1 = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    x0 += src[s * stride];
-    x1 += src[s * stride + half];
-  }
+  const int n0 = part_slots(plan, m, c0), n1 = part_slots(plan, m, c0 + half);
+  for (int s = 0; s < n0; ++s) x0 += src[s * stride];
+  for (int s = 0; s < n1; ++s) x1 += src[s * stride + half];
   if (hs < H + KVH) {  // q and k heads are rotated
     const float c = rc[(size_t)p * half + i], sn = rs[(size_t)p * half + i];
     const float y0 = x0 * c - x1 * sn;
@@ -108,23 +111,24 @@ __global__ void qkv_post_kernel(const float* __restrict__ part, int splits, int 
   dst[i + half] = f2bf(x1);
 }
 
-cudaError_t qkv_post_launch(const float* part, int splits, int M, int H, int KVH, int hd, const float* rope_cos,
+cudaError_t qkv_post_launch(const float* part, const GemmPlanDev& plan, int M, int H, int KVH, int hd, const float* rope_cos,
                             const float* rope_sin, const int32_t* pos, const KvGeom& kv, int layer,
                             const int32_t* pages, const int32_t* page_row, int page_stride, float* q_out,
                             cudaStream_t s) {
-  qkv_post_kernel<<<dim3(M, H + 2 * KVH), hd / 2, 0, s>>>(part, splits, M, H, KVH, hd, rope_cos, rope_sin, pos, kv,
-                                                          layer, pages, page_row, page_stride, q_out);
-  return cudaGetLastError();
+  return launch_pdl(qkv_post_kernel, dim3(M, H + 2 * KVH), dim3(hd / 2), 0, s, part, plan, M, H, KVH, hd, rope_cos,
+                    rope_sin, pos, kv, layer, pages, page_row, page_stride, q_out);
 }
 
 // ----------------------------------- residual add (split-K sum) + RMSNorm + pack
 // One CTA per row, float4 per thread; the normalised row is written straight
 // into the packed activation image of the next GEMM.
-__global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __restrict__ part, int splits, int M,
+__global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __restrict__ part, GemmPlanDev plan, int M,
                                                              int d, float* __restrict__ h,
                                                              const uint16_t* __restrict__ w, float eps,
                                                              uint16_t* __restrict__ x, int TM, int norm_row_begin) {
   __shared__ float red[32];
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const size_t stride = (size_t)M * d;
   const int d4 = d >> 2;
@@ -133,7 +137,8 @@ __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __rest
   float ss = 0.f;
   for (int i4 = threadIdx.x; i4 < d4; i4 += blockDim.x) {
     float4 v = hr[i4];
-    for (int s = 0; s < splits; ++s) {
+    const int ns = part_slots(plan, m, i4 * 4);
+    for (int s = 0; s < ns; ++s) {
       const float4 a = pr[(s * stride) / 4 + i4];
       v.x += a.x;
       v.y += a.y;
@@ -174,23 +179,24 @@ static int norm_threads(int d) {
   return (t + 31) / 32 * 32;
 }
 
-cudaError_t residual_norm_launch(const float* part, int splits, int M, int d, float* h, const uint16_t* norm_w,
+cudaError_t residual_norm_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h, const uint16_t* norm_w,
                                  float eps, uint16_t* x_packed, int TM, cudaStream_t s) {
-  residual_norm_kernel<<<M, norm_threads(d), 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM, 0);
-  return cudaGetLastError();
+  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d)), 0, s, part, plan, M, d, h, norm_w, eps,
+                    x_packed, TM, 0);
 }
 
-cudaError_t residual_norm_rows_launch(const float* part, int splits, int M, int d, float* h,
+cudaError_t residual_norm_rows_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h,
                                       const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
                                       int norm_row_begin, cudaStream_t s) {
-  residual_norm_kernel<<<M, norm_threads(d), 0, s>>>(part, splits, M, d, h, norm_w, eps, x_packed, TM,
-                                                     norm_row_begin);
-  return cudaGetLastError();
+  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d)), 0, s, part, plan, M, d, h, norm_w, eps,
+                    x_packed, TM, norm_row_begin);
 }
 
 // ------------------------------------------------------------- SiLU(gate)*up
-__global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int M, int ffn,
+__global__ void silu_mul_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int ffn,
                                 uint16_t* __restrict__ x, int TM) {
+  pdl_wait();
+  pdl_trigger();
   const int f4 = ffn >> 2;
   const size_t total = (size_t)M * f4;
   const size_t stride4 = (size_t)M * 2 * ffn / 4;
@@ -199,10 +205,13 @@ __global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int 
     const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f), u = g;
     const size_t base = (size_t)m * 2 * f4 + j4;
-    for (int s = 0; s < splits; ++s) {
+    const int ng = part_slots(plan, m, j4 * 4), nu = part_slots(plan, m, ffn + j4 * 4);
+    for (int s = 0; s < ng; ++s) {
       const float4 a = p4[s * stride4 + base];
-      const float4 b = p4[s * stride4 + base + f4];
       g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
+    }
+    for (int s = 0; s < nu; ++s) {
+      const float4 b = p4[s * stride4 + base + f4];
       u.x += b.x; u.y += b.y; u.z += b.z; u.w += b.w;
     }
     uint2 o;
@@ -212,29 +221,31 @@ __global__ void silu_mul_kernel(const float* __restrict__ part, int splits, int 
   }
 }
 
-cudaError_t silu_mul_launch(const float* part, int splits, int M, int ffn, uint16_t* x_packed, int TM,
+cudaError_t silu_mul_launch(const float* part, const GemmPlanDev& plan, int M, int ffn, uint16_t* x_packed, int TM,
                             cudaStream_t s) {
   const size_t total = (size_t)M * ffn / 4;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  silu_mul_kernel<<<blocks, 256, 0, s>>>(part, splits, M, ffn, x_packed, TM);
-  return cudaGetLastError();
+  return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, s, part, plan, M, ffn, x_packed, TM);
 }
 
 // ------------------------------------------------------ logits + greedy argmax
-__global__ void __launch_bounds__(512) argmax_kernel(const float* __restrict__ part, int splits, int M, int V,
+__global__ void __launch_bounds__(512) argmax_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int V,
                                                      float* __restrict__ logits_out, int32_t* __restrict__ next_out,
                                                      int32_t* __restrict__ hist, const int32_t* __restrict__ slot,
                                                      const int32_t* __restrict__ pos, int hist_stride) {
   __shared__ float bv[16];
   __shared__ int bi[16];
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const size_t stride = (size_t)M * V;
   float best = -INFINITY;
   int besti = 0x7fffffff;
   for (int v = threadIdx.x; v < V; v += 512) {
     float x = 0.f;
-    for (int s = 0; s < splits; ++s) x += part[s * stride + (size_t)m * V + v];
+    const int ns = part_slots(plan, m, v);
+    for (int s = 0; s < ns; ++s) x += part[s * stride + (size_t)m * V + v];
     if (logits_out) logits_out[(size_t)m * V + v] = x;
     if (x > best || (x == best && v < besti)) {
       best = x;
@@ -267,11 +278,11 @@ __global__ void __launch_bounds__(512) argmax_kernel(const float* __restrict__ p
   }
 }
 
-cudaError_t argmax_launch(const float* part, int splits, int M, int V, float* logits_out, int32_t* next_out,
+cudaError_t argmax_launch(const float* part, const GemmPlanDev& plan, int M, int V, float* logits_out, int32_t* next_out,
                           int32_t* hist, const int32_t* slot, const int32_t* pos, int hist_stride,
                           cudaStream_t s) {
-  argmax_kernel<<<M, 512, 0, s>>>(part, splits, M, V, logits_out, next_out, hist, slot, pos, hist_stride);
-  return cudaGetLastError();
+  return launch_pdl(argmax_kernel, dim3(M), dim3(512), 0, s, part, plan, M, V, logits_out, next_out, hist, slot, pos,
+                    hist_stride);
 }
 
 // ------------------------------------------------ synthetic weight generator
@@ -346,7 +357,7 @@ __global__ void quant_w4_kernel(const uint16_t* __restrict__ w, int N, int K, ui
           const int kk = j * 32 + q * 8 + e;
           const int code = mx == 0.0 ? 0 : (int)round(__ddiv_rn((double)bf2f(src[kk]), scale));
           if (codes_out) codes_out[(size_t)n * K + (size_t)g * 128 + kk] = (int8_t)code;
-          v |= ((uint32_t)(code + 8) & 0xFu) << (4 * e);
+          v |= ((uint32_t)(code + 8) & 0xFu) << ((e & 1) * 16 + (e >> 1) * 4);
         }
         words[q] = v;
       }

@@ -1,39 +1,49 @@
 // gemm.cu -- the decoder linear layers on 5th-gen tensor cores (tcgen05).
 //
-// Computes P[s][m][n] = sum_{k in split s} W[n][k] * X[m][k] for one weight
-// matrix W [N x K] (BF16, or W4A16 g128 dequantized in the staging path) and a
-// token block X [M x K] (BF16), fp32 partials per split-K slice.  "Swap-AB":
-// the weight rows are the UMMA M=128 side, the tokens the UMMA N side (16..256),
-// so a decode batch of 64 is one N=64 instruction and a prefill of 8k tokens is
-// 32 N=256 tiles -- the same kernel serves decode (HBM-bound, split-K over all
-// 148 SMs) and prefill (tensor-bound).
+// P[slot][m][n] = sum_{k in segment} W[n][k] * X[m][k] for one weight matrix W
+// [N x K] (BF16, or W4A16 g128 dequantised in the staging path) and a token
+// block X [M x K] (BF16), fp32 partials.  "Swap-AB": the weight rows are the
+// UMMA M=128 side and the tokens the UMMA N side (16..256, runtime), so a
+// decode batch of 64 is one N=64 instruction and a prefill is N=256 tiles --
+// one kernel for decode (HBM-bound) and prefill (tensor-bound).
 //
 // Replaces the priced stand-ins `decode_ms_per_layer[tag]` (reference
 // proj/src/sim_config.cpp:23-27) and `tokens * prefill_ms_per_token`
-// (proj/src/engine.cpp:477-478).  Per-layer precision dispatch (BF16 vs W4) is
-// chosen by the caller from the layer table snapshot taken at step launch
-// (proj/src/engine.cpp:523-525).
+// (proj/src/engine.cpp:477-478); the BF16-vs-W4 choice comes from the layer
+// table snapshot taken at step launch (engine.cpp:523-525).
+//
+// Persistent, stream-K balanced: one CTA per SM walks a contiguous range of
+// the global (tile, k-step) sequence, so every SM streams the same number of
+// weight bytes whatever the matrix shape.  A tile split between CTAs leaves
+// one fp32 partial slot per CTA segment; the consuming row kernels sum the
+// slots in slot order (deterministic, see PartSpec in kernels.h).  The
+// partials of a decode step stay in L2.
 //
 // Data movement: every operand chunk is ONE contiguous 1-D bulk async copy
-// (cp.async.bulk -> SASS UBLKCP) into shared memory, because both operands are
-// pre-packed into the UMMA canonical K-major no-swizzle image:
+// (cp.async.bulk -> SASS UBLKCP), because both operands are pre-packed into
+// the UMMA canonical K-major no-swizzle image:
 //   weight chunk (n_tile, kb64)  = 16 KB  [row_group 16][k_chunk 8][row 8][8 bf16]
 //   W4 chunk (n_tile, g128)      = 8448 B [j 4][row 128][16 B codes] + 128 bf16 scales
 //   activation chunk (m_tile,kb) = TM*128 B, same core-matrix order.
-// Weight chunks are addressed through the variant image's page table so a layer
-// image can live in any free pages of the KV/weight arena (KV resizing needs no
-// contiguity).
+// Weight chunks are found through the variant image's page table, so a layer
+// image may live in any free pages of the KV/weight arena.
 //
-// Roles (warp-specialised, mbarrier pipelines):
-//   warp 0 lane 0 : producer (bulk copies, expect_tx)
-//   warp 1 lane 0 : UMMA issuer (tcgen05.mma kind::f16, M=128, N=TM, K=16)
-//   W4 only, warps 2..5 : dequantisers (int4 -> bf16(code*scale) -> smem, proxy fence)
-//   epilogue (4 warps covering the 4 TMEM lane quadrants): tcgen05.ld -> fp32 partials.
+// Warp roles (mbarrier pipelines, no __syncthreads in the main loop):
+//   warp 0 lane 0    producer: bulk copies into a `stages`-deep smem ring (W4: raw
+//                    int4 chunks into their own deeper ring; B is fetched by the
+//                    first dequantiser thread once the MMA released the stage)
+//   warp 1 lane 0    UMMA issuer: tcgen05.mma kind::f16 M=128 N=TM K=16 into one
+//                    of two TMEM accumulators (double buffered across segments)
+//   warps 2..5       epilogue: tcgen05.ld -> fp32 partials, overlapping the next
+//                    segment's loads and MMAs
+//   warps 6..13 (W4) dequantisers: int4 -> bf16(code*scale) via the 0x4300 magic
+//                    (exact), st.shared in the canonical layout, proxy fence.
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
-#include "ptx.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace ms {
 
@@ -47,221 +57,334 @@ __device__ __forceinline__ const uint8_t* chunk_ptr(const GemmWeights& w, int64_
   return reinterpret_cast<const uint8_t*>(w.pages[page]) + off;
 }
 
-template <bool kW4>
-__global__ void __launch_bounds__(kW4 ? 192 : 128, 1)
-    gemm_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, int splits,
-                float* __restrict__ out, int stages) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const int N = W.N, K = W.K;
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Segment walker shared by every role so they all see the same sequence.
+struct SegIter {
+  int64_t g, g1;
+  int nk;
+  __device__ SegIter(const GemmPlanDev& p, int c) : nk(p.nk) {
+    if (p.aligned) {
+      const int64_t t0 = (int64_t)p.tiles * c / p.C, t1 = (int64_t)p.tiles * (c + 1) / p.C;
+      g = t0 * p.nk;
+      g1 = t1 * p.nk;
+    } else {
+      g = p.T * c / p.C;
+      g1 = p.T * (c + 1) / p.C;
+    }
+  }
+  // next segment: tile t, k-steps [k0, k1)
+  __device__ bool next(int& t, int& k0, int& k1) {
+    if (g >= g1) return false;
+    t = (int)(g / nk);
+    k0 = (int)(g - (int64_t)t * nk);
+    const int64_t end = min(g1, (int64_t)(t + 1) * nk);
+    k1 = (int)(end - (int64_t)t * nk);
+    g = end;
+    return true;
+  }
+};
 
-  // k-steps: BF16 steps are 64 wide, W4 steps are one 128-wide group.
-  const int kstep = kW4 ? 128 : 64;
-  const int nk_total = K / kstep;
-  const int k_begin = (int)((int64_t)nk_total * split / splits);
-  const int k_end = (int)((int64_t)nk_total * (split + 1) / splits);
-  const int nk = k_end - k_begin;
+template <bool kW4>
+__global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
+    gemm_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
+                float* __restrict__ out, int stages, int rstages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int N = W.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const int nk = plan.nk;
 
   const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk
   const uint32_t a_bytes = kW4 ? 32768u : 16384u;
   const uint32_t raw_bytes = kW4 ? (uint32_t)kW4ChunkBytes : 0u;
-  const uint32_t stage_bytes = a_bytes + (kW4 ? 2 : 1) * b_bytes + ((raw_bytes + 127u) & ~127u);
+  const uint32_t stage_bytes = a_bytes + (kW4 ? 2 : 1) * b_bytes;  // A + B ring stage
+  const uint32_t raw_stage = (raw_bytes + 127u) & ~127u;             // W4: separate, deeper raw ring
+  const uint32_t tm_cols = TM <= 32 ? 32u : TM <= 64 ? 64u : TM <= 128 ? 128u : 256u;
 
   uint8_t* sbase = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (size_t)stages * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + stages;
-  uint64_t* afull = bars + 2 * stages;  // W4: dequantised A ready
-  uint64_t* accum = bars + 3 * stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * stages + 1);
+  uint8_t* rbase = smem + (size_t)stages * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(rbase + (size_t)rstages * raw_stage);
+  uint64_t* empty = full + stages;
+  uint64_t* afull = full + 2 * stages;
+  uint64_t* tfull = full + 3 * stages;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained
+  uint64_t* rfull = tempty + 2;          // [rstages] raw W4 chunk landed
+  uint64_t* rempty = rfull + rstages;    // [rstages] raw W4 chunk consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + rstages);
 
   auto sA = [&](int s) { return sbase + (size_t)s * stage_bytes; };
   auto sB = [&](int s) { return sbase + (size_t)s * stage_bytes + a_bytes; };
-  auto sRaw = [&](int s) { return sbase + (size_t)s * stage_bytes + a_bytes + 2 * b_bytes; };
-
-  const uint32_t tm_cols = TM <= 32 ? 32u : TM <= 64 ? 64u : TM <= 128 ? 128u : 256u;
+  auto sRaw = [&](int r) { return rbase + (size_t)r * raw_stage; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&afull[s], 128);
+      mbar_init(&afull[s], 256);
     }
-    mbar_init(accum, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    for (int r = 0; r < rstages; ++r) {
+      mbar_init(&rfull[r], 1);
+      mbar_init(&rempty[r], 256);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc_dyn(tmem_slot, tm_cols);
+  if (warp == 1) tmem_alloc_dyn(tmem_slot, 2 * tm_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_d = *tmem_slot;
-
-  const int64_t kb_per_row = K / 64;  // activation chunks per m_tile
-  const uint8_t* xbase = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_row * b_bytes;
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t kb_per_mtile = W.K / 64;
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- producer
-      for (int it = 0; it < nk; ++it) {
-        const int s = it % stages;
-        if (it >= stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-        const int ks = k_begin + it;
-        if (kW4) {
-          mbar_expect_tx(&full[s], raw_bytes + 2 * b_bytes);
-          bulk_g2s(sRaw(s), chunk_ptr(W, (int64_t)n_tile * nk_total + ks, kW4ChunkBytes), raw_bytes, &full[s]);
-          bulk_g2s(sB(s), xbase + (size_t)(2 * ks) * b_bytes, 2 * b_bytes, &full[s]);
-        } else {
-          mbar_expect_tx(&full[s], a_bytes + b_bytes);
-          bulk_g2s(sA(s), chunk_ptr(W, (int64_t)n_tile * nk_total + ks, kBf16ChunkBytes), a_bytes, &full[s]);
-          bulk_g2s(sB(s), xbase + (size_t)ks * b_bytes, b_bytes, &full[s]);
+      // ------------------------------------------------------------ producer
+      // Weights do not depend on the previous kernel: prefetch the first ring
+      // of weight chunks before the grid dependency wait (PDL overlap).
+      uint32_t npre = 0;
+      {
+        SegIter pre(plan, cta);
+        int t, k0, k1;
+        const uint32_t cap = kW4 ? (uint32_t)rstages : (uint32_t)stages;
+        while (npre < cap && pre.next(t, k0, k1)) {
+          const int n_tile = t % plan.n_tiles;
+          for (int k = k0; k < k1 && npre < cap; ++k, ++npre) {
+            if (kW4) {
+              mbar_expect_tx(&rfull[npre], raw_bytes);
+              bulk_g2s(sRaw(npre), chunk_ptr(W, (int64_t)n_tile * nk + k, kW4ChunkBytes), raw_bytes, &rfull[npre]);
+            } else {
+              mbar_expect_tx(&full[npre], a_bytes + b_bytes);
+              bulk_g2s(sA(npre), chunk_ptr(W, (int64_t)n_tile * nk + k, kBf16ChunkBytes), a_bytes, &full[npre]);
+            }
+          }
+        }
+      }
+      pdl_wait();
+      SegIter seg(plan, cta);
+      int t, k0, k1;
+      uint32_t it = 0;
+      while (seg.next(t, k0, k1)) {
+        const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
+        const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
+        for (int k = k0; k < k1; ++k, ++it) {
+          if (it < npre) {  // weight chunk already in flight: only the activations remain
+            if (!kW4) bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
+            continue;
+          }
+          if (kW4) {  // raw int4 chunks only; the dequantisers fetch B
+            const int r = it % rstages;
+            if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
+            mbar_expect_tx(&rfull[r], raw_bytes);
+            bulk_g2s(sRaw(r), chunk_ptr(W, (int64_t)n_tile * nk + k, kW4ChunkBytes), raw_bytes, &rfull[r]);
+          } else {
+            const int s = it % stages;
+            if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+            mbar_expect_tx(&full[s], a_bytes + b_bytes);
+            bulk_g2s(sA(s), chunk_ptr(W, (int64_t)n_tile * nk + k, kBf16ChunkBytes), a_bytes, &full[s]);
+            bulk_g2s(sB(s), xb + (size_t)k * b_bytes, b_bytes, &full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- UMMA issuer
+      // ---------------------------------------------------------- UMMA issuer
       const uint32_t idesc = umma_idesc_bf16(128, (uint32_t)TM);
-      for (int it = 0; it < nk; ++it) {
-        const int s = it % stages;
-        const uint32_t ph = (it / stages) & 1;
-        mbar_wait(&full[s], ph);
-        if (kW4) mbar_wait(&afull[s], ph);
+      SegIter seg(plan, cta);
+      int t, k0, k1;
+      uint32_t it = 0, u = 0;
+      while (seg.next(t, k0, k1)) {
+        const uint32_t acc = u & 1, use = u >> 1;
+        if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA(s)), b0 = smem_u32(sB(s));
+        const uint32_t d = tmem_base + acc * tm_cols;
+        for (int k = k0; k < k1; ++k, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(&full[s], ph);
+          if (kW4) mbar_wait(&afull[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA(s)), b0 = smem_u32(sB(s));
 #pragma unroll
-        for (int sub = 0; sub < (kW4 ? 2 : 1); ++sub) {
+          for (int sub = 0; sub < (kW4 ? 2 : 1); ++sub) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t da = umma_desc(a0 + sub * 16384u + k * 256u, 128u, 1024u);
-            const uint64_t db = umma_desc(b0 + sub * b_bytes + k * 256u, 128u, 1024u);
-            umma_bf16(tmem_d, da, db, idesc, (it | sub | k) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t da = umma_desc(a0 + sub * 16384u + kk * 256u, 128u, 1024u);
+              const uint64_t db = umma_desc(b0 + sub * b_bytes + kk * 256u, 128u, 1024u);
+              umma_bf16(d, da, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
+            }
           }
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tfull[acc]);
+        ++u;
       }
-      umma_commit(accum);
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------- epilogue
+    pdl_wait();
+    const int quad = warp & 3;
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t u = 0;
+    while (seg.next(t, k0, k1)) {
+      const uint32_t acc = u & 1, use = u >> 1;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
+      const int slot = plan.aligned ? 0 : cta - plan_cta_of(plan, (int64_t)t * nk);
+      const int n = n_tile * 128 + quad * 32 + lane;
+      float* o = out + (size_t)slot * M * N;
+      const uint32_t d = tmem_base + acc * tm_cols + ((uint32_t)(quad * 32) << 16);
+      for (int c0 = 0; c0 < TM; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(d + (uint32_t)c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int m = m_tile * TM + c0 + j;
+          if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      ++u;
     }
   } else if (kW4) {
-    // ---------------- dequantisers: thread t owns weight row t of the tile
-    const int t = threadIdx.x - 64;
-    const int rg = t >> 3, r = t & 7;
-    for (int it = 0; it < nk; ++it) {
-      const int s = it % stages;
-      mbar_wait(&full[s], (it / stages) & 1);
-      const uint8_t* raw = sRaw(s);
-      const float sc = bf2f(*reinterpret_cast<const uint16_t*>(raw + 8192 + 2 * t));
-      uint8_t* a = sA(s);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint4 q = *reinterpret_cast<const uint4*>(raw + (j * 128 + t) * 16);
-        const uint32_t words[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int kk = j * 32 + w * 8;  // element offset within the 128-group
-          const int sub = kk >> 6, c = (kk & 63) >> 3;
-          uint32_t o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c0 = (int)((words[w] >> (8 * e)) & 0xFu) - 8;
-            const int c1 = (int)((words[w] >> (8 * e + 4)) & 0xFu) - 8;
-            o[e] = pack_bf2((float)c0 * sc, (float)c1 * sc);
-          }
-          *reinterpret_cast<uint4*>(a + sub * 16384 + ((rg * 8 + c) * 8 + r) * 16) =
-              make_uint4(o[0], o[1], o[2], o[3]);
+    // ---------------------------------------------------------- dequantisers
+    // thread: weight row `row` of the tile, 64-wide half `half` of the group
+    const int tid = threadIdx.x - 192;
+    const int row = tid & 127, half = tid >> 7;
+    const int rg = row >> 3, r = row & 7;
+    const __nv_bfloat162 bias = __floats2bfloat162_rn(136.0f, 136.0f);
+    pdl_wait();
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t it = 0;
+    while (seg.next(t, k0, k1)) {
+      const int m_tile = t / plan.n_tiles;
+      const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
+      for (int k = k0; k < k1; ++k, ++it) {
+        const int s = it % stages, rs = it % rstages;
+        if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);  // MMA done with stage s
+        if (tid == 0) {
+          mbar_expect_tx(&full[s], 2 * b_bytes);
+          bulk_g2s(sB(s), xb + (size_t)(2 * k) * b_bytes, 2 * b_bytes, &full[s]);
         }
+        mbar_wait(&rfull[rs], (it / rstages) & 1);
+        const uint8_t* raw = sRaw(rs);
+        const uint16_t sraw = *reinterpret_cast<const uint16_t*>(raw + 8192 + 2 * row);
+        __nv_bfloat162 sc;
+        sc.x = __ushort_as_bfloat16(sraw);
+        sc.y = sc.x;
+        uint8_t* a = sA(s) + half * 16384;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int j = half * 2 + jj;
+          const uint4 q = *reinterpret_cast<const uint4*>(raw + (j * 128 + row) * 16);
+          const uint32_t words[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int c = jj * 4 + w;  // 8-element k_chunk within the 64-wide half
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t x = ((words[w] >> (4 * i)) & 0x000F000Fu) | 0x43004300u;  // bf16x2 (128+nib)
+              __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
+              v = __hmul2(__hsub2(v, bias), sc);  // exact code, then one rounding of code*scale
+              o[i] = *reinterpret_cast<uint32_t*>(&v);
+            }
+            *reinterpret_cast<uint4*>(a + ((rg * 8 + c) * 8 + r) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&afull[s]);
+        mbar_arrive(&rempty[rs]);
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&afull[s]);
     }
   }
 
-  // ---------------- epilogue: TMEM -> fp32 partials [split][m][n]
-  __syncwarp();
-  const bool epi = kW4 ? (warp >= 2) : true;
-  if (epi) {
-    mbar_wait(accum, 0);
-    tc_fence_after();
-    const int quad = warp & 3;
-    const int n = n_tile * 128 + quad * 32 + lane;
-    float* o = out + (size_t)split * M * N;
-    for (int c0 = 0; c0 < TM; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem_d + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
-      tmem_ld_wait();
-      if (nk == 0) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = m_tile * TM + c0 + j;
-        if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
-      }
-    }
-  }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem_d, tm_cols);
+  if (warp == 1) tmem_dealloc(tmem_base, 2 * tm_cols);
 }
 
-static int pick_stages(bool w4, int TM, size_t* smem_out) {
+static size_t stage_bytes_of(bool w4, int TM) {
   const size_t b = (size_t)TM * 128;
-  const size_t stage = w4 ? (32768 + 2 * b + 8448 + 127) / 128 * 128 : 16384 + b;
-  const size_t budget = w4 ? 220 * 1024 : (TM <= 64 ? 110 * 1024 : 200 * 1024);
-  int st = (int)(budget / stage);
-  if (st > 8) st = 8;
-  if (st < 2) st = 2;
-  *smem_out = st * stage + (3 * st + 2) * 8 + 64;
+  return w4 ? 32768 + 2 * b : 16384 + b;
+}
+
+// BF16: one ring of up to 8 (A,B) stages.  W4: 2 (A,B) stages plus a deep raw
+// int4 ring so that enough weight bytes are in flight per SM.
+static int pick_stages(bool w4, int TM, int* rstages, size_t* smem_out) {
+  const size_t budget = 215 * 1024;
+  const size_t stage = stage_bytes_of(w4, TM);
+  int st, rs = 0;
+  if (w4) {
+    st = 2;
+    rs = (int)((budget - st * stage) / 8576);
+    if (rs > 16) rs = 16;
+    if (rs < 2) rs = 2;
+  } else {
+    st = (int)(budget / stage);
+    if (st > 8) st = 8;
+    if (st < 2) st = 2;
+  }
+  *rstages = rs;
+  *smem_out = st * stage + (size_t)rs * 8576 + (3 * st + 4 + 2 * rs) * 8 + 64;
   return st;
 }
 
-int gemm_pick_splits(int n_tiles, int m_tiles, int nk, int num_sms, int ctas_per_sm) {
-  const int slots = num_sms * ctas_per_sm;
-  int best = 1;
-  double best_cost = 1e30;
-  for (int s = 1; s <= 16 && s <= nk; ++s) {
-    const int units = n_tiles * m_tiles * s;
-    const int waves = (units + slots - 1) / slots;
-    const int per = (nk + s - 1) / s;
-    // per-unit fixed cost ~ 2 k-steps (pipeline fill + epilogue)
-    const double cost = (double)waves * (per + 2) + 0.02 * s;
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = s;
-    }
+GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t part_elems) {
+  GemmPlanDev p{};
+  p.n_tiles = N / 128;
+  p.TM = TM;
+  p.nk = K / (w4 ? 128 : 64);
+  p.tiles = p.n_tiles * ((M + TM - 1) / TM);
+  p.T = (int64_t)p.tiles * p.nk;
+  p.C = (int)std::min<int64_t>(num_sms, p.T);
+  p.aligned = 0;
+  // slots needed by the stream-K partition
+  int max_slots = 1;
+  const bool fits32 = (p.T + 1) * (int64_t)p.C < ((int64_t)1 << 31);
+  if (fits32)
+    for (int t = 0; t < p.tiles; ++t) max_slots = std::max(max_slots, plan_count(p, t));
+  if (!fits32 || (size_t)max_slots * M * N > part_elems) {  // fall back to whole tiles per CTA
+    p.aligned = 1;
+    p.C = std::min(num_sms, p.tiles);
+    max_slots = 1;
   }
-  return best;
+  p.slots = max_slots;
+  return p;
 }
 
-cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, int splits, float* out,
-                        cudaStream_t stream) {
+cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+                        float* out, cudaStream_t stream) {
   size_t smem = 0;
-  const int stages = pick_stages(w4, TM, &smem);
-  dim3 grid(w.N / 128, (M + TM - 1) / TM, splits);
+  int rstages = 0;
+  const int stages = pick_stages(w4, TM, &rstages, &smem);
   if (w4) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr = true;
     }
-    gemm_kernel<true><<<grid, 192, smem, stream>>>(w, x, M, TM, splits, out, stages);
+    return launch_pdl(gemm_kernel<true>, dim3(plan.C), dim3(448), smem, stream, w, x, M, TM, plan, out, stages,
+                      rstages);
   } else {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr = true;
     }
-    gemm_kernel<false><<<grid, 128, smem, stream>>>(w, x, M, TM, splits, out, stages);
+    return launch_pdl(gemm_kernel<false>, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, stages,
+                      rstages);
   }
   return cudaGetLastError();
-}
-
-int gemm_ctas_per_sm(bool w4, int TM) {
-  size_t smem = 0;
-  pick_stages(w4, TM, &smem);
-  int per = (int)((228 * 1024) / (smem + 1024));
-  return per < 1 ? 1 : per;
 }
 
 }  // namespace ms

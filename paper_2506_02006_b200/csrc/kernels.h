@@ -4,7 +4,36 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace ms {
+
+// Every hot-path kernel is launched with programmatic dependent launch so its
+// launch latency and prologue overlap the tail of the previous kernel
+// (MS_PDL=0 disables, for A/B measurements).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // A weight matrix as the GEMM sees it: chunk c of the matrix lives in page
 // (first_chunk + c) / chunks_per_page of its variant image.
@@ -15,10 +44,33 @@ struct GemmWeights {
   int N, K;
 };
 
-cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, int splits, float* out,
-                        cudaStream_t stream);
-int gemm_pick_splits(int n_tiles, int m_tiles, int nk, int num_sms, int ctas_per_sm);
-int gemm_ctas_per_sm(bool w4, int TM);
+// Stream-K partition of one GEMM: T = tiles * nk k-steps split into C
+// contiguous ranges (one persistent CTA each).  CTA c covers global k-steps
+// [floor(c*T/C), floor((c+1)*T/C)); a tile t touched by several CTAs gets one
+// fp32 partial slot per CTA (slot = c - first CTA of t).  `aligned` = whole
+// tiles per CTA (one slot).  Consumers sum part_slots() slots of [slot][M][N]
+// in slot order, so the result is deterministic.
+struct GemmPlanDev {
+  int64_t T;
+  int C, nk, n_tiles, tiles, TM, aligned, slots;
+};
+// 32-bit arithmetic: gemm_plan() guarantees (T + 1) * C < 2^31 for stream-K
+// plans (larger problems use whole-tile plans, where every count is 1).
+__host__ __device__ inline int plan_cta_of(const GemmPlanDev& p, int64_t g) {
+  const uint32_t T = (uint32_t)p.T;
+  return (int)(((uint32_t)(g + 1) * (uint32_t)p.C + T - 1) / T) - 1;
+}
+__host__ __device__ inline int plan_count(const GemmPlanDev& p, int t) {
+  if (p.aligned) return 1;
+  return plan_cta_of(p, (int64_t)(t + 1) * p.nk - 1) - plan_cta_of(p, (int64_t)t * p.nk) + 1;
+}
+__host__ __device__ inline int part_slots(const GemmPlanDev& p, int m, int n) {
+  return plan_count(p, (m / p.TM) * p.n_tiles + (n >> 7));
+}
+
+GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t part_elems);
+cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+                        float* out, cudaStream_t stream);
 
 // Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
 // every layer): [layer][kv_head][K|V][token][head_dim] bf16.
@@ -54,18 +106,18 @@ cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, cons
                               const int32_t* slot, const int32_t* pos, int hist_stride, int M, int d,
                               const uint16_t* norm_w, float eps, float* h, uint16_t* x_packed, int TM,
                               cudaStream_t s);
-cudaError_t qkv_post_launch(const float* part, int splits, int M, int H, int KVH, int hd, const float* rope_cos,
+cudaError_t qkv_post_launch(const float* part, const GemmPlanDev& plan, int M, int H, int KVH, int hd, const float* rope_cos,
                             const float* rope_sin, const int32_t* pos, const KvGeom& kv, int layer,
                             const int32_t* pages, const int32_t* page_row, int page_stride, float* q_out,
                             cudaStream_t s);
-cudaError_t residual_norm_launch(const float* part, int splits, int M, int d, float* h, const uint16_t* norm_w,
+cudaError_t residual_norm_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h, const uint16_t* norm_w,
                                  float eps, uint16_t* x_packed, int TM, cudaStream_t s);
-cudaError_t residual_norm_rows_launch(const float* part, int splits, int M, int d, float* h,
+cudaError_t residual_norm_rows_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h,
                                       const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
                                       int norm_row_begin, cudaStream_t s);
-cudaError_t silu_mul_launch(const float* part, int splits, int M, int ffn, uint16_t* x_packed, int TM,
+cudaError_t silu_mul_launch(const float* part, const GemmPlanDev& plan, int M, int ffn, uint16_t* x_packed, int TM,
                             cudaStream_t s);
-cudaError_t argmax_launch(const float* part, int splits, int M, int V, float* logits_out, int32_t* next_out,
+cudaError_t argmax_launch(const float* part, const GemmPlanDev& plan, int M, int V, float* logits_out, int32_t* next_out,
                           int32_t* hist, const int32_t* slot, const int32_t* pos, int hist_stride,
                           cudaStream_t s);
 cudaError_t gen_weight_launch(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset,

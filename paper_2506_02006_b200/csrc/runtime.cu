@@ -311,20 +311,12 @@ ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
   return ms::GemmWeights{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
 }
 
-int pick_splits(ms_ctx* c, bool w4, int N, int K, int M, int TM) {
-  const int m_tiles = (M + TM - 1) / TM;
-  const int nk = K / (w4 ? 128 : 64);
-  int s = ms::gemm_pick_splits(N / 128, m_tiles, nk, c->num_sms, ms::gemm_ctas_per_sm(w4, TM));
-  while (s > 1 && (size_t)s * M * N > c->part_elems) --s;
-  return s;
-}
-
-int gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
+ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
-  const int s = pick_splits(c, w4, w.N, w.K, M, TM);
-  CK(ms::gemm_launch(w, w4, c->x, M, TM, s, c->part, c->compute));
+  const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, w4, c->num_sms, c->part_elems);
+  CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute));
   c->launches += 1;
-  return s;
+  return plan;
 }
 
 void prof_mark(ms_ctx* c) {
@@ -359,7 +351,7 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   const int asplits = attn_splits(c, M, max_ctx);
   for (int l = 0; l < D.num_layers; ++l) {
     const bool w4 = c->layers[l].bits == 4;
-    int s = gemm(c, mat_weights(c, l, 0), w4, M, TM);
+    ms::GemmPlanDev s = gemm(c, mat_weights(c, l, 0), w4, M, TM);
     CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
                            d_page_row, page_stride, c->q, c->compute));
     c->launches += 1;
@@ -403,7 +395,7 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   const int Mo = M - final_row_begin;
   const int TMo = round16(Mo) > 256 ? 256 : round16(Mo);
   ms::GemmWeights lw{c->lm_table, 0, (int64_t)1 << 40, D.vocab, d};
-  const int s = gemm(c, lw, false, Mo, TMo);
+  const ms::GemmPlanDev s = gemm(c, lw, false, Mo, TMo);
   CK(ms::argmax_launch(c->part, s, Mo, D.vocab, want_logits ? c->logits : nullptr, c->next, c->hist,
                        d_slot + final_row_begin, d_pos + final_row_begin, c->hist_len, c->compute));
   c->launches += 1;
@@ -1102,13 +1094,16 @@ int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_pa
     int dev = 0, sms = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int nk = K / (w4 ? 128 : 64);
-    int s = splits > 0 ? std::min(splits, nk)
-                       : ms::gemm_pick_splits(N / 128, (M + TM - 1) / TM, nk, sms, ms::gemm_ctas_per_sm(w4, TM));
-    CK(ms::gemm_launch(w, w4, x_packed, M, TM, s, out, (cudaStream_t)stream));
-    if (splits_used) *splits_used = s;
+    // `splits` > 0 caps the persistent CTA count (exercises other partitions)
+    const int ctas = splits > 0 ? std::min(splits, sms) : sms;
+    ms::GemmPlanDev plan = ms::gemm_plan(N, K, M, TM, w4, ctas, (size_t)16 * M * N);
+    CK(ms::gemm_launch(w, w4, x_packed, M, TM, plan, out, (cudaStream_t)stream));
+    // slots actually written per tile are part_slots() <= plan.slots; slots a
+    // tile does not use are left untouched (callers pass a zeroed buffer)
+    if (splits_used) *splits_used = plan.aligned ? 1 : plan.slots;
   });
 }
+
 int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int layers, int layer, int H, int KVH,
                      int hd, const int32_t* pages, int max_blocks, const int32_t* ctx_len, int rows, int splits,
                      float* workspace, uint16_t* out, void* stream) {

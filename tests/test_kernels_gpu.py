@@ -85,7 +85,7 @@ def _run_gemm(bits, W, X, TM, splits=0):
     xp = torch.zeros(m_tiles * TM * K, dtype=torch.int16, device="cuda")
     dx = dev_u16(X)
     N.check(N.lib().ms_k_pack_act(C.c_void_p(dx.data_ptr()), M, K, TM, C.c_void_p(xp.data_ptr()), stream()))
-    out = torch.empty(16 * M * Nn, dtype=torch.float32, device="cuda")
+    out = torch.zeros(16 * M * Nn, dtype=torch.float32, device="cuda")
     used = C.c_int()
     N.check(N.lib().ms_k_gemm(bits, C.c_void_p(wp.data_ptr()), Nn, K, C.c_void_p(xp.data_ptr()), M, TM, splits,
                               C.c_void_p(out.data_ptr()), C.byref(used), stream()))

@@ -66,7 +66,8 @@ def test_pack_layouts_roundtrip():
         for g in range(K // 128):
             chunk = img[nt, g]
             words = chunk[:8192].view(np.uint32).reshape(4, 128, 4)  # [j][row][w]
-            nib = ((words[..., None] >> (4 * np.arange(8, dtype=np.uint32))) & 0xF).astype(np.int16) - 8
+            shifts = np.array([(e & 1) * 16 + (e >> 1) * 4 for e in range(8)], np.uint32)
+            nib = ((words[..., None] >> shifts) & 0xF).astype(np.int16) - 8
             dec = nib.transpose(1, 0, 2, 3).reshape(128, 128)  # [row][j*32 + w*8 + e]
             assert np.array_equal(dec, codes[nt * 128:(nt + 1) * 128, g * 128:(g + 1) * 128])
             assert np.array_equal(chunk[8192:].view(np.uint16), s16[nt * 128:(nt + 1) * 128, g])

@@ -1,4 +1,4 @@
-"""Summarise an ncu --csv launch list (gpu__time_duration.sum) per kernel."""
+"""Summarise an ncu --csv launch list (gpu__time_duration.sum [+ dram__bytes_read.sum]) per kernel/grid."""
 import collections
 import csv
 import sys
@@ -8,34 +8,39 @@ def load(path):
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
-    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    out = []
+    ki, mi, vi, ui, idi, gi = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit",
+                                                     "ID", "Grid Size"))
+    launch = {}
     for r in rows[hdr + 1:]:
         if len(r) <= vi:
             continue
+        d = launch.setdefault(int(r[idi]), {"name": r[ki].split("(")[0], "grid": r[gi], "MB": 0.0})
         v = float(r[vi].replace(",", ""))
-        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1e-3)
-        out.append((r[ki].split("(")[0], v * scale))
-    return out
+        if r[mi] == "gpu__time_duration.sum":
+            d["us"] = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3}.get(r[ui], 1e-3)
+        else:
+            d["MB"] = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(r[ui], 1.0)
+    return [launch[k] for k in sorted(launch)]
 
 
 def summary(path):
     seq = load(path)
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    for n, us in seq:
-        agg[n][0] += 1
-        agg[n][1] += us
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for d in seq:
+        key = d["name"] + (" " + d["grid"] if "gemm" in d["name"] else "")
+        a = agg[key]
+        a[0] += 1
+        a[1] += d["us"]
+        a[2] += d["MB"]
     tot = sum(a[1] for a in agg.values())
     lines = []
-    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"{k[:48]:48s} n={n:4d} total={t / 1000:8.3f} ms avg={t / n:8.2f} us {100 * t / tot:5.1f}%")
-    lines.append(f"total {tot / 1000:.3f} ms over {len(seq)} launches")
+    for k, (n, t, mb) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        gbs = mb / t * 1e3 if t else 0.0
+        lines.append(f"{k[:52]:52s} n={n:5d} avg={t / n:8.2f} us  MB/launch={mb / n:8.2f}  GB/s={gbs:6.0f}  "
+                     f"{100 * t / tot:5.1f}%")
+    lines.append(f"total {tot / 1000:.3f} ms over {len(seq)} launches (ncu: serialised, warm L2)")
     return "\n".join(lines), seq
 
 
 if __name__ == "__main__":
-    s, seq = summary(sys.argv[1])
-    print(s)
-    if len(sys.argv) > 2:
-        for n, us in seq[: int(sys.argv[2])]:
-            print(f"  {n[:40]:40s} {us:9.2f} us")
+    print(summary(sys.argv[1])[0])
