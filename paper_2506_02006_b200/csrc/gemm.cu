@@ -57,6 +57,35 @@ __device__ __forceinline__ const uint8_t* chunk_ptr(const GemmWeights& w, int64_
   return reinterpret_cast<const uint8_t*>(w.pages[page]) + off;
 }
 
+// Walks consecutive chunks of one weight image: one division per segment,
+// one page-table load per page crossing (the producer thread must stay far
+// ahead of the MMAs, so no per-chunk 64-bit division or dependent load).
+struct ChunkCursor {
+  const uint64_t* pages;
+  int64_t cpp, page, in_page;
+  const uint8_t* base;
+  int chunk_bytes;
+  __device__ ChunkCursor(const GemmWeights& w, int cb) : pages(w.pages), cpp(w.chunks_per_page), page(-1),
+                                                        in_page(0), base(nullptr), chunk_bytes(cb) {}
+  __device__ void seek(int64_t c) {
+    const int64_t p = c / cpp;
+    in_page = c - p * cpp;
+    if (p != page) {
+      page = p;
+      base = reinterpret_cast<const uint8_t*>(pages[p]);
+    }
+  }
+  __device__ const uint8_t* get() {
+    if (in_page == cpp) {
+      in_page = 0;
+      ++page;
+      base = reinterpret_cast<const uint8_t*>(pages[page]);
+    }
+    return base + in_page * chunk_bytes;
+  }
+  __device__ void advance() { ++in_page; }
+};
+
 // Segment walker shared by every role so they all see the same sequence.
 struct SegIter {
   int64_t g, g1;
@@ -145,19 +174,21 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
       // Weights do not depend on the previous kernel: prefetch the first ring
       // of weight chunks before the grid dependency wait (PDL overlap).
       uint32_t npre = 0;
+      ChunkCursor cur(W, kW4 ? kW4ChunkBytes : kBf16ChunkBytes);
       {
         SegIter pre(plan, cta);
         int t, k0, k1;
         const uint32_t cap = kW4 ? (uint32_t)rstages : (uint32_t)stages;
         while (npre < cap && pre.next(t, k0, k1)) {
           const int n_tile = t % plan.n_tiles;
-          for (int k = k0; k < k1 && npre < cap; ++k, ++npre) {
+          cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
+          for (int k = k0; k < k1 && npre < cap; ++k, ++npre, cur.advance()) {
             if (kW4) {
               mbar_expect_tx(&rfull[npre], raw_bytes);
-              bulk_g2s(sRaw(npre), chunk_ptr(W, (int64_t)n_tile * nk + k, kW4ChunkBytes), raw_bytes, &rfull[npre]);
+              bulk_g2s(sRaw(npre), cur.get(), raw_bytes, &rfull[npre]);
             } else {
               mbar_expect_tx(&full[npre], a_bytes + b_bytes);
-              bulk_g2s(sA(npre), chunk_ptr(W, (int64_t)n_tile * nk + k, kBf16ChunkBytes), a_bytes, &full[npre]);
+              bulk_g2s(sA(npre), cur.get(), a_bytes, &full[npre]);
             }
           }
         }
@@ -169,7 +200,8 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
       while (seg.next(t, k0, k1)) {
         const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
         const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
-        for (int k = k0; k < k1; ++k, ++it) {
+        cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
+        for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
           if (it < npre) {  // weight chunk already in flight: only the activations remain
             if (!kW4) bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
             continue;
@@ -178,12 +210,12 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
             const int r = it % rstages;
             if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
             mbar_expect_tx(&rfull[r], raw_bytes);
-            bulk_g2s(sRaw(r), chunk_ptr(W, (int64_t)n_tile * nk + k, kW4ChunkBytes), raw_bytes, &rfull[r]);
+            bulk_g2s(sRaw(r), cur.get(), raw_bytes, &rfull[r]);
           } else {
             const int s = it % stages;
             if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
             mbar_expect_tx(&full[s], a_bytes + b_bytes);
-            bulk_g2s(sA(s), chunk_ptr(W, (int64_t)n_tile * nk + k, kBf16ChunkBytes), a_bytes, &full[s]);
+            bulk_g2s(sA(s), cur.get(), a_bytes, &full[s]);
             bulk_g2s(sB(s), xb + (size_t)k * b_bytes, b_bytes, &full[s]);
           }
         }
@@ -313,6 +345,242 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
   if (warp == 1) tmem_dealloc(tmem_base, 2 * tm_cols);
 }
 
+
+// --------------------------------------------------------------------------
+// W4A16 g128: dequantise straight into TENSOR MEMORY and issue the A-from-TMEM
+// form of tcgen05.mma, so the dequantised operand never touches shared memory
+// (shared memory only carries the raw int4 chunks and the activations).
+//   warp 0 lane 0   producer: raw int4 chunk ring + activation (B) ring
+//   warp 1 lane 0   UMMA issuer: tcgen05.mma [d], [a_tmem], b_desc  (M=128, N=TM)
+//   warps 2..5      epilogue (TMEM accumulators -> fp32 partials)
+//   warps 6..13     dequantisers: warp w writes TMEM lanes 32*(w%4).. (its rows),
+//                   K-half (w-6)/4 of the 128-wide group; bf16(code*scale) via
+//                   the 0x4300 magic, tcgen05.st.32x32b.x32, wait::st, arrive.
+// TMEM: [acc_bufs x TM columns of fp32 accumulators][kAStages x 64 columns of
+// packed bf16 A (row = lane, 2 K-elements per 32-bit column)] -- 512 columns.
+constexpr int kAStages = 4;
+
+__global__ void __launch_bounds__(448, 1)
+    gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
+                        float* __restrict__ out, int bstages, int rstages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int N = W.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const int nk = plan.nk;
+  const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk; a B stage holds two
+  const uint32_t raw_stage = 8576u;
+  const uint32_t tm_cols = TM <= 32 ? 32u : TM <= 64 ? 64u : TM <= 128 ? 128u : 256u;
+  const uint32_t acc_bufs = TM <= 128 ? 2u : 1u;
+  const uint32_t a_col0 = acc_bufs * tm_cols;
+
+  uint8_t* bbase = smem;
+  uint8_t* rbase = smem + (size_t)bstages * 2 * b_bytes;
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(rbase + (size_t)rstages * raw_stage);
+  uint64_t* bempty = bfull + bstages;
+  uint64_t* rfull = bempty + bstages;
+  uint64_t* rempty = rfull + rstages;
+  uint64_t* afull = rempty + rstages;
+  uint64_t* aempty = afull + kAStages;
+  uint64_t* tfull = aempty + kAStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  auto sB = [&](int s) { return bbase + (size_t)s * 2 * b_bytes; };
+  auto sRaw = [&](int r) { return rbase + (size_t)r * raw_stage; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < bstages; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    for (int r = 0; r < rstages; ++r) {
+      mbar_init(&rfull[r], 1);
+      mbar_init(&rempty[r], 256);
+    }
+    for (int a = 0; a < kAStages; ++a) {
+      mbar_init(&afull[a], 256);
+      mbar_init(&aempty[a], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t kb_per_mtile = W.K / 64;
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ producer
+      uint32_t npre = 0;  // raw chunks issued before the grid-dependency wait
+      ChunkCursor cur(W, kW4ChunkBytes);
+      {
+        SegIter pre(plan, cta);
+        int t, k0, k1;
+        while (npre < (uint32_t)rstages && pre.next(t, k0, k1)) {
+          const int n_tile = t % plan.n_tiles;
+          cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
+          for (int k = k0; k < k1 && npre < (uint32_t)rstages; ++k, ++npre, cur.advance()) {
+            mbar_expect_tx(&rfull[npre], kW4ChunkBytes);
+            bulk_g2s(sRaw(npre), cur.get(), kW4ChunkBytes, &rfull[npre]);
+          }
+        }
+      }
+      pdl_wait();
+      SegIter seg(plan, cta);
+      int t, k0, k1;
+      uint32_t it = 0;
+      while (seg.next(t, k0, k1)) {
+        const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
+        const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
+        cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
+        for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
+          const int s = it % bstages;
+          if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ((it / bstages) & 1) ^ 1);
+          mbar_expect_tx(&bfull[s], 2 * b_bytes);
+          bulk_g2s(sB(s), xb + (size_t)(2 * k) * b_bytes, 2 * b_bytes, &bfull[s]);
+          if (it >= npre) {
+            const int r = it % rstages;
+            if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
+            mbar_expect_tx(&rfull[r], kW4ChunkBytes);
+            bulk_g2s(sRaw(r), cur.get(), kW4ChunkBytes, &rfull[r]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- UMMA issuer
+      const uint32_t idesc = umma_idesc_bf16(128, (uint32_t)TM);
+      SegIter seg(plan, cta);
+      int t, k0, k1;
+      uint32_t it = 0, u = 0;
+      while (seg.next(t, k0, k1)) {
+        const uint32_t acc = acc_bufs == 2 ? (u & 1) : 0u;
+        const uint32_t use = acc_bufs == 2 ? (u >> 1) : u;
+        if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * tm_cols;
+        for (int k = k0; k < k1; ++k, ++it) {
+          const int s = it % bstages, a = it % kAStages;
+          mbar_wait(&bfull[s], (it / bstages) & 1);
+          mbar_wait(&afull[a], (it / kAStages) & 1);
+          tc_fence_after();
+          const uint32_t b0 = smem_u32(sB(s));
+          const uint32_t ta = tmem_base + a_col0 + (uint32_t)a * 64u;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t db = umma_desc(b0 + sub * b_bytes + kk * 256u, 128u, 1024u);
+              umma_bf16_ts(d, ta + sub * 32u + kk * 8u, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&bempty[s]);
+          umma_commit(&aempty[a]);
+        }
+        umma_commit(&tfull[acc]);
+        ++u;
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------- epilogue
+    pdl_wait();
+    const int quad = warp & 3;
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t u = 0;
+    while (seg.next(t, k0, k1)) {
+      const uint32_t acc = acc_bufs == 2 ? (u & 1) : 0u;
+      const uint32_t use = acc_bufs == 2 ? (u >> 1) : u;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
+      const int slot = plan.aligned ? 0 : cta - plan_cta_of(plan, (int64_t)t * nk);
+      const int n = n_tile * 128 + quad * 32 + lane;
+      float* o = out + (size_t)slot * M * N;
+      const uint32_t d = tmem_base + acc * tm_cols + ((uint32_t)(quad * 32) << 16);
+      for (int c0 = 0; c0 < TM; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(d + (uint32_t)c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int m = m_tile * TM + c0 + j;
+          if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      ++u;
+    }
+  } else {
+    // ---------------------------------------------------------- dequantisers
+    const int quad = warp & 3, half = (warp - 6) >> 2;
+    const int row = quad * 32 + lane;
+    const __nv_bfloat162 bias = __floats2bfloat162_rn(136.0f, 136.0f);
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + a_col0 + (uint32_t)half * 32u;
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t it = 0;
+    while (seg.next(t, k0, k1)) {
+      for (int k = k0; k < k1; ++k, ++it) {
+        const int rs = it % rstages, a = it % kAStages;
+        mbar_wait(&rfull[rs], (it / rstages) & 1);
+        const uint8_t* raw = sRaw(rs);
+        __nv_bfloat162 sc;
+        sc.x = __ushort_as_bfloat16(*reinterpret_cast<const uint16_t*>(raw + 8192 + 2 * row));
+        sc.y = sc.x;
+        uint32_t o[32];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const uint4 q = *reinterpret_cast<const uint4*>(raw + ((half * 2 + jj) * 128 + row) * 16);
+          const uint32_t words[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t x = ((words[w] >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
+              __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
+              v = __hmul2(__hsub2(v, bias), sc);
+              o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
+            }
+        }
+        mbar_arrive(&rempty[rs]);  // raw chunk consumed (values are in registers)
+        if (it >= (uint32_t)kAStages) mbar_wait(&aempty[a], ((it / kAStages) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st32(lane_base + (uint32_t)a * 64u, o);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&afull[a]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, 512);
+}
+
+static int pick_w4_stages(int TM, int* rstages, size_t* smem_out) {
+  const size_t budget = 215 * 1024;
+  const size_t bst = (size_t)TM * 128 * 2;
+  int bs = TM <= 64 ? 6 : (TM <= 128 ? 4 : 2);
+  int rs = (int)((budget - bs * bst) / 8576);
+  if (rs > 12) rs = 12;
+  if (rs < 2) rs = 2;
+  *rstages = rs;
+  *smem_out = bs * bst + (size_t)rs * 8576 + (2 * bs + 2 * rs + 2 * kAStages + 4) * 8 + 64;
+  return bs;
+}
+
 static size_t stage_bytes_of(bool w4, int TM) {
   const size_t b = (size_t)TM * 128;
   return w4 ? 32768 + 2 * b : 16384 + b;
@@ -362,11 +630,31 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
   return p;
 }
 
+// MS_W4_SMEM=1 selects the shared-memory dequant path (A operand in smem).
+static bool w4_tmem_path() {
+  static const bool on = [] {
+    const char* e = std::getenv("MS_W4_SMEM");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                         float* out, cudaStream_t stream) {
   size_t smem = 0;
   int rstages = 0;
   const int stages = pick_stages(w4, TM, &rstages, &smem);
+  if (w4 && w4_tmem_path()) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_w4_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr = true;
+    }
+    int rs = 0;
+    size_t sm = 0;
+    const int bs = pick_w4_stages(TM, &rs, &sm);
+    return launch_pdl(gemm_w4_tmem_kernel, dim3(plan.C), dim3(448), sm, stream, w, x, M, TM, plan, out, bs, rs);
+  }
   if (w4) {
     static bool attr = false;
     if (!attr) {

@@ -1085,10 +1085,14 @@ int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_pa
     if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "gemm: bits must be 16 or 4");
     if (N % 128 || K % 128 || M < 1 || TM % 16 || TM < 16 || TM > 256) fail(MS_EVALIDATION, "gemm: bad shape");
     static thread_local uint64_t* table = nullptr;
+    static thread_local uint64_t cached = 0;
     if (!table) CK(cudaMalloc(&table, sizeof(uint64_t)));
     const uint64_t addr = (uint64_t)w_packed;
-    CK(cudaMemcpyAsync(table, &addr, sizeof(addr), cudaMemcpyHostToDevice, (cudaStream_t)stream));
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    if (addr != cached) {  // one-entry page table for a contiguous packed matrix
+      CK(cudaMemcpyAsync(table, &addr, sizeof(addr), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+      CK(cudaStreamSynchronize((cudaStream_t)stream));
+      cached = addr;
+    }
     ms::GemmWeights w{table, 0, (int64_t)1 << 40, N, K};
     const bool w4 = bits == 4;
     int dev = 0, sms = 148;
