@@ -115,7 +115,7 @@ struct SegIter {
 template <bool kW4>
 __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
     gemm_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                float* __restrict__ out, int stages, int rstages) {
+                float* __restrict__ out, int stages, int rstages, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
               mbar_expect_tx(&rfull[npre], raw_bytes);
               bulk_g2s(sRaw(npre), cur.get(), raw_bytes, &rfull[npre]);
             } else {
-              mbar_expect_tx(&full[npre], a_bytes + b_bytes);
+              mbar_expect_tx(&full[npre], a_bytes + ((dbg & 1) ? 0u : b_bytes));
               bulk_g2s(sA(npre), cur.get(), a_bytes, &full[npre]);
             }
           }
@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
         cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
         for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
           if (it < npre) {  // weight chunk already in flight: only the activations remain
-            if (!kW4) bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
+            if (!kW4) {
+              if (dbg & 1) mbar_expect_tx(&full[it], 0);  // (debug) no B: balance nothing, arrive count already 1
+              else bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
+            }
             continue;
           }
           if (kW4) {  // raw int4 chunks only; the dequantisers fetch B
@@ -214,9 +217,9 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
           } else {
             const int s = it % stages;
             if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-            mbar_expect_tx(&full[s], a_bytes + b_bytes);
+            mbar_expect_tx(&full[s], a_bytes + ((dbg & 1) ? 0u : b_bytes));
             bulk_g2s(sA(s), cur.get(), a_bytes, &full[s]);
-            bulk_g2s(sB(s), xb + (size_t)k * b_bytes, b_bytes, &full[s]);
+            if (!(dbg & 1)) bulk_g2s(sB(s), xb + (size_t)k * b_bytes, b_bytes, &full[s]);
           }
         }
       }
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
             for (int kk = 0; kk < 4; ++kk) {
               const uint64_t da = umma_desc(a0 + sub * 16384u + kk * 256u, 128u, 1024u);
               const uint64_t db = umma_desc(b0 + sub * b_bytes + kk * 256u, 128u, 1024u);
-              umma_bf16(d, da, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
+              if (!(dbg & 2)) umma_bf16(d, da, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
             }
           }
           umma_commit(&empty[s]);
@@ -346,6 +349,15 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
 }
 
 
+// MS_GEMM_DEBUG (experiments only): bit0 skip activation loads, bit1 skip MMAs.
+static int gemm_debug() {
+  static const int v = [] {
+    const char* e = std::getenv("MS_GEMM_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 // --------------------------------------------------------------------------
 // W4A16 g128: dequantise straight into TENSOR MEMORY and issue the A-from-TMEM
 // form of tcgen05.mma, so the dequantised operand never touches shared memory
@@ -359,10 +371,11 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
 // TMEM: [acc_bufs x TM columns of fp32 accumulators][kAStages x 64 columns of
 // packed bf16 A (row = lane, 2 K-elements per 32-bit column)] -- 512 columns.
 constexpr int kAStages = 4;
+constexpr int kDqGroups = 2;  // dequantiser warp groups (4 warps each)
 
 __global__ void __launch_bounds__(448, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                        float* __restrict__ out, int bstages, int rstages) {
+                        float* __restrict__ out, int bstages, int rstages, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -395,10 +408,10 @@ __global__ void __launch_bounds__(448, 1)
     }
     for (int r = 0; r < rstages; ++r) {
       mbar_init(&rfull[r], 1);
-      mbar_init(&rempty[r], 256);
+      mbar_init(&rempty[r], 4);  // the 4 warps of the dequantiser group that took the chunk
     }
     for (int a = 0; a < kAStages; ++a) {
-      mbar_init(&afull[a], 256);
+      mbar_init(&afull[a], 4);
       mbar_init(&aempty[a], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -418,39 +431,36 @@ __global__ void __launch_bounds__(448, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ producer
-      uint32_t npre = 0;  // raw chunks issued before the grid-dependency wait
+      // raw int4 chunks: lane 0 (independent of the activation ring, so the
+      // weight stream runs `rstages` ahead; weights need no grid dependency)
       ChunkCursor cur(W, kW4ChunkBytes);
-      {
-        SegIter pre(plan, cta);
-        int t, k0, k1;
-        while (npre < (uint32_t)rstages && pre.next(t, k0, k1)) {
-          const int n_tile = t % plan.n_tiles;
-          cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
-          for (int k = k0; k < k1 && npre < (uint32_t)rstages; ++k, ++npre, cur.advance()) {
-            mbar_expect_tx(&rfull[npre], kW4ChunkBytes);
-            bulk_g2s(sRaw(npre), cur.get(), kW4ChunkBytes, &rfull[npre]);
-          }
+      SegIter seg(plan, cta);
+      int t, k0, k1;
+      uint32_t it = 0;
+      while (seg.next(t, k0, k1)) {
+        const int n_tile = t % plan.n_tiles;
+        cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
+        for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
+          const int r = it % rstages;
+          if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
+          mbar_expect_tx(&rfull[r], kW4ChunkBytes);
+          bulk_g2s(sRaw(r), cur.get(), kW4ChunkBytes, &rfull[r]);
         }
       }
+    } else if (lane == 1) {
+      // activation (B) chunks: lane 1, after the grid dependency
       pdl_wait();
       SegIter seg(plan, cta);
       int t, k0, k1;
       uint32_t it = 0;
       while (seg.next(t, k0, k1)) {
-        const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
+        const int m_tile = t / plan.n_tiles;
         const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
-        cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
-        for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
+        for (int k = k0; k < k1; ++k, ++it) {
           const int s = it % bstages;
           if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ((it / bstages) & 1) ^ 1);
           mbar_expect_tx(&bfull[s], 2 * b_bytes);
           bulk_g2s(sB(s), xb + (size_t)(2 * k) * b_bytes, 2 * b_bytes, &bfull[s]);
-          if (it >= npre) {
-            const int r = it % rstages;
-            if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
-            mbar_expect_tx(&rfull[r], kW4ChunkBytes);
-            bulk_g2s(sRaw(r), cur.get(), kW4ChunkBytes, &rfull[r]);
-          }
         }
       }
     }
@@ -479,7 +489,7 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint64_t db = umma_desc(b0 + sub * b_bytes + kk * 256u, 128u, 1024u);
-              umma_bf16_ts(d, ta + sub * 32u + kk * 8u, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
+              if (!(dbg & 2)) umma_bf16_ts(d, ta + sub * 32u + kk * 8u, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
             }
           }
           umma_commit(&bempty[s]);
@@ -523,43 +533,56 @@ __global__ void __launch_bounds__(448, 1)
     }
   } else {
     // ---------------------------------------------------------- dequantisers
-    const int quad = warp & 3, half = (warp - 6) >> 2;
+    // kDqGroups groups of 4 warps; group g takes k-steps it = g, g + kDqGroups, ...
+    // (so several k-steps are in flight); warp quadrant q owns TMEM lanes /
+    // weight rows 32q..32q+31 and dequantises the whole 128-wide group of its
+    // row: 64 packed bf16x2 columns, two tcgen05.st.32x32b.x32.
+    const int quad = warp & 3, grp = (warp - 6) >> 2;
     const int row = quad * 32 + lane;
     const __nv_bfloat162 bias = __floats2bfloat162_rn(136.0f, 136.0f);
-    const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + a_col0 + (uint32_t)half * 32u;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + a_col0;
     SegIter seg(plan, cta);
     int t, k0, k1;
     uint32_t it = 0;
     while (seg.next(t, k0, k1)) {
       for (int k = k0; k < k1; ++k, ++it) {
+        if ((int)(it % kDqGroups) != grp) continue;
         const int rs = it % rstages, a = it % kAStages;
         mbar_wait(&rfull[rs], (it / rstages) & 1);
         const uint8_t* raw = sRaw(rs);
         __nv_bfloat162 sc;
         sc.x = __ushort_as_bfloat16(*reinterpret_cast<const uint16_t*>(raw + 8192 + 2 * row));
         sc.y = sc.x;
-        uint32_t o[32];
+        uint4 q[4];
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const uint4 q = *reinterpret_cast<const uint4*>(raw + ((half * 2 + jj) * 128 + row) * 16);
-          const uint32_t words[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-          for (int w = 0; w < 4; ++w)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint32_t x = ((words[w] >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
-              __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
-              v = __hmul2(__hsub2(v, bias), sc);
-              o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
-            }
-        }
-        mbar_arrive(&rempty[rs]);  // raw chunk consumed (values are in registers)
+        for (int j = 0; j < 4; ++j) q[j] = *reinterpret_cast<const uint4*>(raw + (j * 128 + row) * 16);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[rs]);  // raw chunk consumed (values are in registers)
         if (it >= (uint32_t)kAStages) mbar_wait(&aempty[a], ((it / kAStages) & 1) ^ 1);
         tc_fence_after();
-        tmem_st32(lane_base + (uint32_t)a * 64u, o);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t o[32];
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const uint4 qq = q[hh * 2 + jj];
+            const uint32_t words[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t x = ((words[w] >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
+                __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
+                v = __hmul2(__hsub2(v, bias), sc);
+                o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
+              }
+          }
+          tmem_st32(lane_base + (uint32_t)a * 64u + (uint32_t)hh * 32u, o);
+        }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&afull[a]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[a]);
       }
     }
   }
@@ -653,7 +676,8 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
     int rs = 0;
     size_t sm = 0;
     const int bs = pick_w4_stages(TM, &rs, &sm);
-    return launch_pdl(gemm_w4_tmem_kernel, dim3(plan.C), dim3(448), sm, stream, w, x, M, TM, plan, out, bs, rs);
+    return launch_pdl(gemm_w4_tmem_kernel, dim3(plan.C), dim3(448), sm, stream, w, x, M, TM, plan, out, bs, rs,
+                      gemm_debug());
   }
   if (w4) {
     static bool attr = false;
@@ -662,7 +686,7 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
       attr = true;
     }
     return launch_pdl(gemm_kernel<true>, dim3(plan.C), dim3(448), smem, stream, w, x, M, TM, plan, out, stages,
-                      rstages);
+                      rstages, gemm_debug());
   } else {
     static bool attr = false;
     if (!attr) {
@@ -670,7 +694,7 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
       attr = true;
     }
     return launch_pdl(gemm_kernel<false>, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, stages,
-                      rstages);
+                      rstages, gemm_debug());
   }
   return cudaGetLastError();
 }
