@@ -13,6 +13,43 @@
 
 namespace ms {
 
+// Sum of the first n split-K partial slots of one element, slot order fixed.
+// The slot loads are issued together (predicated, unrolled) so their L2
+// latencies overlap instead of chaining through the adds.
+__device__ __forceinline__ float sum_slots(const float* p, size_t stride, int n) {
+  float v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = s < n ? __ldcg(p + s * stride) : 0.f;
+  float acc = 0.f;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (s < n) acc += v[s];
+  for (int s = 8; s < n; ++s) acc += __ldcg(p + s * stride);
+  return acc;
+}
+__device__ __forceinline__ float4 sum_slots4(const float4* p, size_t stride4, int n) {
+  float4 v[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) v[s] = s < n ? __ldcg(p + s * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < 6; ++s)
+    if (s < n) {
+      acc.x += v[s].x;
+      acc.y += v[s].y;
+      acc.z += v[s].z;
+      acc.w += v[s].w;
+    }
+  for (int s = 6; s < n; ++s) {
+    const float4 a = __ldcg(p + s * stride4);
+    acc.x += a.x;
+    acc.y += a.y;
+    acc.z += a.z;
+    acc.w += a.w;
+  }
+  return acc;
+}
+
 template <int kThreads>
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
@@ -67,7 +104,10 @@ cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, cons
 }
 
 // --------------------------------- QKV: split-K sum, RoPE, q out, K/V -> KV pages
-// grid (rows, H + 2*KVH heads), one thread per rotation pair (i, i + hd/2).
+// grid (rows, head groups of 8), block (hd/2, 8): one thread per rotation pair
+// (i, i + hd/2) of one head.  Few fat CTAs: thousands of 64-thread CTAs are
+// bound by the CTA launch rate, not by the (tiny) data.
+constexpr int kQkvHeadsPerCta = 8;
 __global__ void qkv_post_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int H, int KVH, int hd,
                                 const float* __restrict__ rc, const float* __restrict__ rs,
                                 const int32_t* __restrict__ pos, KvGeom kv, int layer,
@@ -75,17 +115,16 @@ __global__ void qkv_post_kernel(const float* __restrict__ part, GemmPlanDev plan
                                 int page_stride, float* __restrict__ q_out) {
   pdl_wait();
   pdl_trigger();
-  const int m = blockIdx.x, hs = blockIdx.y, i = threadIdx.x;
+  const int m = blockIdx.x, hs = blockIdx.y * kQkvHeadsPerCta + threadIdx.y, i = threadIdx.x;
+  if (hs >= H + 2 * KVH) return;
   const int N = (H + 2 * KVH) * hd;
   const int half = hd >> 1;
   const int p = pos[m];
   const size_t stride = (size_t)M * N;
   const int c0 = hs * hd + i;
   const float* src = part + (size_t)m * N + c0;
-  float x0 = 0.f, x1 = 0.f;
-  const int n0 = part_slots(plan, m, c0), n1 = part_slots(plan, m, c0 + half);
-  for (int s = 0; s < n0; ++s) x0 += src[s * stride];
-  for (int s = 0; s < n1; ++s) x1 += src[s * stride + half];
+  float x0 = sum_slots(src, stride, part_slots(plan, m, c0));
+  float x1 = sum_slots(src + half, stride, part_slots(plan, m, c0 + half));
   if (hs < H + KVH) {  // q and k heads are rotated
     const float c = rc[(size_t)p * half + i], sn = rs[(size_t)p * half + i];
     const float y0 = x0 * c - x1 * sn;
@@ -115,8 +154,10 @@ cudaError_t qkv_post_launch(const float* part, const GemmPlanDev& plan, int M, i
                             const float* rope_sin, const int32_t* pos, const KvGeom& kv, int layer,
                             const int32_t* pages, const int32_t* page_row, int page_stride, float* q_out,
                             cudaStream_t s) {
-  return launch_pdl(qkv_post_kernel, dim3(M, H + 2 * KVH), dim3(hd / 2), 0, s, part, plan, M, H, KVH, hd, rope_cos,
-                    rope_sin, pos, kv, layer, pages, page_row, page_stride, q_out);
+  const int heads = H + 2 * KVH;
+  return launch_pdl(qkv_post_kernel, dim3(M, (heads + kQkvHeadsPerCta - 1) / kQkvHeadsPerCta),
+                    dim3(hd / 2, kQkvHeadsPerCta), 0, s, part, plan, M, H, KVH, hd, rope_cos, rope_sin, pos, kv, layer,
+                    pages, page_row, page_stride, q_out);
 }
 
 // ----------------------------------- residual add (split-K sum) + RMSNorm + pack
@@ -137,14 +178,11 @@ __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __rest
   float ss = 0.f;
   for (int i4 = threadIdx.x; i4 < d4; i4 += blockDim.x) {
     float4 v = hr[i4];
-    const int ns = part_slots(plan, m, i4 * 4);
-    for (int s = 0; s < ns; ++s) {
-      const float4 a = pr[(s * stride) / 4 + i4];
-      v.x += a.x;
-      v.y += a.y;
-      v.z += a.z;
-      v.w += a.w;
-    }
+    const float4 a = sum_slots4(pr + i4, stride / 4, part_slots(plan, m, i4 * 4));
+    v.x += a.x;
+    v.y += a.y;
+    v.z += a.z;
+    v.w += a.w;
     hr[i4] = v;
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
@@ -205,15 +243,8 @@ __global__ void silu_mul_kernel(const float* __restrict__ part, GemmPlanDev plan
     const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f), u = g;
     const size_t base = (size_t)m * 2 * f4 + j4;
-    const int ng = part_slots(plan, m, j4 * 4), nu = part_slots(plan, m, ffn + j4 * 4);
-    for (int s = 0; s < ng; ++s) {
-      const float4 a = p4[s * stride4 + base];
-      g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
-    }
-    for (int s = 0; s < nu; ++s) {
-      const float4 b = p4[s * stride4 + base + f4];
-      u.x += b.x; u.y += b.y; u.z += b.z; u.w += b.w;
-    }
+    g = sum_slots4(p4 + base, stride4, part_slots(plan, m, j4 * 4));
+    u = sum_slots4(p4 + base + f4, stride4, part_slots(plan, m, ffn + j4 * 4));
     uint2 o;
     o.x = pack_bf2((g.x / (1.0f + expf(-g.x))) * u.x, (g.y / (1.0f + expf(-g.y))) * u.y);
     o.y = pack_bf2((g.z / (1.0f + expf(-g.z))) * u.z, (g.w / (1.0f + expf(-g.w))) * u.w);
@@ -225,7 +256,7 @@ cudaError_t silu_mul_launch(const float* part, const GemmPlanDev& plan, int M, i
                             cudaStream_t s) {
   const size_t total = (size_t)M * ffn / 4;
   int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > 148 * 8) blocks = 148 * 8;
   return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, s, part, plan, M, ffn, x_packed, TM);
 }
 
@@ -243,9 +274,7 @@ __global__ void __launch_bounds__(512) argmax_kernel(const float* __restrict__ p
   float best = -INFINITY;
   int besti = 0x7fffffff;
   for (int v = threadIdx.x; v < V; v += 512) {
-    float x = 0.f;
-    const int ns = part_slots(plan, m, v);
-    for (int s = 0; s < ns; ++s) x += part[s * stride + (size_t)m * V + v];
+    const float x = sum_slots(part + (size_t)m * V + v, stride, part_slots(plan, m, v));
     if (logits_out) logits_out[(size_t)m * V + v] = x;
     if (x > best || (x == best && v < besti)) {
       best = x;

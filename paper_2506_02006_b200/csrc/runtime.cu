@@ -339,6 +339,16 @@ int attn_splits(ms_ctx* c, int rows, int max_ctx) {
   return s;
 }
 
+// MS_SKIP (timing experiments only, results become garbage): bit0 qkv_post,
+// bit1 residual_norm, bit2 silu_mul, bit3 attention, bit4 layer GEMMs.
+int skip_mask() {
+  static const int v = [] {
+    const char* e = std::getenv("MS_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 // The decoder over M rows whose per-row metadata already sits in device memory.
 void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_pos, const int32_t* d_ctx,
              const int32_t* d_tokens, const int32_t* d_pages, const int32_t* d_page_row, int page_stride,
@@ -351,8 +361,10 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   const int asplits = attn_splits(c, M, max_ctx);
   for (int l = 0; l < D.num_layers; ++l) {
     const bool w4 = c->layers[l].bits == 4;
-    ms::GemmPlanDev s = gemm(c, mat_weights(c, l, 0), w4, M, TM);
-    CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
+    const int skip = skip_mask();
+    ms::GemmPlanDev s = (skip & 16) ? ms::gemm_plan(1024, 1024, M, TM, false, c->num_sms, c->part_elems)
+                                    : gemm(c, mat_weights(c, l, 0), w4, M, TM);
+    if (!(skip & 1)) CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
                            d_page_row, page_stride, c->q, c->compute));
     c->launches += 1;
     ms::AttnArgs a{};
@@ -374,22 +386,23 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     a.out_packed = 1;
     a.TM = TM;
     prof_mark(c);
-    CK(ms::attn_decode_launch(a, c->compute));
+    if (!(skip & 8)) CK(ms::attn_decode_launch(a, c->compute));
     prof_mark(c);
     c->launches += asplits > 1 ? 2 : 1;
-    s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
-    CK(ms::residual_norm_launch(c->part, s, M, d, c->h, c->norms + ((size_t)l * 2 + 1) * d, D.rms_eps, c->x, TM,
+    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
+    if (!(skip & 2)) CK(ms::residual_norm_launch(c->part, s, M, d, c->h, c->norms + ((size_t)l * 2 + 1) * d, D.rms_eps, c->x, TM,
                                 c->compute));
     c->launches += 1;
-    s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
-    CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
+    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
+    if (!(skip & 4)) CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
     c->launches += 1;
-    s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
+    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
     const bool last = l == D.num_layers - 1;
     const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
     const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
-    CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out,
-                                     last ? final_row_begin : 0, c->compute));
+    if (!(skip & 2) || last)
+      CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out,
+                                       last ? final_row_begin : 0, c->compute));
     c->launches += 1;
   }
   const int Mo = M - final_row_begin;
