@@ -192,7 +192,7 @@ def run_ours(args):
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    total_steps = 2 * (args.warmup + args.steps) + args.steps + 2 * max(4, args.steps // 2) + args.e2e_steps + 8
+    total_steps = 2 * (args.warmup + args.steps) + args.steps + 6 * max(4, args.steps // 2) + args.e2e_steps + 8
     dev, table = build_model(local_rank, total_steps)
     slots = np.arange(BATCH, dtype=np.int32)
     pos = np.full(BATCH, CTX - 1, dtype=np.int32)
@@ -256,33 +256,46 @@ def run_ours(args):
     # then the freed pages are carved into KV ids and detached back) vs without.
     swap_layer = W4_LAYERS[0]
     nsw = max(4, args.steps // 2)
-    t_noswap, _, _, _, _ = timed(nsw)
-    barrier()
-    dev.sync()
-    dev.timer_start()
-    ticket = dev.swap_begin(swap_layer, 16)
-    swaps = 0
     extra_id = 10_000_000
-    for _ in range(nsw):
-        dev.decode(slots, pos, table, want_next=False)
-        pos = pos + 1
-        if dev.swap_done(ticket):
-            freed = dev.swap_commit(ticket)
-            swaps += 1
-            if ticket.bits == 4:  # down-swap: attach the freed pages as KV blocks, then give them back
-                n_att = freed - dev_layer_pages(4)
-                if n_att > 0:
-                    dev.kv_attach(extra_id, n_att)
-                    dev.kv_detach(list(range(extra_id, extra_id + n_att)))
-                    extra_id += n_att
-            ticket = dev.swap_begin(swap_layer, 4 if ticket.bits == 16 else 16)
-    t_swap = dev.timer_stop()
-    dev.swap_wait(ticket)
-    dev.swap_commit(ticket)
-    if dev.layer_bits(swap_layer) != 4:
-        t2 = dev.swap_begin(swap_layer, 4)
-        dev.swap_wait(t2)
-        dev.swap_commit(t2)
+
+    def swap_window(n):
+        """n decode steps while layer `swap_layer` streams W4 <-> BF16 images."""
+        nonlocal pos, extra_id
+        barrier()
+        dev.sync()
+        dev.timer_start()
+        ticket = dev.swap_begin(swap_layer, 16)
+        done = 0
+        for _ in range(n):
+            dev.decode(slots, pos, table, want_next=False)
+            pos = pos + 1
+            if dev.swap_done(ticket):
+                freed = dev.swap_commit(ticket)
+                done += 1
+                if ticket.bits == 4:  # down-swap: carve the freed pages into KV ids, then detach them
+                    n_att = freed - dev_layer_pages(4)
+                    if n_att > 0:
+                        dev.kv_attach(extra_id, n_att)
+                        dev.kv_detach(list(range(extra_id, extra_id + n_att)))
+                        extra_id += n_att
+                ticket = dev.swap_begin(swap_layer, 4 if ticket.bits == 16 else 16)
+        t = dev.timer_stop()
+        dev.swap_wait(ticket)
+        dev.swap_commit(ticket)
+        if dev.layer_bits(swap_layer) != 4:
+            t2 = dev.swap_begin(swap_layer, 4)
+            dev.swap_wait(t2)
+            dev.swap_commit(t2)
+        return t, done
+
+    # alternate A (no swap) / B (swap traffic) three times; medians
+    t_a, t_b, swaps = [], [], 0
+    for _ in range(3):
+        t_a.append(timed(nsw)[0])
+        tb, dn = swap_window(nsw)
+        t_b.append(tb)
+        swaps += dn
+    t_noswap, t_swap = float(np.median(t_a)), float(np.median(t_b))
     stall_ms_per_token = max(0.0, t_swap - t_noswap) / (nsw * BATCH)
     # ---- e2e through the C ABI with host buffers: H2D of the step inputs
     # (tokens, slots, positions, block table) and D2H of the next tokens.
@@ -350,7 +363,10 @@ def run_ours(args):
         "serving": serving,
         "swap_upload_ms": {"w4_layer_mean": float(np.mean(swap_ms))},
         "swap_exposed_stall_ms_per_token": stall_ms_per_token,
-        "swap_stall_test": {"steps": nsw, "swaps_committed": swaps, "ms_without": t_noswap, "ms_with": t_swap},
+        "swap_stall_test": {"steps_per_window": nsw, "windows": 3, "swaps_committed": swaps,
+                            "ms_without_median": t_noswap, "ms_with_median": t_swap,
+                            "ms_without": t_a, "ms_with": t_b,
+                            "frac_of_tpot": (max(0.0, t_swap - t_noswap) / t_noswap) if t_noswap else None},
         "e2e": {"value": BATCH * args.e2e_steps * world / e2e_s, "unit": "tok/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
