@@ -170,6 +170,12 @@ int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int 
                      int KVH, int hd, const int32_t* pages, int max_blocks, const int32_t* ctx_len, int rows,
                      int splits, float* workspace, uint16_t* out, void* stream);
 
+/* Causal prefill attention of one sequence (positions 0..n-1): q [n][H][hd]
+ * fp32, pages = that sequence's page index per 16-token block; out bf16
+ * [n][H*hd] row-major. */
+int ms_k_attn_prefill(const float* q, const void* arena, int64_t page_bytes, int layers, int layer, int H, int KVH,
+                      int hd, const int32_t* pages, int n, uint16_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

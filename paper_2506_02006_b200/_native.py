@@ -89,6 +89,8 @@ SIGNATURES = [
     ("ms_k_pack_act", C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _P]),
     ("ms_k_gemm", C.c_int, [C.c_int, _P, C.c_int, C.c_int, _P, C.c_int, C.c_int, C.c_int, _P,
                             C.POINTER(C.c_int), _P]),
+    ("ms_k_attn_prefill", C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_int,
+                                    _P, _P]),
     ("ms_k_attn_decode", C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P,
                                    C.c_int, _P, C.c_int, C.c_int, _P, _P, _P]),
 ]

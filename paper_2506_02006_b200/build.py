@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
            "-I" + os.path.join(ROOT, "include")]
-CU_SOURCES = ["gemm.cu", "attention.cu", "elementwise.cu", "runtime.cu"]
+CU_SOURCES = ["gemm.cu", "attention.cu", "prefill_attention.cu", "elementwise.cu", "runtime.cu"]
 
 
 def _run(cmd):

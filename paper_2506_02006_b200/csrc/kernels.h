@@ -101,6 +101,19 @@ struct AttnArgs {
 };
 cudaError_t attn_decode_launch(const AttnArgs& a, cudaStream_t stream);
 
+// Causal prefill attention of ONE sequence (positions 0..n-1) over its paged KV.
+struct PrefillAttnArgs {
+  const float* q;         // [n][H][hd] fp32, RoPE applied
+  KvGeom kv;
+  int layer;
+  const int32_t* pages;   // the sequence's page indices (block j -> page)
+  int n, H, KVH;
+  float scale_log2;
+  uint16_t* out;          // packed activation image (TM > 0) or row-major [n][H*hd] (TM == 0)
+  int TM;
+};
+cudaError_t prefill_attn_launch(const PrefillAttnArgs& a, cudaStream_t stream);
+
 // elementwise / row kernels (elementwise.cu)
 cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, const int32_t* hist,
                               const int32_t* slot, const int32_t* pos, int hist_stride, int M, int d,

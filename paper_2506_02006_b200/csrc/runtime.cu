@@ -367,28 +367,45 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     if (!(skip & 1)) CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
                            d_page_row, page_stride, c->q, c->compute));
     c->launches += 1;
-    ms::AttnArgs a{};
-    a.q = c->q;
-    a.kv = c->kv;
-    a.layer = l;
-    a.pages = d_pages;
-    a.page_row = d_page_row;
-    a.page_stride = page_stride;
-    a.ctx_len = d_ctx;
-    a.rows = M;
-    a.H = H;
-    a.KVH = KVH;
-    a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-    a.splits = asplits;
-    a.part_o = c->attn_ws;
-    a.part_ml = c->attn_ws + (size_t)asplits * M * H * hd;
-    a.out = c->x;
-    a.out_packed = 1;
-    a.TM = TM;
     prof_mark(c);
-    if (!(skip & 8)) CK(ms::attn_decode_launch(a, c->compute));
+    if (d_page_row != nullptr) {
+      // prefill: one sequence, tiled causal attention (page table row 0)
+      ms::PrefillAttnArgs pa{};
+      pa.q = c->q;
+      pa.kv = c->kv;
+      pa.layer = l;
+      pa.pages = d_pages;
+      pa.n = M;
+      pa.H = H;
+      pa.KVH = KVH;
+      pa.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+      pa.out = c->x;
+      pa.TM = TM;
+      if (!(skip & 8)) CK(ms::prefill_attn_launch(pa, c->compute));
+      c->launches += 1;
+    } else {
+      ms::AttnArgs a{};
+      a.q = c->q;
+      a.kv = c->kv;
+      a.layer = l;
+      a.pages = d_pages;
+      a.page_row = d_page_row;
+      a.page_stride = page_stride;
+      a.ctx_len = d_ctx;
+      a.rows = M;
+      a.H = H;
+      a.KVH = KVH;
+      a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+      a.splits = asplits;
+      a.part_o = c->attn_ws;
+      a.part_ml = c->attn_ws + (size_t)asplits * M * H * hd;
+      a.out = c->x;
+      a.out_packed = 1;
+      a.TM = TM;
+      if (!(skip & 8)) CK(ms::attn_decode_launch(a, c->compute));
+      c->launches += asplits > 1 ? 2 : 1;
+    }
     prof_mark(c);
-    c->launches += asplits > 1 ? 2 : 1;
     if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
     if (!(skip & 2)) CK(ms::residual_norm_launch(c->part, s, M, d, c->h, c->norms + ((size_t)l * 2 + 1) * d, D.rms_eps, c->x, TM,
                                 c->compute));
@@ -1145,6 +1162,25 @@ int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int 
     a.TM = 16;
     if (a.splits > 1 && !workspace) fail(MS_EVALIDATION, "attn: split-KV needs a workspace");
     CK(ms::attn_decode_launch(a, (cudaStream_t)stream));
+  });
+}
+
+int ms_k_attn_prefill(const float* q, const void* arena, int64_t page_bytes, int layers, int layer, int H, int KVH,
+                      int hd, const int32_t* pages, int n, uint16_t* out, void* stream) {
+  return guard([&] {
+    ms::PrefillAttnArgs a{};
+    a.q = q;
+    a.kv = ms::KvGeom{(char*)arena, page_bytes, layers, KVH, hd, 16};
+    a.layer = layer;
+    a.pages = pages;
+    a.n = n;
+    a.H = H;
+    a.KVH = KVH;
+    a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    a.out = out;
+    a.TM = 0;
+    if (n < 1 || H % KVH) fail(MS_EVALIDATION, "attn_prefill: bad shape");
+    CK(ms::prefill_attn_launch(a, (cudaStream_t)stream));
   });
 }
 

@@ -162,3 +162,40 @@ def test_paged_attention(H, KVH, hd, ctxs, splits):
         _, ref32 = O.attention(q[r].reshape(-1), k, v, H, KVH, hd)
         # bf16 output rounding (2^-8 relative) + fp32 softmax/accumulation
         np.testing.assert_allclose(got[r], ref32, rtol=1e-2, atol=2e-3)
+
+
+@pytest.mark.parametrize("H,KVH,hd,n", [(4, 2, 64, 1), (4, 2, 64, 77), (8, 8, 128, 130), (32, 8, 128, 300),
+                                        (8, 1, 128, 64)])
+def test_prefill_attention(H, KVH, hd, n):
+    """Causal prefill attention over paged KV vs the oracle, query by query."""
+    N = _native()
+    L, layer = 2, 1
+    page_bytes = 16 * L * KVH * 2 * hd * 2
+    nb = (n + 15) // 16
+    n_pages = nb + 3
+    rng = np.random.default_rng(5)
+    arena = O.f32_to_bf16(rng.uniform(-1, 1, n_pages * page_bytes // 2).astype(np.float32))
+    pages = rng.permutation(n_pages).astype(np.int32)[:nb]
+    q = rng.uniform(-1, 1, (n, H, hd)).astype(np.float32)
+    d_arena = dev_u16(arena)
+    d_q = torch.from_numpy(q).cuda()
+    d_pages = torch.from_numpy(pages.copy()).cuda()
+    out = torch.empty(n * H * hd, dtype=torch.int16, device="cuda")
+    N.check(N.lib().ms_k_attn_prefill(C.c_void_p(d_q.data_ptr()), C.c_void_p(d_arena.data_ptr()), page_bytes, L,
+                                      layer, H, KVH, hd, C.c_void_p(d_pages.data_ptr()), n,
+                                      C.c_void_p(out.data_ptr()), stream()))
+    torch.cuda.synchronize()
+    got = O.bf16_to_f32(to_np_u16(out)).reshape(n, H * hd)
+    head_elems = 16 * hd
+    k = np.empty((n, KVH, hd), np.uint16)
+    v = np.empty((n, KVH, hd), np.uint16)
+    for t in range(n):
+        base = pages[t // 16] * (page_bytes // 2) + layer * KVH * 2 * head_elems
+        for kh in range(KVH):
+            off = base + kh * 2 * head_elems + (t % 16) * hd
+            k[t, kh] = arena[off: off + hd]
+            v[t, kh] = arena[off + head_elems: off + head_elems + hd]
+    for qi in sorted({0, n // 3, n // 2, n - 1}):
+        _, ref32 = O.attention(q[qi].reshape(-1), k[: qi + 1], v[: qi + 1], H, KVH, hd)
+        # P is rounded to bf16 for the PV MMA (scores keep fp32 accuracy via the q hi/lo split)
+        np.testing.assert_allclose(got[qi], ref32, rtol=2e-2, atol=4e-3)
