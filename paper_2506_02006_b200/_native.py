@@ -9,7 +9,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmorphserve.so")
+_LIB_PATH = os.path.join(os.environ.get("MS_LIB_DIR") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib"),
+                         "libmorphserve.so")
 
 MS_OK, MS_EVALIDATION, MS_ERUNTIME, MS_ELOGIC = 0, 2, 3, 4
 

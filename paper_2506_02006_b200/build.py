@@ -16,13 +16,14 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "lib")
-OBJ = os.path.join(PKG, "lib", "obj")
+LIB = os.environ.get("MS_LIB_DIR", os.path.join(PKG, "lib"))  # MS_LIB_DIR: experiment variants only
+OBJ = os.path.join(LIB, "obj")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
            "-I" + os.path.join(ROOT, "include")]
+NVFLAGS += os.environ.get("MS_NVCC_EXTRA", "").split()  # experiments only
 CU_SOURCES = ["gemm.cu", "attention.cu", "prefill_attention.cu", "elementwise.cu", "runtime.cu"]
 
 

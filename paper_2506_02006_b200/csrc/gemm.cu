@@ -349,7 +349,8 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
 }
 
 
-// MS_GEMM_DEBUG (experiments only): bit0 skip activation loads, bit1 skip MMAs.
+// MS_GEMM_DEBUG (experiments only): bit0 skip activation loads, bit1 skip MMAs,
+// bit2 (W4 TMEM) skip the dequant ALU work and TMEM stores.
 static int gemm_debug() {
   static const int v = [] {
     const char* e = std::getenv("MS_GEMM_DEBUG");
@@ -362,20 +363,31 @@ static int gemm_debug() {
 // W4A16 g128: dequantise straight into TENSOR MEMORY and issue the A-from-TMEM
 // form of tcgen05.mma, so the dequantised operand never touches shared memory
 // (shared memory only carries the raw int4 chunks and the activations).
-//   warp 0 lane 0   producer: raw int4 chunk ring + activation (B) ring
+//   warp 0 lane 0   producer: raw int4 chunk ring (weights: no grid dependency)
 //   warp 1 lane 0   UMMA issuer: tcgen05.mma [d], [a_tmem], b_desc  (M=128, N=TM)
 //   warps 2..5      epilogue (TMEM accumulators -> fp32 partials)
-//   warps 6..13     dequantisers: warp w writes TMEM lanes 32*(w%4).. (its rows),
-//                   K-half (w-6)/4 of the 128-wide group; bf16(code*scale) via
-//                   the 0x4300 magic, tcgen05.st.32x32b.x32, wait::st, arrive.
-// TMEM: [acc_bufs x TM columns of fp32 accumulators][kAStages x 64 columns of
+//   warp 6 lane 0   activation (B) ring, after the grid dependency (own warp:
+//                   two spin-waiting roles in one warp serialise each other)
+//   warps 7..       kG dequantiser groups of 4 warps: warp w writes TMEM lanes
+//                   32*(w%4).. (its rows); bf16(code*scale) via the 0x4300
+//                   magic, tcgen05.st.32x32b.x32, wait::st, arrive.
+// TMEM: [acc_bufs x TM columns of fp32 accumulators][astages x 64 columns of
 // packed bf16 A (row = lane, 2 K-elements per 32-bit column)] -- 512 columns.
-constexpr int kAStages = 4;
-constexpr int kDqGroups = 2;  // dequantiser warp groups (4 warps each)
+// kG dequantiser groups of 4 warps each keep kG chunks in flight, so the
+// dequant ALU work (~4 instructions per bf16x2) is latency-hidden.
+constexpr int kMaxAStages = 8;
 
-__global__ void __launch_bounds__(448, 1)
+// bf16x2 (128 + nib_lo, 128 + nib_hi) from the nibbles at bits 0..3 / 16..19.
+__device__ __forceinline__ uint32_t nib_magic(uint32_t w) {
+  uint32_t x;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(w), "r"(0x000F000Fu), "r"(0x43004300u));
+  return x;
+}
+
+template <int kG>
+__global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                        float* __restrict__ out, int bstages, int rstages, int dbg) {
+                        float* __restrict__ out, int bstages, int rstages, int astages, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -386,6 +398,15 @@ __global__ void __launch_bounds__(448, 1)
   const uint32_t tm_cols = TM <= 32 ? 32u : TM <= 64 ? 64u : TM <= 128 ? 128u : 256u;
   const uint32_t acc_bufs = TM <= 128 ? 2u : 1u;
   const uint32_t a_col0 = acc_bufs * tm_cols;
+  // (debug, dbg bit3, kernel microbench only) CTA 0 timeline: [event][it] globaltimer
+  uint64_t* tl = (dbg & 8) && blockIdx.x == 0 ? reinterpret_cast<uint64_t*>(out + (size_t)150 * M * N) : nullptr;
+  auto stamp = [&](int ev, uint32_t i) {
+    if (tl && i < 64) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      tl[ev * 64 + i] = t;
+    }
+  };
 
   uint8_t* bbase = smem;
   uint8_t* rbase = smem + (size_t)bstages * 2 * b_bytes;
@@ -394,8 +415,8 @@ __global__ void __launch_bounds__(448, 1)
   uint64_t* rfull = bempty + bstages;
   uint64_t* rempty = rfull + rstages;
   uint64_t* afull = rempty + rstages;
-  uint64_t* aempty = afull + kAStages;
-  uint64_t* tfull = aempty + kAStages;
+  uint64_t* aempty = afull + kMaxAStages;
+  uint64_t* tfull = aempty + kMaxAStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   auto sB = [&](int s) { return bbase + (size_t)s * 2 * b_bytes; };
@@ -410,7 +431,7 @@ __global__ void __launch_bounds__(448, 1)
       mbar_init(&rfull[r], 1);
       mbar_init(&rempty[r], 4);  // the 4 warps of the dequantiser group that took the chunk
     }
-    for (int a = 0; a < kAStages; ++a) {
+    for (int a = 0; a < astages; ++a) {
       mbar_init(&afull[a], 4);
       mbar_init(&aempty[a], 1);
     }
@@ -420,6 +441,7 @@ __global__ void __launch_bounds__(448, 1)
     }
     fence_mbar_init();
   }
+  stamp(6, threadIdx.x == 0 ? 0 : 64);
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -431,8 +453,8 @@ __global__ void __launch_bounds__(448, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ producer
-      // raw int4 chunks: lane 0 (independent of the activation ring, so the
-      // weight stream runs `rstages` ahead; weights need no grid dependency)
+      // raw int4 chunks (independent of the activation ring, so the weight
+      // stream runs `rstages` ahead; weights need no grid dependency)
       ChunkCursor cur(W, kW4ChunkBytes);
       SegIter seg(plan, cta);
       int t, k0, k1;
@@ -445,22 +467,7 @@ __global__ void __launch_bounds__(448, 1)
           if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
           mbar_expect_tx(&rfull[r], kW4ChunkBytes);
           bulk_g2s(sRaw(r), cur.get(), kW4ChunkBytes, &rfull[r]);
-        }
-      }
-    } else if (lane == 1) {
-      // activation (B) chunks: lane 1, after the grid dependency
-      pdl_wait();
-      SegIter seg(plan, cta);
-      int t, k0, k1;
-      uint32_t it = 0;
-      while (seg.next(t, k0, k1)) {
-        const int m_tile = t / plan.n_tiles;
-        const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
-        for (int k = k0; k < k1; ++k, ++it) {
-          const int s = it % bstages;
-          if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ((it / bstages) & 1) ^ 1);
-          mbar_expect_tx(&bfull[s], 2 * b_bytes);
-          bulk_g2s(sB(s), xb + (size_t)(2 * k) * b_bytes, 2 * b_bytes, &bfull[s]);
+          stamp(0, it);
         }
       }
     }
@@ -478,9 +485,10 @@ __global__ void __launch_bounds__(448, 1)
         tc_fence_after();
         const uint32_t d = tmem_base + acc * tm_cols;
         for (int k = k0; k < k1; ++k, ++it) {
-          const int s = it % bstages, a = it % kAStages;
+          const int s = it % bstages, a = it % astages;
           mbar_wait(&bfull[s], (it / bstages) & 1);
-          mbar_wait(&afull[a], (it / kAStages) & 1);
+          mbar_wait(&afull[a], (it / astages) & 1);
+          stamp(4, it);
           tc_fence_after();
           const uint32_t b0 = smem_u32(sB(s));
           const uint32_t ta = tmem_base + a_col0 + (uint32_t)a * 64u;
@@ -497,6 +505,30 @@ __global__ void __launch_bounds__(448, 1)
         }
         umma_commit(&tfull[acc]);
         ++u;
+      }
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {
+      // activation (B) chunks: own warp (a spin-wait here must not hold up the
+      // weight producer), after the grid dependency
+      pdl_wait();
+      SegIter seg(plan, cta);
+      int t, k0, k1;
+      uint32_t it = 0;
+      while (seg.next(t, k0, k1)) {
+        const int m_tile = t / plan.n_tiles;
+        const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
+        for (int k = k0; k < k1; ++k, ++it) {
+          const int s = it % bstages;
+          if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ((it / bstages) & 1) ^ 1);
+          if (dbg & 1) {  // (debug) no activation traffic: complete the stage empty
+            mbar_expect_tx(&bfull[s], 0);
+            continue;
+          }
+          mbar_expect_tx(&bfull[s], 2 * b_bytes);
+          bulk_g2s(sB(s), xb + (size_t)(2 * k) * b_bytes, 2 * b_bytes, &bfull[s]);
+          stamp(5, it);
+        }
       }
     }
   } else if (warp < 6) {
@@ -529,15 +561,16 @@ __global__ void __launch_bounds__(448, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0 && quad == 0) stamp(7, u);
       ++u;
     }
   } else {
     // ---------------------------------------------------------- dequantisers
-    // kDqGroups groups of 4 warps; group g takes k-steps it = g, g + kDqGroups, ...
-    // (so several k-steps are in flight); warp quadrant q owns TMEM lanes /
-    // weight rows 32q..32q+31 and dequantises the whole 128-wide group of its
-    // row: 64 packed bf16x2 columns, two tcgen05.st.32x32b.x32.
-    const int quad = warp & 3, grp = (warp - 6) >> 2;
+    // kG groups of 4 warps; group g takes k-steps it = g, g + kG, ... (so kG
+    // chunks are in flight); warp quadrant q owns TMEM lanes / weight rows
+    // 32q..32q+31 and dequantises the whole 128-wide group of its row: 64
+    // packed bf16x2 columns, two tcgen05.st.32x32b.x32.
+    const int quad = warp & 3, grp = (warp - 7) >> 2;
     const int row = quad * 32 + lane;
     const __nv_bfloat162 bias = __floats2bfloat162_rn(136.0f, 136.0f);
     const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + a_col0;
@@ -545,10 +578,13 @@ __global__ void __launch_bounds__(448, 1)
     int t, k0, k1;
     uint32_t it = 0;
     while (seg.next(t, k0, k1)) {
-      for (int k = k0; k < k1; ++k, ++it) {
-        if ((int)(it % kDqGroups) != grp) continue;
-        const int rs = it % rstages, a = it % kAStages;
+      // first k-step of this segment owned by this group
+      int k = k0 + (int)((grp - (int)(it % kG) + kG) % kG);
+      it += (uint32_t)(k - k0);
+      for (; k < k1; k += kG, it += kG) {
+        const int rs = it % rstages, a = it % astages;
         mbar_wait(&rfull[rs], (it / rstages) & 1);
+        if (lane == 0 && quad == 0) stamp(1, it);
         const uint8_t* raw = sRaw(rs);
         __nv_bfloat162 sc;
         sc.x = __ushort_as_bfloat16(*reinterpret_cast<const uint16_t*>(raw + 8192 + 2 * row));
@@ -558,8 +594,14 @@ __global__ void __launch_bounds__(448, 1)
         for (int j = 0; j < 4; ++j) q[j] = *reinterpret_cast<const uint4*>(raw + (j * 128 + row) * 16);
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[rs]);  // raw chunk consumed (values are in registers)
-        if (it >= (uint32_t)kAStages) mbar_wait(&aempty[a], ((it / kAStages) & 1) ^ 1);
+        if (it >= (uint32_t)astages) mbar_wait(&aempty[a], ((it / astages) & 1) ^ 1);
+        if (lane == 0 && quad == 0) stamp(2, it);
         tc_fence_after();
+        if (dbg & 4) {  // (debug) no dequant ALU / TMEM stores: hand the stage straight on
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&afull[a]);
+          continue;
+        }
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           uint32_t o[32];
@@ -571,9 +613,9 @@ __global__ void __launch_bounds__(448, 1)
             for (int w = 0; w < 4; ++w)
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                const uint32_t x = ((words[w] >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
+                const uint32_t x = nib_magic(words[w] >> (4 * i));
                 __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
-                v = __hmul2(__hsub2(v, bias), sc);
+                v = __hmul2(__hsub2(v, bias), sc);  // exact code, then one rounding of code*scale
                 o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
               }
           }
@@ -583,24 +625,40 @@ __global__ void __launch_bounds__(448, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[a]);
+        if (lane == 0 && quad == 0) stamp(3, it);
       }
+      it -= (uint32_t)(k - k1);  // back to the segment end
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  stamp(6, threadIdx.x == 0 ? 1 : 64);
   if (warp == 1) tmem_dealloc(tmem_base, 512);
 }
 
-static int pick_w4_stages(int TM, int* rstages, size_t* smem_out) {
+// Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 4).
+static int w4_groups() {
+  static const int v = [] {
+    const char* e = std::getenv("MS_W4_GROUPS");
+    const int g = e ? std::atoi(e) : 4;
+    return g == 2 || g == 3 ? g : 4;
+  }();
+  return v;
+}
+
+static int pick_w4_stages(int TM, int* rstages, int* astages, size_t* smem_out) {
   const size_t budget = 215 * 1024;
   const size_t bst = (size_t)TM * 128 * 2;
   int bs = TM <= 64 ? 6 : (TM <= 128 ? 4 : 2);
   int rs = (int)((budget - bs * bst) / 8576);
-  if (rs > 12) rs = 12;
+  if (rs > 16) rs = 16;
   if (rs < 2) rs = 2;
   *rstages = rs;
-  *smem_out = bs * bst + (size_t)rs * 8576 + (2 * bs + 2 * rs + 2 * kAStages + 4) * 8 + 64;
+  const int tm_cols = TM <= 32 ? 32 : TM <= 64 ? 64 : TM <= 128 ? 128 : 256;
+  const int acc = (TM <= 128 ? 2 : 1) * tm_cols;
+  *astages = std::min(kMaxAStages, (512 - acc) / 64);
+  *smem_out = bs * bst + (size_t)rs * 8576 + (2 * bs + 2 * rs + 2 * kMaxAStages + 4) * 8 + 64;
   return bs;
 }
 
@@ -662,22 +720,32 @@ static bool w4_tmem_path() {
   return on;
 }
 
+template <int kG>
+static cudaError_t launch_w4_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+                                  float* out, int bs, int rs, int as, size_t sm, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  return launch_pdl(gemm_w4_tmem_kernel<kG>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M, TM, plan,
+                    out, bs, rs, as, gemm_debug());
+}
+
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                         float* out, cudaStream_t stream) {
   size_t smem = 0;
   int rstages = 0;
   const int stages = pick_stages(w4, TM, &rstages, &smem);
   if (w4 && w4_tmem_path()) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_w4_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
-    }
-    int rs = 0;
+    int rs = 0, as = 0;
     size_t sm = 0;
-    const int bs = pick_w4_stages(TM, &rs, &sm);
-    return launch_pdl(gemm_w4_tmem_kernel, dim3(plan.C), dim3(448), sm, stream, w, x, M, TM, plan, out, bs, rs,
-                      gemm_debug());
+    const int bs = pick_w4_stages(TM, &rs, &as, &sm);
+    switch (w4_groups()) {
+      case 2: return launch_w4_tmem<2>(w, x, M, TM, plan, out, bs, rs, as, sm, stream);
+      case 3: return launch_w4_tmem<3>(w, x, M, TM, plan, out, bs, rs, as, sm, stream);
+      default: return launch_w4_tmem<4>(w, x, M, TM, plan, out, bs, rs, as, sm, stream);
+    }
   }
   if (w4) {
     static bool attr = false;

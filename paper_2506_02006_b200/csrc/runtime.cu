@@ -12,8 +12,10 @@
 //   CostModel::swap_duration_ms      proj/src/sim_config.cpp:29-33  -> ms_swap_begin (+ copy stream)
 //   MorphState::complete_swap        proj/src/engine.cpp:30-38      -> ms_swap_commit (pointer flip)
 //   KvBlockPool::attach/detach       proj/src/kv_pool.cpp:77-100    -> ms_kv_attach / ms_kv_detach
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -132,7 +134,8 @@ struct Layer {
 };
 
 struct Staging {  // one slot of the per-step H2D ring
-  int32_t* h = nullptr;   // pinned
+  int32_t* h = nullptr;   // pinned, mapped
+  int32_t* hd = nullptr;  // device alias of h (zero-copy)
   int32_t* d = nullptr;   // device
   size_t words = 0;
   cudaEvent_t used = nullptr;
@@ -244,15 +247,29 @@ void write_table(ms_ctx* c, Layer& L, int slot, const std::vector<int32_t>& page
   CK(cudaMemcpyAsync(L.d_table[slot], L.h_table[slot], pages.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
 }
 
+// Upload granularity: the LayerSwapper's H2D copies share the copy engines
+// with each decode step's small metadata upload, so they are issued in
+// pieces of at most this many bytes (MS_UPLOAD_CHUNK; default 0 = whole pages:
+// measured, smaller pieces do not reduce the decode stall).
+int64_t upload_piece_bytes() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("MS_UPLOAD_CHUNK");
+    return e ? (int64_t)std::atoll(e) : (int64_t)0;
+  }();
+  return v;
+}
+
 void upload_image(ms_ctx* c, const uint8_t* img, const ImageGeom& g, const std::vector<int32_t>& pages,
                   cudaStream_t s) {
-  const int64_t used = g.cpp * g.chunk_bytes;
+  const int64_t piece = upload_piece_bytes();
   for (int64_t p = 0; p < g.pages; ++p) {
     const int64_t chunks = std::min<int64_t>(g.cpp, g.total_chunks - p * g.cpp);
     const int64_t bytes = chunks * g.chunk_bytes;
-    (void)used;
-    CK(cudaMemcpyAsync(c->arena + (int64_t)pages[p] * c->page_bytes, img + p * c->page_bytes, bytes,
-                       cudaMemcpyHostToDevice, s));
+    char* dst = c->arena + (int64_t)pages[p] * c->page_bytes;
+    const uint8_t* src = img + p * c->page_bytes;
+    const int64_t step = piece > 0 ? piece : bytes;
+    for (int64_t off = 0; off < bytes; off += step)
+      CK(cudaMemcpyAsync(dst + off, src + off, std::min(step, bytes - off), cudaMemcpyHostToDevice, s));
   }
 }
 
@@ -438,8 +455,9 @@ Staging& next_staging(ms_ctx* c, size_t words) {
   if (st.words < words) {
     if (st.h) cudaFreeHost(st.h);
     if (st.d) cudaFree(st.d);
-    st.words = words * 2;
-    CK(cudaHostAlloc(&st.h, st.words * 4, cudaHostAllocDefault));
+    st.words = words * 2 + 4;
+    CK(cudaHostAlloc(&st.h, st.words * 4, cudaHostAllocMapped | cudaHostAllocPortable));
+    CK(cudaHostGetDevicePointer(&st.hd, st.h, 0));
     CK(cudaMalloc(&st.d, st.words * 4));
   }
   return st;
@@ -454,6 +472,29 @@ int32_t page_of(ms_ctx* c, int64_t id) {
 void check_ready(ms_ctx* c) {
   if (!c->weights_ready) fail(MS_EVALIDATION, "weights not initialised");
   if (!c->hist) fail(MS_EVALIDATION, "token history not reserved (ms_hist_reserve)");
+}
+
+// Per-step metadata upload by zero-copy reads of the mapped staging buffer:
+// the step never queues behind LayerSwapper uploads in the copy engines
+// (a cudaMemcpyAsync H2D on the compute stream waits for every H2D copy
+// submitted before it, i.e. for a whole in-flight layer image).
+__global__ void stage_in_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void hist_in_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+
+void stage_in(ms_ctx* c, Staging& st, size_t words) {
+  const int64_t n16 = (int64_t)((words * 4 + 15) / 16);
+  const int blocks = (int)std::min<int64_t>(64, (n16 + 255) / 256);
+  stage_in_kernel<<<blocks, 256, 0, c->compute>>>(reinterpret_cast<const int4*>(st.hd), reinterpret_cast<int4*>(st.d),
+                                                  n16);
+  CK(cudaGetLastError());
+  c->launches += 1;
 }
 
 __global__ void hist_scatter_kernel(int32_t* hist, int stride, const int32_t* slot, const int32_t* pos,
@@ -911,8 +952,9 @@ int ms_hist_write(ms_ctx* c, int32_t slot, int32_t offset, const int32_t* host_t
       if (host_tokens[i] < 0 || host_tokens[i] >= c->desc.vocab) fail(MS_EVALIDATION, "token id out of vocab");
     Staging& st = next_staging(c, (size_t)n);
     std::memcpy(st.h, host_tokens, (size_t)n * 4);
-    CK(cudaMemcpyAsync(c->hist + (size_t)slot * c->hist_len + offset, st.h, (size_t)n * 4, cudaMemcpyHostToDevice,
-                       c->compute));
+    hist_in_kernel<<<(n + 255) / 256, 256, 0, c->compute>>>(st.hd, c->hist + (size_t)slot * c->hist_len + offset, n);
+    CK(cudaGetLastError());
+    c->launches += 1;
     CK(cudaEventRecord(st.used, c->compute));
     st.armed = true;
   });
@@ -956,7 +998,7 @@ int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float
     }
     CK(cudaSetDevice(c->device));
     CK(cudaEventRecord(c->ev_step0, c->compute));
-    CK(cudaMemcpyAsync(st.d, st.h, (size_t)n * (4 + mb) * 4, cudaMemcpyHostToDevice, c->compute));
+    stage_in(c, st, (size_t)n * (4 + mb));
     CK(cudaEventRecord(st.used, c->compute));
     st.armed = true;
     const int32_t* d_slot = st.d;
@@ -1006,7 +1048,7 @@ int ms_prefill(ms_ctx* c, int32_t slot, int32_t n_tokens, const int64_t* block_i
     for (int j = 0; j < nb; ++j) row[j] = page_of(c, block_ids[j]);
     CK(cudaSetDevice(c->device));
     CK(cudaEventRecord(c->ev_step0, c->compute));
-    CK(cudaMemcpyAsync(st.d, st.h, ((size_t)n * 4 + mb) * 4, cudaMemcpyHostToDevice, c->compute));
+    stage_in(c, st, (size_t)n * 4 + mb);
     CK(cudaEventRecord(st.used, c->compute));
     st.armed = true;
     const int TM = std::min(256, round16(n));
@@ -1114,15 +1156,20 @@ int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_pa
   return guard([&] {
     if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "gemm: bits must be 16 or 4");
     if (N % 128 || K % 128 || M < 1 || TM % 16 || TM < 16 || TM > 256) fail(MS_EVALIDATION, "gemm: bad shape");
-    static thread_local uint64_t* table = nullptr;
-    static thread_local uint64_t cached = 0;
-    if (!table) CK(cudaMalloc(&table, sizeof(uint64_t)));
+    // one-entry page table per contiguous packed matrix (up to 64 distinct
+    // matrices; written once, so later calls may be graph-captured)
+    static thread_local uint64_t* tables = nullptr;
+    static thread_local std::vector<uint64_t> known;
+    if (!tables) CK(cudaMalloc(&tables, 64 * sizeof(uint64_t)));
     const uint64_t addr = (uint64_t)w_packed;
-    if (addr != cached) {  // one-entry page table for a contiguous packed matrix
-      CK(cudaMemcpyAsync(table, &addr, sizeof(addr), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    size_t idx = std::find(known.begin(), known.end(), addr) - known.begin();
+    if (idx == known.size()) {
+      if (known.size() == 64) fail(MS_EVALIDATION, "gemm: more than 64 distinct weight matrices");
+      CK(cudaMemcpyAsync(tables + idx, &addr, sizeof(addr), cudaMemcpyHostToDevice, (cudaStream_t)stream));
       CK(cudaStreamSynchronize((cudaStream_t)stream));
-      cached = addr;
+      known.push_back(addr);
     }
+    uint64_t* table = tables + idx;
     ms::GemmWeights w{table, 0, (int64_t)1 << 40, N, K};
     const bool w4 = bits == 4;
     int dev = 0, sms = 148;

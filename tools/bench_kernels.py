@@ -27,19 +27,28 @@ def stream():
 
 
 def time_it(fn, iters=50, warm=5):
+    """Average device time per call; the calls are replayed from a CUDA graph
+    so that host launch cost (ctypes + plan) does not floor small kernels."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(iters):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(iters):
-        fn()
+    g.replay()
     b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) / iters
 
 
 def gemm(bits, Nn, K, M, TM, ctas=0):
+    """One GEMM shape; the weights rotate over enough copies (> 300 MB) that
+    every call streams them from HBM, not from the 126 MB L2."""
     L = N.lib()
     w = torch.randint(-2000, 2000, (Nn * K,), dtype=torch.int16, device="cuda")
     if bits == 16:
@@ -50,27 +59,44 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
         wp = torch.empty((Nn // 128) * (K // 128) * 8448, dtype=torch.uint8, device="cuda")
         N.check(L.ms_k_quant_w4(C.c_void_p(w.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), None, stream()))
         wbytes = Nn * K // 2 + Nn * K // 128 * 2
+    del w
+    copies = [wp] + [wp.clone() for _ in range(max(0, -(-300_000_000 // wp.numel() // wp.element_size()) - 1))]
     xp = torch.randint(-2000, 2000, (((M + TM - 1) // TM) * TM * K,), dtype=torch.int16, device="cuda")
     out = torch.zeros(160 * M * Nn, dtype=torch.float32, device="cuda")
     used = C.c_int()
+    i = [0]
 
     def run():
-        N.check(L.ms_k_gemm(bits, C.c_void_p(wp.data_ptr()), Nn, K, C.c_void_p(xp.data_ptr()), M, TM, ctas,
+        w_ = copies[i[0] % len(copies)]
+        i[0] += 1
+        N.check(L.ms_k_gemm(bits, C.c_void_p(w_.data_ptr()), Nn, K, C.c_void_p(xp.data_ptr()), M, TM, ctas,
                             C.c_void_p(out.data_ptr()), C.byref(used), stream()))
-    ms = time_it(run)
+    ms = time_it(run, iters=4 * len(copies) if len(copies) > 12 else 48, warm=len(copies) + 2)
     total = wbytes + M * K * 2 + M * Nn * 4
-    return {"bits": bits, "N": Nn, "K": K, "M": M, "us": ms * 1e3, "GBps": total / ms / 1e6, "slots": used.value}
+    if int(os.environ.get("MS_GEMM_DEBUG", "0")) & 8:
+        torch.cuda.synchronize()
+        tl = out[150 * M * Nn:150 * M * Nn + 2 * 8 * 64].view(torch.int64).view(8, 64).cpu().numpy()
+        t0 = tl[6, 0]
+        names = ["raw_issue", "grp_rfull", "grp_aempty", "grp_afull", "mma_go", "b_issue", "start/end", "epi_done"]
+        for e in range(8):
+            v = [(x - t0) / 1000 if x > 0 and x - t0 < 10**7 else None for x in tl[e]]
+            print(f"{names[e]:10s}", " ".join(f"{x:5.2f}" if x is not None else "  -  " for x in v[:24]))
+    return {"bits": bits, "N": Nn, "K": K, "M": M, "us": ms * 1e3, "GBps": total / ms / 1e6, "slots": used.value,
+            "copies": len(copies)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="gemm")
     ap.add_argument("--M", type=int, default=64)
+    ap.add_argument("--names", default=",".join(SHAPES))
+    ap.add_argument("--bits", default="16,4")
     args = ap.parse_args()
     res = []
     if "gemm" in args.which:
-        for name, (Nn, K) in SHAPES.items():
-            for bits in (16, 4):
+        for name in args.names.split(","):
+            Nn, K = SHAPES[name]
+            for bits in [int(b) for b in args.bits.split(",")]:
                 if name == "lm_head" and bits == 4:
                     continue
                 r = gemm(bits, Nn, K, args.M, min(256, (args.M + 15) // 16 * 16))
