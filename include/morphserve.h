@@ -146,6 +146,18 @@ int ms_kv_fill_synthetic(ms_ctx* ctx, const int64_t* block_ids, int64_t n, uint6
 int64_t ms_launch_count(ms_ctx* ctx);
 int ms_timer_start(ms_ctx* ctx);
 int ms_timer_stop(ms_ctx* ctx, float* ms);
+/* Per-kernel-category device time of the decode/prefill steps launched while
+ * enabled (an event after every launch on the compute stream; this serialises
+ * programmatic-dependent-launch overlap, so totals exceed the unprofiled step).
+ * ms_prof_kernels_read fills ms_out[MS_PK_COUNT] / launches_out[MS_PK_COUNT]
+ * and resets.  Instrumentation only, not a reference interface. */
+enum {
+  MS_PK_EMBED = 0, MS_PK_GEMM_QKV, MS_PK_GEMM_QKV_W4, MS_PK_QKV_POST, MS_PK_ATTN, MS_PK_GEMM_O, MS_PK_GEMM_O_W4,
+  MS_PK_NORM, MS_PK_GEMM_GU, MS_PK_GEMM_GU_W4, MS_PK_SILU, MS_PK_GEMM_DOWN, MS_PK_GEMM_DOWN_W4, MS_PK_LM_HEAD,
+  MS_PK_ARGMAX, MS_PK_COUNT
+};
+int ms_prof_kernels(ms_ctx* ctx, int enable);
+int ms_prof_kernels_read(ms_ctx* ctx, float* ms_out, int64_t* launches_out);
 int ms_prof_attention(ms_ctx* ctx, int enable);
 int ms_prof_attention_read(ms_ctx* ctx, float* total_ms, int64_t* launches);
 

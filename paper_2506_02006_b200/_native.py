@@ -83,6 +83,8 @@ SIGNATURES = [
     ("ms_timer_start", C.c_int, [_P]),
     ("ms_timer_stop", C.c_int, [_P, C.POINTER(C.c_float)]),
     ("ms_prof_attention", C.c_int, [_P, C.c_int]),
+    ("ms_prof_kernels", C.c_int, [_P, C.c_int]),
+    ("ms_prof_kernels_read", C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_int64)]),
     ("ms_prof_attention_read", C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_int64)]),
     ("ms_k_gen_weight", C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_double, C.c_double, _P, _P]),
     ("ms_k_pack_bf16", C.c_int, [_P, C.c_int, C.c_int, _P, _P]),

@@ -61,25 +61,31 @@ __device__ __forceinline__ const uint8_t* chunk_ptr(const GemmWeights& w, int64_
 // one page-table load per page crossing (the producer thread must stay far
 // ahead of the MMAs, so no per-chunk 64-bit division or dependent load).
 struct ChunkCursor {
-  const uint64_t* pages;
+  const GemmWeights* w;
   int64_t cpp, page, in_page;
   const uint8_t* base;
   int chunk_bytes;
-  __device__ ChunkCursor(const GemmWeights& w, int cb) : pages(w.pages), cpp(w.chunks_per_page), page(-1),
-                                                        in_page(0), base(nullptr), chunk_bytes(cb) {}
+  __device__ ChunkCursor(const GemmWeights& w_, int cb)
+      : w(&w_), cpp(w_.chunks_per_page), page(-1), in_page(0), base(nullptr), chunk_bytes(cb) {}
+  __device__ const uint8_t* page_base(int64_t p) const {
+    const int64_t i = p - w->inl_p0;
+    return reinterpret_cast<const uint8_t*>(i >= 0 && i < w->n_inl ? w->inl[i] : w->pages[p]);
+  }
   __device__ void seek(int64_t c) {
     const int64_t p = c / cpp;
     in_page = c - p * cpp;
     if (p != page) {
       page = p;
-      base = reinterpret_cast<const uint8_t*>(pages[p]);
+      base = page_base(p);
     }
   }
   __device__ const uint8_t* get() {
-    if (in_page == cpp) {
-      in_page = 0;
-      ++page;
-      base = reinterpret_cast<const uint8_t*>(pages[page]);
+    if (in_page >= cpp) {  // crossed one or more page ends (advance() does not normalise)
+      do {
+        in_page -= cpp;
+        ++page;
+      } while (in_page >= cpp);
+      base = page_base(page);
     }
     return base + in_page * chunk_bytes;
   }
@@ -160,6 +166,29 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
     }
     fence_mbar_init();
   }
+  // Producer (thread 0, which initialised the barriers): weights do not
+  // depend on the previous kernel, so the first ring of weight chunks is
+  // issued before the TMEM allocation / CTA barrier and the grid dependency.
+  uint32_t npre = 0;
+  ChunkCursor cur(W, kW4 ? kW4ChunkBytes : kBf16ChunkBytes);
+  if (threadIdx.x == 0) {
+    SegIter pre(plan, cta);
+    int t, k0, k1;
+    const uint32_t cap = kW4 ? (uint32_t)rstages : (uint32_t)stages;
+    while (npre < cap && pre.next(t, k0, k1)) {
+      const int n_tile = t % plan.n_tiles;
+      cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
+      for (int k = k0; k < k1 && npre < cap; ++k, ++npre, cur.advance()) {
+        if (kW4) {
+          mbar_expect_tx(&rfull[npre], raw_bytes);
+          bulk_g2s(sRaw(npre), cur.get(), raw_bytes, &rfull[npre]);
+        } else {
+          mbar_expect_tx(&full[npre], a_bytes + ((dbg & 1) ? 0u : b_bytes));
+          bulk_g2s(sA(npre), cur.get(), a_bytes, &full[npre]);
+        }
+      }
+    }
+  }
   if (warp == 1) tmem_alloc_dyn(tmem_slot, 2 * tm_cols);
   tc_fence_before();
   __syncthreads();
@@ -171,28 +200,6 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ producer
-      // Weights do not depend on the previous kernel: prefetch the first ring
-      // of weight chunks before the grid dependency wait (PDL overlap).
-      uint32_t npre = 0;
-      ChunkCursor cur(W, kW4 ? kW4ChunkBytes : kBf16ChunkBytes);
-      {
-        SegIter pre(plan, cta);
-        int t, k0, k1;
-        const uint32_t cap = kW4 ? (uint32_t)rstages : (uint32_t)stages;
-        while (npre < cap && pre.next(t, k0, k1)) {
-          const int n_tile = t % plan.n_tiles;
-          cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
-          for (int k = k0; k < k1 && npre < cap; ++k, ++npre, cur.advance()) {
-            if (kW4) {
-              mbar_expect_tx(&rfull[npre], raw_bytes);
-              bulk_g2s(sRaw(npre), cur.get(), raw_bytes, &rfull[npre]);
-            } else {
-              mbar_expect_tx(&full[npre], a_bytes + ((dbg & 1) ? 0u : b_bytes));
-              bulk_g2s(sA(npre), cur.get(), a_bytes, &full[npre]);
-            }
-          }
-        }
-      }
       pdl_wait();
       SegIter seg(plan, cta);
       int t, k0, k1;
@@ -225,38 +232,45 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------------------------------------------------- UMMA issuer
-      const uint32_t idesc = umma_idesc_bf16(128, (uint32_t)TM);
-      SegIter seg(plan, cta);
-      int t, k0, k1;
-      uint32_t it = 0, u = 0;
-      while (seg.next(t, k0, k1)) {
-        const uint32_t acc = u & 1, use = u >> 1;
-        if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
+    // ------------------------------------------------------------ UMMA issuer
+    // whole warp, warp-uniform control; one elected lane issues
+    const uint32_t idesc = umma_idesc_bf16(128, (uint32_t)TM);
+    const uint64_t dA0 = umma_desc(smem_u32(sA(0)), 128u, 1024u);
+    const uint64_t dB0 = umma_desc(smem_u32(sB(0)), 128u, 1024u);
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t u = 0, s = 0, ph = 0;
+    while (seg.next(t, k0, k1)) {
+      const uint32_t acc = u & 1, use = u >> 1;
+      if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * tm_cols;
+      for (int k = k0; k < k1; ++k) {
+        mbar_wait(&full[s], ph);
+        if (kW4) mbar_wait(&afull[s], ph);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * tm_cols;
-        for (int k = k0; k < k1; ++k, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          mbar_wait(&full[s], ph);
-          if (kW4) mbar_wait(&afull[s], ph);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA(s)), b0 = smem_u32(sB(s));
+        const uint64_t da = desc_add(dA0, s * stage_bytes), db = desc_add(dB0, s * stage_bytes);
+        if (elect_one()) {
 #pragma unroll
           for (int sub = 0; sub < (kW4 ? 2 : 1); ++sub) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t da = umma_desc(a0 + sub * 16384u + kk * 256u, 128u, 1024u);
-              const uint64_t db = umma_desc(b0 + sub * b_bytes + kk * 256u, 128u, 1024u);
-              if (!(dbg & 2)) umma_bf16(d, da, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
+              if (!(dbg & 2))
+                umma_bf16(d, desc_add(da, sub * 16384u + kk * 256u), desc_add(db, sub * b_bytes + kk * 256u), idesc,
+                          (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
             }
           }
           umma_commit(&empty[s]);
         }
-        umma_commit(&tfull[acc]);
-        ++u;
+        __syncwarp();
+        if (++s == (uint32_t)stages) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      ++u;
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------- epilogue
@@ -442,6 +456,22 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     fence_mbar_init();
   }
   stamp(6, threadIdx.x == 0 ? 0 : 64);
+  // Producer (thread 0, which initialised the barriers): the first ring of raw
+  // int4 chunks is issued before the TMEM allocation and the CTA barrier.
+  uint32_t npre = 0;
+  ChunkCursor cur(W, kW4ChunkBytes);
+  if (threadIdx.x == 0) {
+    SegIter pre(plan, cta);
+    int t, k0, k1;
+    while (npre < (uint32_t)rstages && pre.next(t, k0, k1)) {
+      cur.seek(W.first_chunk + (int64_t)(t % plan.n_tiles) * nk + k0);
+      for (int k = k0; k < k1 && npre < (uint32_t)rstages; ++k, ++npre, cur.advance()) {
+        mbar_expect_tx(&rfull[npre], kW4ChunkBytes);
+        bulk_g2s(sRaw(npre), cur.get(), kW4ChunkBytes, &rfull[npre]);
+        stamp(0, npre);
+      }
+    }
+  }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -455,16 +485,20 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
       // ------------------------------------------------------------ producer
       // raw int4 chunks (independent of the activation ring, so the weight
       // stream runs `rstages` ahead; weights need no grid dependency)
-      ChunkCursor cur(W, kW4ChunkBytes);
       SegIter seg(plan, cta);
       int t, k0, k1;
       uint32_t it = 0;
       while (seg.next(t, k0, k1)) {
+        if (it + (uint32_t)(k1 - k0) <= npre) {  // whole segment already issued
+          it += (uint32_t)(k1 - k0);
+          continue;
+        }
         const int n_tile = t % plan.n_tiles;
         cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
         for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
+          if (it < npre) continue;
           const int r = it % rstages;
-          if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
+          mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
           mbar_expect_tx(&rfull[r], kW4ChunkBytes);
           bulk_g2s(sRaw(r), cur.get(), kW4ChunkBytes, &rfull[r]);
           stamp(0, it);
@@ -472,40 +506,53 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------------------------------------------------- UMMA issuer
-      const uint32_t idesc = umma_idesc_bf16(128, (uint32_t)TM);
-      SegIter seg(plan, cta);
-      int t, k0, k1;
-      uint32_t it = 0, u = 0;
-      while (seg.next(t, k0, k1)) {
-        const uint32_t acc = acc_bufs == 2 ? (u & 1) : 0u;
-        const uint32_t use = acc_bufs == 2 ? (u >> 1) : u;
-        if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
+    // ------------------------------------------------------------ UMMA issuer
+    // whole warp, warp-uniform control; one elected lane issues
+    const uint32_t idesc = umma_idesc_bf16(128, (uint32_t)TM);
+    const uint64_t dB0 = umma_desc(smem_u32(sB(0)), 128u, 1024u);
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t it = 0, u = 0, s = 0, sph = 0, a = 0, aph = 0;
+    while (seg.next(t, k0, k1)) {
+      const uint32_t acc = acc_bufs == 2 ? (u & 1) : 0u;
+      const uint32_t use = acc_bufs == 2 ? (u >> 1) : u;
+      if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * tm_cols;
+      for (int k = k0; k < k1; ++k, ++it) {
+        mbar_wait(&bfull[s], sph);
+        mbar_wait(&afull[a], aph);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * tm_cols;
-        for (int k = k0; k < k1; ++k, ++it) {
-          const int s = it % bstages, a = it % astages;
-          mbar_wait(&bfull[s], (it / bstages) & 1);
-          mbar_wait(&afull[a], (it / astages) & 1);
-          stamp(4, it);
-          tc_fence_after();
-          const uint32_t b0 = smem_u32(sB(s));
-          const uint32_t ta = tmem_base + a_col0 + (uint32_t)a * 64u;
+        stamp(4, it);
+        const uint64_t db = desc_add(dB0, s * 2u * b_bytes);
+        const uint32_t ta = tmem_base + a_col0 + a * 64u;
+        if (elect_one()) {
 #pragma unroll
           for (int sub = 0; sub < 2; ++sub) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t db = umma_desc(b0 + sub * b_bytes + kk * 256u, 128u, 1024u);
-              if (!(dbg & 2)) umma_bf16_ts(d, ta + sub * 32u + kk * 8u, db, idesc, (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
+              if (!(dbg & 2))
+                umma_bf16_ts(d, ta + sub * 32u + kk * 8u, desc_add(db, sub * b_bytes + kk * 256u), idesc,
+                             (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
             }
           }
           umma_commit(&bempty[s]);
           umma_commit(&aempty[a]);
         }
-        umma_commit(&tfull[acc]);
-        ++u;
+        __syncwarp();
+        stamp(7, it);
+        if (++s == (uint32_t)bstages) {
+          s = 0;
+          sph ^= 1;
+        }
+        if (++a == (uint32_t)astages) {
+          a = 0;
+          aph ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      ++u;
     }
   } else if (warp == 6) {
     if (lane == 0) {
@@ -561,7 +608,6 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (lane == 0 && quad == 0) stamp(7, u);
       ++u;
     }
   } else {
@@ -686,6 +732,17 @@ static int pick_stages(bool w4, int TM, int* rstages, size_t* smem_out) {
   *rstages = rs;
   *smem_out = st * stage + (size_t)rs * 8576 + (3 * st + 4 + 2 * rs) * 8 + 64;
   return st;
+}
+
+void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages) {
+  const int64_t chunks = (int64_t)(w.N / 128) * (w.K / (w4 ? 128 : 64));
+  const int64_t p0 = w.first_chunk / w.chunks_per_page;
+  const int64_t p1 = (w.first_chunk + chunks - 1) / w.chunks_per_page;
+  w.n_inl = 0;
+  if (p1 - p0 + 1 > kGemmInlinePages) return;
+  w.inl_p0 = (int)p0;
+  for (int64_t p = p0; p <= p1; ++p) w.inl[p - p0] = host_pages[p];
+  w.n_inl = (int)(p1 - p0 + 1);
 }
 
 GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t part_elems) {

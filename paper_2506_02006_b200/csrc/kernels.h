@@ -37,12 +37,22 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 // A weight matrix as the GEMM sees it: chunk c of the matrix lives in page
 // (first_chunk + c) / chunks_per_page of its variant image.
+// The pages a matrix spans are also passed inline in the kernel parameters
+// (up to kGemmInlinePages), so the producer's first bulk copy does not wait
+// for a dependent global load of the page table.
+constexpr int kGemmInlinePages = 48;
 struct GemmWeights {
   const uint64_t* pages;  // device array of page base addresses
   int64_t first_chunk;
   int64_t chunks_per_page;
   int N, K;
+  int n_inl = 0;          // pages [inl_p0, inl_p0 + n_inl) are inlined below
+  int inl_p0 = 0;
+  uint64_t inl[kGemmInlinePages] = {};
 };
+// Fill the inline page table from a host copy of `pages` (host_pages[p] ==
+// pages[p]); leaves n_inl = 0 when the matrix spans too many pages.
+void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages);
 
 // Stream-K partition of one GEMM: T = tiles * nk k-steps split into C
 // contiguous ranges (one persistent CTA each).  CTA c covers global k-steps
@@ -98,7 +108,15 @@ struct AttnArgs {
   uint16_t* out;            // bf16 output
   int out_packed;           // 1: packed activation image (K = H*hd, TM), 0: row-major [rows][H*hd]
   int TM;
+  int stages;               // K/V ring depth (set by attn_decode_launch)
+  // persistent stream-K path (used when pws != nullptr and splits <= 1):
+  float* pws;               // [ctas][2][G][HD + 2] partial (acc, m, l) of items split between CTAs
+  int* pcnt;                // [rows * KVH] arrival counters, zero between launches (self-resetting)
+  int ctas;                 // persistent grid size (set by attn_decode_launch)
 };
+// Persistent-grid size and workspace floats the stream-K decode attention needs.
+int attn_persist_ctas(int num_sms);
+size_t attn_persist_ws_floats(int num_sms, int G, int HD);
 cudaError_t attn_decode_launch(const AttnArgs& a, cudaStream_t stream);
 
 // Causal prefill attention of ONE sequence (positions 0..n-1) over its paged KV.

@@ -109,6 +109,21 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo, 
   d |= (uint64_t)1 << 46;
   return d;
 }
+// One lane of a converged warp (tcgen05.mma / commit are single-thread
+// instructions; issuing them from a warp-uniform loop keeps descriptors in
+// uniform registers: measured 33 cyc/MMA at M128 N64 vs 90-300 from a lone
+// divergent thread, tools/mma_rate.cu).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+// Advance a shared-memory descriptor by `bytes` (start address field, no carry).
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
 // Instruction descriptor, kind::f16: D=F32, A=B=BF16, both K-major.
 __device__ __forceinline__ uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);

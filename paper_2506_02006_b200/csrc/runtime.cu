@@ -180,6 +180,8 @@ struct ms_ctx {
   float* q = nullptr;
   float* attn_ws = nullptr;
   size_t attn_ws_elems = 0;
+  float* attn_pws = nullptr;   // persistent attention partials
+  int* attn_pcnt = nullptr;    // persistent attention item counters [max_batch * KVH]
   int32_t* next = nullptr;
   float* logits = nullptr;
   int max_blocks = 0;
@@ -197,6 +199,11 @@ struct ms_ctx {
   bool prof_attn = false;
   std::vector<cudaEvent_t> prof_ev;  // pairs
   size_t prof_used = 0;
+  // per-kernel-category step profile (ms_prof_kernels): an event after every launch
+  bool prof_all = false;
+  std::vector<cudaEvent_t> pk_ev;
+  std::vector<int> pk_cat;
+  size_t pk_used = 0;
   cudaEvent_t tm0 = nullptr, tm1 = nullptr;
 };
 
@@ -325,7 +332,9 @@ void make_resident_bf16(ms_ctx* c) {
 ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
   Layer& L = c->layers[l];
   const ImageGeom& g = geom_of(c, L.bits);
-  return ms::GemmWeights{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
+  ms::GemmWeights w{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
+  ms::gemm_inline_pages(w, L.bits == 4, L.h_table[L.slot]);
+  return w;
 }
 
 ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
@@ -336,6 +345,19 @@ ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM
   return plan;
 }
 
+// categories of ms_prof_kernels_read (include/morphserve.h MS_PK_*)
+void pk_mark(ms_ctx* c, int cat) {
+  if (!c->prof_all) return;
+  if (c->pk_used == c->pk_ev.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->pk_ev.push_back(e);
+    c->pk_cat.push_back(0);
+  }
+  c->pk_cat[c->pk_used] = cat;
+  CK(cudaEventRecord(c->pk_ev[c->pk_used++], c->compute));
+}
+
 void prof_mark(ms_ctx* c) {
   if (!c->prof_attn) return;
   if (c->prof_used == c->prof_ev.size()) {
@@ -344,6 +366,16 @@ void prof_mark(ms_ctx* c) {
     c->prof_ev.push_back(e);
   }
   CK(cudaEventRecord(c->prof_ev[c->prof_used++], c->compute));
+}
+
+// MS_ATTN_PERSIST=1 (experiments): persistent stream-K decode attention
+// instead of one CTA per (kv_head, row, split).
+bool attn_persistent() {
+  static const bool v = [] {
+    const char* e = std::getenv("MS_ATTN_PERSIST");
+    return e && e[0] == '1';
+  }();
+  return v;
 }
 
 int attn_splits(ms_ctx* c, int rows, int max_ctx) {
@@ -372,18 +404,22 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
              int max_ctx, int final_row_begin, bool want_logits) {
   const ms_model_desc& D = c->desc;
   const int d = D.hidden, H = D.num_heads, KVH = D.num_kv_heads, hd = D.head_dim;
+  pk_mark(c, -1);
   CK(ms::embed_norm_launch(c->embed, d_tokens, c->hist, d_slot, d_pos, c->hist_len, M, d, c->norms, D.rms_eps,
                            c->h, c->x, TM, c->compute));
   c->launches += 1;
+  pk_mark(c, MS_PK_EMBED);
   const int asplits = attn_splits(c, M, max_ctx);
   for (int l = 0; l < D.num_layers; ++l) {
     const bool w4 = c->layers[l].bits == 4;
     const int skip = skip_mask();
     ms::GemmPlanDev s = (skip & 16) ? ms::gemm_plan(1024, 1024, M, TM, false, c->num_sms, c->part_elems)
                                     : gemm(c, mat_weights(c, l, 0), w4, M, TM);
+    pk_mark(c, w4 ? MS_PK_GEMM_QKV_W4 : MS_PK_GEMM_QKV);
     if (!(skip & 1)) CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
                            d_page_row, page_stride, c->q, c->compute));
     c->launches += 1;
+    pk_mark(c, MS_PK_QKV_POST);
     prof_mark(c);
     if (d_page_row != nullptr) {
       // prefill: one sequence, tiled causal attention (page table row 0)
@@ -416,21 +452,32 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       a.splits = asplits;
       a.part_o = c->attn_ws;
       a.part_ml = c->attn_ws + (size_t)asplits * M * H * hd;
+      if (attn_persistent()) {  // stream-K attention balances any context mix by itself
+        a.splits = 1;
+        a.pws = c->attn_pws;
+        a.pcnt = c->attn_pcnt;
+      }
       a.out = c->x;
       a.out_packed = 1;
       a.TM = TM;
       if (!(skip & 8)) CK(ms::attn_decode_launch(a, c->compute));
       c->launches += asplits > 1 ? 2 : 1;
     }
+    pk_mark(c, MS_PK_ATTN);
     prof_mark(c);
     if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
+    pk_mark(c, w4 ? MS_PK_GEMM_O_W4 : MS_PK_GEMM_O);
     if (!(skip & 2)) CK(ms::residual_norm_launch(c->part, s, M, d, c->h, c->norms + ((size_t)l * 2 + 1) * d, D.rms_eps, c->x, TM,
                                 c->compute));
     c->launches += 1;
+    pk_mark(c, MS_PK_NORM);
     if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
+    pk_mark(c, w4 ? MS_PK_GEMM_GU_W4 : MS_PK_GEMM_GU);
     if (!(skip & 4)) CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
     c->launches += 1;
+    pk_mark(c, MS_PK_SILU);
     if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
+    pk_mark(c, w4 ? MS_PK_GEMM_DOWN_W4 : MS_PK_GEMM_DOWN);
     const bool last = l == D.num_layers - 1;
     const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
     const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
@@ -438,14 +485,19 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out,
                                        last ? final_row_begin : 0, c->compute));
     c->launches += 1;
+    pk_mark(c, MS_PK_NORM);
   }
   const int Mo = M - final_row_begin;
   const int TMo = round16(Mo) > 256 ? 256 : round16(Mo);
   ms::GemmWeights lw{c->lm_table, 0, (int64_t)1 << 40, D.vocab, d};
+  const uint64_t lm_addr = (uint64_t)c->lm_packed;
+  ms::gemm_inline_pages(lw, false, &lm_addr);
   const ms::GemmPlanDev s = gemm(c, lw, false, Mo, TMo);
+  pk_mark(c, MS_PK_LM_HEAD);
   CK(ms::argmax_launch(c->part, s, Mo, D.vocab, want_logits ? c->logits : nullptr, c->next, c->hist,
                        d_slot + final_row_begin, d_pos + final_row_begin, c->hist_len, c->compute));
   c->launches += 1;
+  pk_mark(c, MS_PK_ARGMAX);
 }
 
 Staging& next_staging(ms_ctx* c, size_t words) {
@@ -573,6 +625,11 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       CK(cudaMalloc(&c->q, (size_t)c->max_rows * H * hd * sizeof(float)));
       c->attn_ws_elems = (size_t)16 * desc->max_batch * H * (hd + 2);
       CK(cudaMalloc(&c->attn_ws, c->attn_ws_elems * sizeof(float)));
+      CK(cudaMalloc(&c->attn_pws, ms::attn_persist_ws_floats(c->num_sms, H / desc->num_kv_heads, hd) * sizeof(float)));
+      CK(cudaMalloc(&c->attn_pcnt, (size_t)std::max(desc->max_batch, desc->max_prefill_tokens) * desc->num_kv_heads *
+                                       sizeof(int)));
+      CK(cudaMemset(c->attn_pcnt, 0, (size_t)std::max(desc->max_batch, desc->max_prefill_tokens) *
+                                         desc->num_kv_heads * sizeof(int)));
       CK(cudaMalloc(&c->next, (size_t)c->max_rows * sizeof(int32_t)));
       CK(cudaMalloc(&c->logits, (size_t)desc->max_batch * desc->vocab * sizeof(float)));
       CK(cudaHostAlloc(&c->h_next, (size_t)c->max_rows * sizeof(int32_t), cudaHostAllocDefault));
@@ -638,7 +695,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
-                 c->h, c->x, c->part, c->q, c->attn_ws, c->next, c->logits, c->hist};
+                 c->h, c->x, c->part, c->q, c->attn_ws, c->attn_pws, c->attn_pcnt, c->next, c->logits, c->hist};
   for (void* p : dev) cudaFree(p);
   cudaFreeHost(c->h_next);
   cudaFreeHost(c->h_logits);
@@ -1107,6 +1164,32 @@ int ms_timer_stop(ms_ctx* c, float* ms_out) {
   });
 }
 
+int ms_prof_kernels(ms_ctx* c, int enable) {
+  return guard([&] {
+    c->prof_all = enable != 0;
+    c->pk_used = 0;
+  });
+}
+
+int ms_prof_kernels_read(ms_ctx* c, float* ms_out, int64_t* launches_out) {
+  return guard([&] {
+    CK(cudaStreamSynchronize(c->compute));
+    for (int k = 0; k < MS_PK_COUNT; ++k) {
+      ms_out[k] = 0.f;
+      launches_out[k] = 0;
+    }
+    for (size_t i = 1; i < c->pk_used; ++i) {
+      const int cat = c->pk_cat[i];
+      if (cat < 0 || c->pk_cat[i - 1] == MS_PK_ARGMAX) continue;  // step start: gap between steps not counted
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->pk_ev[i - 1], c->pk_ev[i]));
+      ms_out[cat] += ms;
+      launches_out[cat] += 1;
+    }
+    c->pk_used = 0;
+  });
+}
+
 int ms_prof_attention(ms_ctx* c, int enable) {
   return guard([&] {
     c->prof_attn = enable != 0;
@@ -1172,6 +1255,7 @@ int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_pa
     uint64_t* table = tables + idx;
     ms::GemmWeights w{table, 0, (int64_t)1 << 40, N, K};
     const bool w4 = bits == 4;
+    ms::gemm_inline_pages(w, w4, &addr);
     int dev = 0, sms = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1208,6 +1292,21 @@ int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int 
     a.out_packed = 0;
     a.TM = 16;
     if (a.splits > 1 && !workspace) fail(MS_EVALIDATION, "attn: split-KV needs a workspace");
+    if (splits == 0) {  // persistent stream-K kernel (the decode-step path)
+      static thread_local float* pws = nullptr;
+      static thread_local int* pcnt = nullptr;
+      int dev = 0, sms = 148;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      if (!pws) {
+        CK(cudaMalloc(&pws, ms::attn_persist_ws_floats(sms, 8, 128) * sizeof(float)));
+        CK(cudaMalloc(&pcnt, (size_t)(1 << 16) * sizeof(int)));
+        CK(cudaMemset(pcnt, 0, (size_t)(1 << 16) * sizeof(int)));
+      }
+      if ((size_t)rows * KVH > (1 << 16)) fail(MS_EVALIDATION, "attn: too many rows x kv heads");
+      a.pws = pws;
+      a.pcnt = pcnt;
+    }
     CK(ms::attn_decode_launch(a, (cudaStream_t)stream));
   });
 }

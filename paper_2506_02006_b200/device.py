@@ -194,6 +194,20 @@ class DeviceModel:
         N.check(self.lib.ms_timer_stop(self.h, C.byref(ms)))
         return ms.value
 
+    PK_NAMES = ["embed", "gemm_qkv", "gemm_qkv_w4", "qkv_post", "attn", "gemm_o", "gemm_o_w4", "norm", "gemm_gu",
+                "gemm_gu_w4", "silu", "gemm_down", "gemm_down_w4", "lm_head", "argmax"]
+
+    def prof_kernels(self, enable: bool):
+        N.check(self.lib.ms_prof_kernels(self.h, int(enable)))
+
+    def prof_kernels_read(self) -> dict:
+        """{category: (total ms, launches)} since prof_kernels(True)."""
+        k = len(self.PK_NAMES)
+        ms = (C.c_float * k)()
+        n = (C.c_int64 * k)()
+        N.check(self.lib.ms_prof_kernels_read(self.h, ms, n))
+        return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(self.PK_NAMES) if n[i]}
+
     def prof_attention(self, enable: bool):
         N.check(self.lib.ms_prof_attention(self.h, int(enable)))
 

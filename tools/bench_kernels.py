@@ -77,7 +77,7 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
         torch.cuda.synchronize()
         tl = out[150 * M * Nn:150 * M * Nn + 2 * 8 * 64].view(torch.int64).view(8, 64).cpu().numpy()
         t0 = tl[6, 0]
-        names = ["raw_issue", "grp_rfull", "grp_aempty", "grp_afull", "mma_go", "b_issue", "start/end", "epi_done"]
+        names = ["raw_issue", "grp_rfull", "grp_aempty", "grp_afull", "mma_go", "b_issue", "start/end", "mma_issued"]
         for e in range(8):
             v = [(x - t0) / 1000 if x > 0 and x - t0 < 10**7 else None for x in tl[e]]
             print(f"{names[e]:10s}", " ".join(f"{x:5.2f}" if x is not None else "  -  " for x in v[:24]))

@@ -43,7 +43,14 @@ def child(steps, w4):
         dev.decode(slots, pos, table, want_next=False)
         pos = pos + 1
     ms = dev.timer_stop() / steps
-    print(json.dumps({"ms_per_step": ms}))
+    prof = {}
+    if os.environ.get("PROF"):
+        dev.prof_kernels(True)
+        for _ in range(steps):
+            dev.decode(slots, pos, table, want_next=False)
+            pos = pos + 1
+        prof = {k: (round(v[0] / steps * 1e3, 1), v[1] // steps) for k, v in dev.prof_kernels_read().items()}
+    print(json.dumps({"ms_per_step": ms, "us_per_step_by_kernel": prof}))
     dev.close()
 
 
@@ -63,7 +70,7 @@ def main():
         out = subprocess.run([sys.executable, __file__, "--child", "--steps", str(a.steps), "--w4", str(a.w4)],
                              env=env, capture_output=True, text=True)
         line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
-        res[name] = json.loads(line[-1])["ms_per_step"] if line else out.stderr[-400:]
+        res[name] = json.loads(line[-1]) if line else out.stderr[-400:]
         print(name, res[name], flush=True)
     print(json.dumps({"w4_layers": a.w4, "ms_per_step": res}))
 
