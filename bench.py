@@ -229,7 +229,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- all-BF16 step
+    # ---- all-BF16 step (both arms start at the same context length, so the
+    # BF16 / mixed comparison sees identical KV bytes per step)
+    pos = np.full(BATCH, CTX - 1, dtype=np.int32)
     for _ in range(args.warmup):
         dev.decode(slots, pos, table, want_next=False)
         pos = pos + 1
@@ -241,6 +243,7 @@ def run_ours(args):
     for t in tickets:
         swap_ms.append(dev.swap_wait(t))
         dev.swap_commit(t)
+    pos = np.full(BATCH, CTX - 1, dtype=np.int32)
     for _ in range(args.warmup):
         dev.decode(slots, pos, table, want_next=False)
         pos = pos + 1

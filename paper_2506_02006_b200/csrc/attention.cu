@@ -34,6 +34,65 @@ static int attn_env(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
+// Sum of the first n split-K partial slots of one element (slot order fixed,
+// as elementwise.cu sum_slots: bit-identical to the unfused qkv_post path).
+__device__ __forceinline__ float attn_sum_slots(const float* p, size_t stride, int n) {
+  float v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = s < n ? __ldcg(p + s * stride) : 0.f;
+  float acc = 0.f;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (s < n) acc += v[s];
+  for (int s = 8; s < n; ++s) acc += __ldcg(p + s * stride);
+  return acc;
+}
+
+// Fused QKV post-processing for one (kv_head, row) CTA: q of the G heads of the
+// group (RoPE'd, fp32) into `qs`, and -- by the CTA that streams the row's last
+// block -- the rotated K and the V of the new token into the paged cache.  The
+// arithmetic is qkv_post_kernel's (elementwise.cu), element for element.
+template <int HD, int G>
+__device__ __forceinline__ void attn_qkv_fused(const AttnArgs& a, int kvh, int row, bool append, float* qs) {
+  constexpr int half = HD / 2;
+  const int H = a.H, KVH = a.KVH;
+  const int N = (H + 2 * KVH) * HD;
+  const int p = a.pos[row];
+  const size_t stride = (size_t)a.rows * N;
+  const int nheads = G + (append ? 2 : 0);
+  for (int idx = threadIdx.x; idx < nheads * half; idx += blockDim.x) {
+    const int hh = idx / half, i = idx - hh * half;
+    const int hs = hh < G ? kvh * G + hh : (hh == G ? H + kvh : H + KVH + kvh);  // q, k, v head slot
+    const int c0 = hs * HD + i;
+    const float* src = a.qkv_part + (size_t)row * N + c0;
+    float x0 = attn_sum_slots(src, stride, part_slots(a.qkv_plan, row, c0));
+    float x1 = attn_sum_slots(src + half, stride, part_slots(a.qkv_plan, row, c0 + half));
+    if (hs < H + KVH) {
+      const float c = a.rope_cos[(size_t)p * half + i], sn = a.rope_sin[(size_t)p * half + i];
+      const float y0 = x0 * c - x1 * sn;
+      const float y1 = x1 * c + x0 * sn;
+      x0 = y0;
+      x1 = y1;
+    }
+    if (hh < G) {
+      qs[hh * HD + i] = x0;
+      qs[hh * HD + i + half] = x1;
+    } else {
+      const int prow = a.page_row ? a.page_row[row] : row;
+      const int32_t page = a.pages[(size_t)prow * a.page_stride + p / a.kv.block_tokens];
+      const bool is_v = hh == G + 1;
+      uint16_t* dst = reinterpret_cast<uint16_t*>(a.kv.arena + (int64_t)page * a.kv.page_bytes + a.kv.layer_off(a.layer) +
+                                                  (int64_t)kvh * 2 * a.kv.head_bytes() +
+                                                  (is_v ? a.kv.head_bytes() : 0)) +
+                      (p % a.kv.block_tokens) * HD;
+      dst[i] = f2bf(x0);
+      dst[i + half] = f2bf(x1);
+    }
+  }
+  // the new K/V token is read back through the async (bulk copy) proxy
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <int HD, int G, int BT>
 __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
   constexpr int VEC = HD / 32;
@@ -66,7 +125,12 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
     }
     fence_mbar_init();
   }
+  // q source: fused QKV post-processing into shared memory, or the q buffer
+  float* qsm = scratch + (size_t)4 * G * HD + 8 * G;  // [G][HD] fp32
+  const bool fused = a.qkv_part != nullptr;
+  if (fused) attn_qkv_fused<HD, G>(a, kvh, row, b1 == nb, qsm);
   __syncthreads();
+  const float* qsrc = fused ? qsm : a.q + ((size_t)row * a.H + kvh * G) * HD;
 
   float m[G], l[G], acc[G][VEC];
   if (warp == 4) {
@@ -90,7 +154,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
     const int rot = (2 * t + h) & 15;
     float qr[8][8];
     {
-      const float* qp = a.q + ((size_t)row * a.H + kvh) * HD;
+      const float* qp = qsrc;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int c = (2 * i + rot) & 15;
@@ -177,7 +241,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
     float qv[G][VEC];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float* qp = a.q + ((size_t)row * a.H + kvh * G + g) * HD + lane * VEC;
+      const float* qp = qsrc + (size_t)g * HD + lane * VEC;
 #pragma unroll
       for (int i = 0; i < VEC; ++i) qv[g][i] = qp[i] * a.scale_log2;
       m[g] = -INFINITY;
@@ -691,7 +755,7 @@ static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
   static const int ctas_per_sm = attn_env("MS_ATTN_CTAS", 0);
   AttnArgs a = a_in;
   a.stages = stages;
-  size_t smem = (size_t)stages * BT * HD * 4 + 2 * stages * 8 + (size_t)4 * G * (HD + 2) * 4;
+  size_t smem = (size_t)stages * BT * HD * 4 + 2 * stages * 8 + (size_t)4 * G * (HD + 2) * 4 + (size_t)G * HD * 4;
   if (ctas_per_sm > 0) smem = std::max(smem, (size_t)(220 * 1024) / ctas_per_sm);  // cap residency
   static bool attr = false;
   if (!attr) {

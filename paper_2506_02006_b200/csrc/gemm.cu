@@ -693,12 +693,19 @@ static int w4_groups() {
   return v;
 }
 
+static int w4_env(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 static int pick_w4_stages(int TM, int* rstages, int* astages, size_t* smem_out) {
   const size_t budget = 215 * 1024;
   const size_t bst = (size_t)TM * 128 * 2;
+  static const int bs_env = w4_env("MS_W4_BSTAGES", 0), rs_env = w4_env("MS_W4_RSTAGES", 16);
   int bs = TM <= 64 ? 6 : (TM <= 128 ? 4 : 2);
+  if (bs_env > 0 && (size_t)bs_env * bst <= budget / 2) bs = bs_env;
   int rs = (int)((budget - bs * bst) / 8576);
-  if (rs > 16) rs = 16;
+  if (rs > rs_env) rs = rs_env;
   if (rs < 2) rs = 2;
   *rstages = rs;
   const int tm_cols = TM <= 32 ? 32 : TM <= 64 ? 64 : TM <= 128 ? 128 : 256;

@@ -93,7 +93,16 @@ struct KvGeom {
 };
 
 struct AttnArgs {
-  const float* q;           // [rows][H][hd] fp32, RoPE applied
+  const float* q;           // [rows][H][hd] fp32, RoPE applied (unused when qkv_part is set)
+  // fused QKV post-processing (decode): when qkv_part != nullptr every CTA sums
+  // the QKV GEMM's split-K partial slots for its q heads (+ RoPE) itself, and
+  // the CTA holding the row's last block also rotates/appends the new K and V
+  // token into the paged cache before streaming it (replaces qkv_post_kernel).
+  const float* qkv_part;    // [slots][rows][(H + 2 KVH) hd]
+  GemmPlanDev qkv_plan;
+  const float* rope_cos;    // [max_pos][hd/2]
+  const float* rope_sin;
+  const int32_t* pos;       // [rows] position of the new token
   KvGeom kv;
   int layer;
   const int32_t* pages;     // page index table, row r uses pages + page_row[r] * page_stride

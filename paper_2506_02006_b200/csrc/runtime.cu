@@ -416,10 +416,15 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     ms::GemmPlanDev s = (skip & 16) ? ms::gemm_plan(1024, 1024, M, TM, false, c->num_sms, c->part_elems)
                                     : gemm(c, mat_weights(c, l, 0), w4, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_QKV_W4 : MS_PK_GEMM_QKV);
-    if (!(skip & 1)) CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
-                           d_page_row, page_stride, c->q, c->compute));
-    c->launches += 1;
-    pk_mark(c, MS_PK_QKV_POST);
+    // decode: the attention kernel does the QKV post-processing itself
+    const bool fuse_qkv = d_page_row == nullptr && !attn_persistent();
+    if (!fuse_qkv) {
+      if (!(skip & 1))
+        CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
+                               d_page_row, page_stride, c->q, c->compute));
+      c->launches += 1;
+      pk_mark(c, MS_PK_QKV_POST);
+    }
     prof_mark(c);
     if (d_page_row != nullptr) {
       // prefill: one sequence, tiled causal attention (page table row 0)
@@ -452,6 +457,13 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       a.splits = asplits;
       a.part_o = c->attn_ws;
       a.part_ml = c->attn_ws + (size_t)asplits * M * H * hd;
+      if (fuse_qkv) {
+        a.qkv_part = c->part;
+        a.qkv_plan = s;
+        a.rope_cos = c->rope_cos;
+        a.rope_sin = c->rope_sin;
+        a.pos = d_pos;
+      }
       if (attn_persistent()) {  // stream-K attention balances any context mix by itself
         a.splits = 1;
         a.pws = c->attn_pws;

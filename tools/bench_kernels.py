@@ -14,6 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2506_02006_b200 import _native as N  # noqa: E402
@@ -81,6 +82,13 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
         for e in range(8):
             v = [(x - t0) / 1000 if x > 0 and x - t0 < 10**7 else None for x in tl[e]]
             print(f"{names[e]:10s}", " ".join(f"{x:5.2f}" if x is not None else "  -  " for x in v[:24]))
+        iss, rf = tl[0].astype(float), tl[1].astype(float)
+        n = int(np.sum(rf > 0))
+        lat = [(rf[i] - iss[i]) / 1000 for i in range(n) if iss[i] > 0]
+        gaps = [(rf[i + 1] - rf[i]) / 1000 for i in range(n - 1)]
+        print("chunks", n, "issue->full latency us: first", [round(x, 2) for x in lat[:4]], "mean(after 16)",
+              round(float(np.mean(lat[16:])), 2) if len(lat) > 16 else None,
+              "full->full gap mean(after 16)", round(float(np.mean(gaps[16:])), 3) if len(gaps) > 16 else None)
     return {"bits": bits, "N": Nn, "K": K, "M": M, "us": ms * 1e3, "GBps": total / ms / 1e6, "slots": used.value,
             "copies": len(copies)}
 

@@ -18,7 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-MASKS = {"full": 0, "no_rows": 7, "no_attn": 8, "no_gemm": 16, "no_attn_rows": 15, "gemm_only": 15,
+MASKS = {"full": 0, "no_rows": 7, "no_qkvpost": 1, "no_norm": 2, "no_silu": 4, "no_attn": 8, "no_gemm": 16, "no_attn_rows": 15, "gemm_only": 15,
          "rows_only": 24, "nothing": 31}
 
 
