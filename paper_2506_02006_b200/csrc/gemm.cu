@@ -118,15 +118,225 @@ struct SegIter {
   }
 };
 
+// ------------------------------------------------------------- tail gang
+__device__ __forceinline__ float tail_sum_slots(const float* p, size_t stride, int n) {
+  float v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = s < n ? __ldcg(p + s * stride) : 0.f;
+  float acc = 0.f;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (s < n) acc += v[s];
+  for (int s = 8; s < n; ++s) acc += __ldcg(p + s * stride);
+  return acc;
+}
+
+// Runs after the CTA's MMA/epilogue work (all threads, after a CTA barrier).
+// `scratch` = the kernel's (now idle) dynamic shared memory: static shared
+// arrays would push the GEMMs over the 227 KB per-CTA limit.
+__device__ void gemm_tail_gang(const GemmEpi& e, const GemmPlanDev& plan, int M, int N, const float* __restrict__ part,
+                               uint8_t* scratch) {
+  uint32_t& s_rank = *reinterpret_cast<uint32_t*>(scratch);
+  float* s_red = reinterpret_cast<float*>(scratch + 128);
+  const int C = plan.C;
+  auto gt = [] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (threadIdx.x == 0) {
+    __threadfence();  // this CTA's partial stores before its arrival
+    s_rank = atomicAdd(e.ctr, 1u) - e.base;
+    if (e.tl) e.tl[blockIdx.x * 4 + 1] = gt();
+  }
+  __syncthreads();
+  const int rank = (int)s_rank;
+  const int units = e.op == kEpiResidualNorm ? M : C;  // norm: one row per helper
+  const int nh = min(C, units);
+  if (rank < C - nh) return;
+  const int hid = rank - (C - nh);
+  if (threadIdx.x == 0) {
+    while ((int)(*reinterpret_cast<volatile uint32_t*>(e.ctr) - e.base) < C) __nanosleep(64);
+    __threadfence();
+    if (e.tl) e.tl[blockIdx.x * 4 + 2] = gt();
+  }
+  __syncthreads();
+  const int nthr = blockDim.x;
+  if (e.op == kEpiResidualNorm) {
+    // rows round-robin over the helpers; per row every thread keeps up to
+    // kV float4 columns in registers, so all slot loads are issued together
+    constexpr int kV = 8;
+    const int d = N, d4 = d >> 2;
+    const size_t stride4 = (size_t)M * d / 4;
+    for (int m = hid; m < M; m += nh) {
+      float4* hr = reinterpret_cast<float4*>(e.h + (size_t)m * d);
+      const float4* pr = reinterpret_cast<const float4*>(part + (size_t)m * d);
+      float4 v[kV];
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < kV; ++j) {
+        const int i4 = threadIdx.x + j * nthr;
+        if (i4 < d4) {
+          const int ns = part_slots(plan, m, i4 * 4);
+          float4 acc = __ldcg(hr + i4);
+          float4 t[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t[q] = q < ns ? __ldcg(pr + i4 + q * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < ns) {
+              sum.x += t[q].x;
+              sum.y += t[q].y;
+              sum.z += t[q].z;
+              sum.w += t[q].w;
+            }
+          for (int q = 4; q < ns; ++q) {
+            const float4 x = __ldcg(pr + i4 + q * stride4);
+            sum.x += x.x;
+            sum.y += x.y;
+            sum.z += x.z;
+            sum.w += x.w;
+          }
+          acc.x += sum.x;
+          acc.y += sum.y;
+          acc.z += sum.z;
+          acc.w += sum.w;
+          v[j] = acc;
+          hr[i4] = acc;
+          ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+        }
+      }
+      for (int i4 = threadIdx.x + kV * nthr; i4 < d4; i4 += nthr) {  // (d > 4 * kV * nthr only)
+        float4 acc = hr[i4];
+        const int ns = part_slots(plan, m, i4 * 4);
+        for (int q = 0; q < ns; ++q) {
+          const float4 x = __ldcg(pr + i4 + q * stride4);
+          acc.x += x.x;
+          acc.y += x.y;
+          acc.z += x.z;
+          acc.w += x.w;
+        }
+        hr[i4] = acc;
+        ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+      }
+      if (e.w == nullptr || m < e.row_begin) continue;  // uniform per CTA
+      ss = warp_sum(ss);
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        float t = threadIdx.x < (unsigned)(nthr >> 5) ? s_red[threadIdx.x] : 0.f;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) s_red[0] = t;
+      }
+      __syncthreads();
+      const float r = 1.0f / sqrtf(s_red[0] / (float)d + e.eps);
+      const int mo = m - e.row_begin;
+      const uint2* w4 = reinterpret_cast<const uint2*>(e.w);
+      for (int i4 = threadIdx.x; i4 < d4; i4 += nthr) {
+        const int jj = (i4 - (int)threadIdx.x) / nthr;
+        float4 vv;
+        if (jj < kV) {
+#pragma unroll
+          for (int j = 0; j < kV; ++j)
+            if (j == jj) vv = v[j];
+        } else {
+          vv = hr[i4];
+        }
+        const uint2 wv = w4[i4];
+        uint2 o;
+        o.x = pack_bf2((vv.x * r) * __uint_as_float(wv.x << 16), (vv.y * r) * __uint_as_float(wv.x & 0xFFFF0000u));
+        o.y = pack_bf2((vv.z * r) * __uint_as_float(wv.y << 16), (vv.w * r) * __uint_as_float(wv.y & 0xFFFF0000u));
+        *reinterpret_cast<uint2*>(e.x + act_off(mo, i4 * 4, d, e.tm_out)) = o;
+      }
+    }
+  } else {  // kEpiSiluMul: N = 2 * ffn, [gate | up]; float4 groups, 4 in flight per thread
+    const int ffn = N >> 1, f4 = ffn >> 2;
+    const size_t total = (size_t)M * f4;
+    const size_t stride4 = (size_t)M * N / 4;
+    const size_t per = (total + nh - 1) / nh;
+    const size_t i0 = (size_t)hid * per, i1 = min(total, i0 + per);
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    for (size_t base = i0; base < i1; base += 4 * (size_t)nthr) {
+      float4 g[4], u[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const size_t idx = base + threadIdx.x + (size_t)j * nthr;
+        g[j] = u[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (idx < i1) {
+          const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
+          const size_t o = (size_t)m * (N / 4) + j4;
+          const int ng = part_slots(plan, m, j4 * 4), nu = part_slots(plan, m, ffn + j4 * 4);
+          float4 tg[4], tu[4];  // all slot loads in flight together (predicated, unrolled)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            tg[q] = q < ng ? __ldcg(p4 + o + q * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            tu[q] = q < nu ? __ldcg(p4 + o + f4 + q * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q < ng) {
+              g[j].x += tg[q].x;
+              g[j].y += tg[q].y;
+              g[j].z += tg[q].z;
+              g[j].w += tg[q].w;
+            }
+            if (q < nu) {
+              u[j].x += tu[q].x;
+              u[j].y += tu[q].y;
+              u[j].z += tu[q].z;
+              u[j].w += tu[q].w;
+            }
+          }
+          for (int q = 4; q < ng; ++q) {
+            const float4 x = __ldcg(p4 + o + q * stride4);
+            g[j].x += x.x;
+            g[j].y += x.y;
+            g[j].z += x.z;
+            g[j].w += x.w;
+          }
+          for (int q = 4; q < nu; ++q) {
+            const float4 x = __ldcg(p4 + o + f4 + q * stride4);
+            u[j].x += x.x;
+            u[j].y += x.y;
+            u[j].z += x.z;
+            u[j].w += x.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const size_t idx = base + threadIdx.x + (size_t)j * nthr;
+        if (idx >= i1) continue;
+        const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
+        uint2 o;
+        o.x = pack_bf2((g[j].x / (1.0f + expf(-g[j].x))) * u[j].x, (g[j].y / (1.0f + expf(-g[j].y))) * u[j].y);
+        o.y = pack_bf2((g[j].z / (1.0f + expf(-g[j].z))) * u[j].z, (g[j].w / (1.0f + expf(-g[j].w))) * u[j].w);
+        *reinterpret_cast<uint2*>(e.x + act_off(m, j4 * 4, ffn, e.tm_out)) = o;
+      }
+    }
+  }
+  if (e.tl) {
+    __syncthreads();
+    if (threadIdx.x == 0) e.tl[blockIdx.x * 4 + 3] = gt();
+  }
+}
+
 template <bool kW4>
 __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
     gemm_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                float* __restrict__ out, int stages, int rstages, int dbg) {
+                float* __restrict__ out, int stages, int rstages, int dbg, GemmEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
   const int nk = plan.nk;
+  if (epi.tl && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    epi.tl[blockIdx.x * 4 + 0] = t;
+  }
 
   const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk
   const uint32_t a_bytes = kW4 ? 32768u : 16384u;
@@ -360,6 +570,7 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem_base, 2 * tm_cols);
+  if (epi.op != kEpiNone) gemm_tail_gang(epi, plan, M, N, out, smem);
 }
 
 
@@ -401,7 +612,7 @@ __device__ __forceinline__ uint32_t nib_magic(uint32_t w) {
 template <int kG>
 __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                        float* __restrict__ out, int bstages, int rstages, int astages, int dbg) {
+                        float* __restrict__ out, int bstages, int rstages, int astages, int dbg, GemmEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -681,6 +892,7 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   __syncthreads();
   stamp(6, threadIdx.x == 0 ? 1 : 64);
   if (warp == 1) tmem_dealloc(tmem_base, 512);
+  if (epi.op != kEpiNone) gemm_tail_gang(epi, plan, M, N, out, smem);
 }
 
 // Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 4).
@@ -786,18 +998,19 @@ static bool w4_tmem_path() {
 
 template <int kG>
 static cudaError_t launch_w4_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                  float* out, int bs, int rs, int as, size_t sm, cudaStream_t stream) {
+                                  float* out, int bs, int rs, int as, size_t sm, cudaStream_t stream,
+                                  const GemmEpi& epi) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   return launch_pdl(gemm_w4_tmem_kernel<kG>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M, TM, plan,
-                    out, bs, rs, as, gemm_debug());
+                    out, bs, rs, as, gemm_debug(), epi);
 }
 
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                        float* out, cudaStream_t stream) {
+                        float* out, cudaStream_t stream, const GemmEpi& epi) {
   size_t smem = 0;
   int rstages = 0;
   const int stages = pick_stages(w4, TM, &rstages, &smem);
@@ -806,9 +1019,9 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
     size_t sm = 0;
     const int bs = pick_w4_stages(TM, &rs, &as, &sm);
     switch (w4_groups()) {
-      case 2: return launch_w4_tmem<2>(w, x, M, TM, plan, out, bs, rs, as, sm, stream);
-      case 3: return launch_w4_tmem<3>(w, x, M, TM, plan, out, bs, rs, as, sm, stream);
-      default: return launch_w4_tmem<4>(w, x, M, TM, plan, out, bs, rs, as, sm, stream);
+      case 2: return launch_w4_tmem<2>(w, x, M, TM, plan, out, bs, rs, as, sm, stream, epi);
+      case 3: return launch_w4_tmem<3>(w, x, M, TM, plan, out, bs, rs, as, sm, stream, epi);
+      default: return launch_w4_tmem<4>(w, x, M, TM, plan, out, bs, rs, as, sm, stream, epi);
     }
   }
   if (w4) {
@@ -818,7 +1031,7 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
       attr = true;
     }
     return launch_pdl(gemm_kernel<true>, dim3(plan.C), dim3(448), smem, stream, w, x, M, TM, plan, out, stages,
-                      rstages, gemm_debug());
+                      rstages, gemm_debug(), epi);
   } else {
     static bool attr = false;
     if (!attr) {
@@ -826,7 +1039,7 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
       attr = true;
     }
     return launch_pdl(gemm_kernel<false>, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, stages,
-                      rstages, gemm_debug());
+                      rstages, gemm_debug(), epi);
   }
   return cudaGetLastError();
 }

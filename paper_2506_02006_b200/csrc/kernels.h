@@ -79,8 +79,32 @@ __host__ __device__ inline int part_slots(const GemmPlanDev& p, int m, int n) {
 }
 
 GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t part_elems);
+
+// Row work fused into the GEMM's tail ("tail gang"): every CTA counts itself
+// in on `ctr` once its partials are written; the last `helpers` CTAs to arrive
+// wait for the rest and then do the row pass over the complete partials, so the
+// separate row kernel (and its launch + grid-dependency latency) disappears.
+// Deterministic: each output element is produced by one CTA summing the slots
+// in slot order, exactly as the standalone row kernels do.  `ctr` is a
+// monotonically increasing arrival counter; `base` = its value before this
+// launch (kept by the host), so no reset is needed.
+enum { kEpiNone = 0, kEpiResidualNorm = 1, kEpiSiluMul = 2 };
+struct GemmEpi {
+  int op = kEpiNone;
+  uint32_t* ctr = nullptr;
+  uint32_t base = 0;
+  // residual + RMSNorm (N = d): h[M][d] += sum(partials); x = pack(bf16(norm(h) * w)) for rows >= row_begin
+  float* h = nullptr;
+  const uint16_t* w = nullptr;
+  float eps = 0.f;
+  int row_begin = 0;
+  // both: packed activation image of the next GEMM (tm_out rows per m-tile)
+  uint16_t* x = nullptr;
+  int tm_out = 0;
+  unsigned long long* tl = nullptr;  // (debug) per-CTA [start, arrive, released, done] globaltimer
+};
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                        float* out, cudaStream_t stream);
+                        float* out, cudaStream_t stream, const GemmEpi& epi = GemmEpi());
 
 // Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
 // every layer): [layer][kv_head][K|V][token][head_dim] bf16.

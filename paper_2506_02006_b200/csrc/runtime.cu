@@ -180,6 +180,10 @@ struct ms_ctx {
   float* q = nullptr;
   float* attn_ws = nullptr;
   size_t attn_ws_elems = 0;
+  uint32_t* gang_ctr = nullptr;          // GEMM tail-gang arrival counters (ring, never reset)
+  std::vector<uint64_t> gang_count;      // host mirror: arrivals so far per counter
+  int gang_next = 0;
+  int64_t tl_counter = 0;
   float* attn_pws = nullptr;   // persistent attention partials
   int* attn_pcnt = nullptr;    // persistent attention item counters [max_batch * KVH]
   int32_t* next = nullptr;
@@ -337,12 +341,81 @@ ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
   return w;
 }
 
-ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
+constexpr int kGangCounters = 256;
+
+// MS_FUSE_ROWS=1 (experiment, off by default): residual-norm / SiLU in the
+// GEMM tails (tail gang) instead of standalone row kernels.  Measured slower
+// on B200 (the tail's row pass runs on 148 x 192-480 threads after the last
+// CTA arrives: +9 us per norm, +18 us per SiLU vs a 4-10 us standalone kernel
+// that starts under PDL), so the standalone kernels stay the default.
+bool fuse_rows() {
+  static const bool v = [] {
+    const char* e = std::getenv("MS_FUSE_ROWS");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM, ms::GemmEpi epi = ms::GemmEpi()) {
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
   const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, w4, c->num_sms, c->part_elems);
-  CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute));
+  if (epi.op != ms::kEpiNone) {  // next arrival counter; every CTA of the plan arrives once
+    const int i = c->gang_next;
+    c->gang_next = (c->gang_next + 1) % kGangCounters;
+    epi.ctr = c->gang_ctr + i;
+    epi.base = (uint32_t)c->gang_count[i];
+    c->gang_count[i] += (uint64_t)plan.C;
+  }
+  static unsigned long long* tl = nullptr;  // (debug) MS_TAIL_TL=<layer*4+mat>: dump that GEMM's tail timeline
+  static const int tl_pick = [] {
+    const char* e = std::getenv("MS_TAIL_TL");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (tl_pick >= 0 && epi.op != ms::kEpiNone && c->tl_counter++ == tl_pick) {
+    if (!tl) CK(cudaMalloc(&tl, 4096 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(tl, 0, 4096 * sizeof(unsigned long long), c->compute));
+    epi.tl = tl;
+    CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute, epi));
+    std::vector<unsigned long long> h(4 * plan.C);
+    CK(cudaMemcpyAsync(h.data(), tl, h.size() * 8, cudaMemcpyDeviceToHost, c->compute));
+    CK(cudaStreamSynchronize(c->compute));
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < plan.C; ++i) t0 = std::min(t0, h[4 * i]);
+    double a_min = 1e30, a_max = 0, r_max = 0, d_max = 0, s_max = 0;
+    for (int i = 0; i < plan.C; ++i) {
+      s_max = std::max(s_max, (h[4 * i] - t0) / 1e3);
+      a_min = std::min(a_min, (h[4 * i + 1] - t0) / 1e3);
+      a_max = std::max(a_max, (h[4 * i + 1] - t0) / 1e3);
+      if (h[4 * i + 2]) r_max = std::max(r_max, (h[4 * i + 2] - t0) / 1e3);
+      if (h[4 * i + 3]) d_max = std::max(d_max, (h[4 * i + 3] - t0) / 1e3);
+    }
+    fprintf(stderr, "tail tl op=%d C=%d N=%d: last start %.2f us, arrivals %.2f..%.2f, released by %.2f, done %.2f\n",
+            epi.op, plan.C, w.N, s_max, a_min, a_max, r_max, d_max);
+  } else {
+    CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute, epi));
+  }
   c->launches += 1;
   return plan;
+}
+
+ms::GemmEpi epi_norm(ms_ctx* c, const uint16_t* w, int tm_out, int row_begin) {
+  ms::GemmEpi e;
+  e.op = ms::kEpiResidualNorm;
+  e.h = c->h;
+  e.w = w;
+  e.eps = c->desc.rms_eps;
+  e.row_begin = row_begin;
+  e.x = c->x;
+  e.tm_out = tm_out;
+  return e;
+}
+
+ms::GemmEpi epi_silu(ms_ctx* c, int tm_out) {
+  ms::GemmEpi e;
+  e.op = ms::kEpiSiluMul;
+  e.x = c->x;
+  e.tm_out = tm_out;
+  return e;
 }
 
 // categories of ms_prof_kernels_read (include/morphserve.h MS_PK_*)
@@ -477,27 +550,36 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     }
     pk_mark(c, MS_PK_ATTN);
     prof_mark(c);
-    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
+    // residual + RMSNorm and SiLU*up run in the GEMM tails (tail gang) unless
+    // disabled or a timing experiment skips pieces of the step
+    const bool fuse = fuse_rows() && skip == 0;
+    const uint16_t* n2 = c->norms + ((size_t)l * 2 + 1) * d;
+    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 1), w4, M, TM, fuse ? epi_norm(c, n2, TM, 0) : ms::GemmEpi());
     pk_mark(c, w4 ? MS_PK_GEMM_O_W4 : MS_PK_GEMM_O);
-    if (!(skip & 2)) CK(ms::residual_norm_launch(c->part, s, M, d, c->h, c->norms + ((size_t)l * 2 + 1) * d, D.rms_eps, c->x, TM,
-                                c->compute));
-    c->launches += 1;
-    pk_mark(c, MS_PK_NORM);
-    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
+    if (!fuse) {
+      if (!(skip & 2)) CK(ms::residual_norm_launch(c->part, s, M, d, c->h, n2, D.rms_eps, c->x, TM, c->compute));
+      c->launches += 1;
+      pk_mark(c, MS_PK_NORM);
+    }
+    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 2), w4, M, TM, fuse ? epi_silu(c, TM) : ms::GemmEpi());
     pk_mark(c, w4 ? MS_PK_GEMM_GU_W4 : MS_PK_GEMM_GU);
-    if (!(skip & 4)) CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
-    c->launches += 1;
-    pk_mark(c, MS_PK_SILU);
-    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
-    pk_mark(c, w4 ? MS_PK_GEMM_DOWN_W4 : MS_PK_GEMM_DOWN);
+    if (!fuse) {
+      if (!(skip & 4)) CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
+      c->launches += 1;
+      pk_mark(c, MS_PK_SILU);
+    }
     const bool last = l == D.num_layers - 1;
     const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
     const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
-    if (!(skip & 2) || last)
-      CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out,
-                                       last ? final_row_begin : 0, c->compute));
-    c->launches += 1;
-    pk_mark(c, MS_PK_NORM);
+    const int row_begin = last ? final_row_begin : 0;
+    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 3), w4, M, TM, fuse ? epi_norm(c, nw, tm_out, row_begin) : ms::GemmEpi());
+    pk_mark(c, w4 ? MS_PK_GEMM_DOWN_W4 : MS_PK_GEMM_DOWN);
+    if (!fuse) {
+      if (!(skip & 2) || last)
+        CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out, row_begin, c->compute));
+      c->launches += 1;
+      pk_mark(c, MS_PK_NORM);
+    }
   }
   const int Mo = M - final_row_begin;
   const int TMo = round16(Mo) > 256 ? 256 : round16(Mo);
@@ -642,6 +724,9 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
                                        sizeof(int)));
       CK(cudaMemset(c->attn_pcnt, 0, (size_t)std::max(desc->max_batch, desc->max_prefill_tokens) *
                                          desc->num_kv_heads * sizeof(int)));
+      CK(cudaMalloc(&c->gang_ctr, kGangCounters * sizeof(uint32_t)));
+      CK(cudaMemset(c->gang_ctr, 0, kGangCounters * sizeof(uint32_t)));
+      c->gang_count.assign(kGangCounters, 0);
       CK(cudaMalloc(&c->next, (size_t)c->max_rows * sizeof(int32_t)));
       CK(cudaMalloc(&c->logits, (size_t)desc->max_batch * desc->vocab * sizeof(float)));
       CK(cudaHostAlloc(&c->h_next, (size_t)c->max_rows * sizeof(int32_t), cudaHostAllocDefault));
@@ -707,7 +792,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
-                 c->h, c->x, c->part, c->q, c->attn_ws, c->attn_pws, c->attn_pcnt, c->next, c->logits, c->hist};
+                 c->h, c->x, c->part, c->q, c->attn_ws, c->attn_pws, c->attn_pcnt, c->gang_ctr, c->next, c->logits, c->hist};
   for (void* p : dev) cudaFree(p);
   cudaFreeHost(c->h_next);
   cudaFreeHost(c->h_logits);
