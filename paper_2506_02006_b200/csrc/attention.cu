@@ -53,14 +53,15 @@ __device__ __forceinline__ float attn_sum_slots(const float* p, size_t stride, i
 // block -- the rotated K and the V of the new token into the paged cache.  The
 // arithmetic is qkv_post_kernel's (elementwise.cu), element for element.
 template <int HD, int G>
-__device__ __forceinline__ void attn_qkv_fused(const AttnArgs& a, int kvh, int row, bool append, float* qs) {
+__device__ __forceinline__ void attn_qkv_fused(const AttnArgs& a, int kvh, int row, bool append, float* qs, int tid,
+                                               int nthr) {
   constexpr int half = HD / 2;
   const int H = a.H, KVH = a.KVH;
   const int N = (H + 2 * KVH) * HD;
   const int p = a.pos[row];
   const size_t stride = (size_t)a.rows * N;
   const int nheads = G + (append ? 2 : 0);
-  for (int idx = threadIdx.x; idx < nheads * half; idx += blockDim.x) {
+  for (int idx = tid; idx < nheads * half; idx += nthr) {
     const int hh = idx / half, i = idx - hh * half;
     const int hs = hh < G ? kvh * G + hh : (hh == G ? H + kvh : H + KVH + kvh);  // q, k, v head slot
     const int c0 = hs * HD + i;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
   // q source: fused QKV post-processing into shared memory, or the q buffer
   float* qsm = scratch + (size_t)4 * G * HD + 8 * G;  // [G][HD] fp32
   const bool fused = a.qkv_part != nullptr;
-  if (fused) attn_qkv_fused<HD, G>(a, kvh, row, b1 == nb, qsm);
+  if (fused) attn_qkv_fused<HD, G>(a, kvh, row, b1 == nb, qsm, threadIdx.x, blockDim.x);
   __syncthreads();
   const float* qsrc = fused ? qsm : a.q + ((size_t)row * a.H + kvh * G) * HD;
 
@@ -396,6 +397,253 @@ __global__ void attn_combine_kernel(AttnArgs a) {
   const int K = a.H * HD;
   const size_t off = a.out_packed ? act_off(row, h * HD + dim, K, a.TM) : (size_t)row * K + h * HD + dim;
   a.out[off] = f2bf(o);
+}
+
+// ---------------------------------------------------------------------------
+// GQA decode attention (G = H / KVH >= 2 query heads per KV head, hd 128) on the
+// tensor cores: per 16-token block one consumer warp computes S = Q K^T with
+// mma.sync m16n8k16 (the G query heads are the M rows; q = hi + lo bf16 split
+// keeps fp32-level score accuracy, as in prefill_attention.cu), the online
+// softmax on the accumulator fragments, and O += P V (P bf16).  The producer
+// warp stages each block's K and V rows with 16-byte cp.async into an
+// XOR-swizzled layout (chunk c of row r at c ^ (r & 7)) so the ldmatrix
+// fragment loads are bank-conflict free; completion is tracked per stage by an
+// mbarrier (cp.async.mbarrier.arrive.noinc).  About 140 instructions per block
+// per warp, versus ~1000 for the CUDA-core consumer with G shuffle reductions.
+__device__ __forceinline__ void gqa_cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void gqa_cp_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void gqa_ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void gqa_ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void gqa_mma(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// byte offset of 16-B chunk c (0..15) of row r (0..15) in a swizzled 16 x 256 B tile
+__device__ __forceinline__ uint32_t gqa_swz(int r, int c) { return (uint32_t)(r * 256 + ((c ^ (r & 7)) * 16)); }
+
+template <int G>
+__global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
+  constexpr int HD = 128, BT = 16;
+  constexpr uint32_t kStageBytes = (uint32_t)BT * HD * 2 * 2;  // K tile then V tile, swizzled
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int S = a.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* kv_ready = empty + S;  // the new token's K/V is in the cache (fused QKV)
+  float* scratch = reinterpret_cast<float*>(kv_ready + 1);  // [4][G][HD] acc + [4][G][2] m,l, then q [G][HD]
+
+  pdl_wait();
+  pdl_trigger();
+  const int kvh = blockIdx.x, row = blockIdx.y, split = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ctx = a.ctx_len[row];
+  const int nb = (ctx + BT - 1) / BT;
+  const int b0 = (int)((int64_t)nb * split / a.splits), b1 = (int)((int64_t)nb * (split + 1) / a.splits);
+  const int prow = a.page_row ? a.page_row[row] : row;
+  const int32_t* ptab = a.pages + (size_t)prow * a.page_stride;
+  const int64_t kv_off = a.kv.layer_off(a.layer) + (int64_t)kvh * 2 * a.kv.head_bytes();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 32);  // the 32 producer lanes' cp.async groups
+      mbar_init(&empty[s], 1);  // the one warp that consumed the block
+    }
+    mbar_init(kv_ready, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  float* qsm = scratch + (size_t)4 * G * HD + 8 * G;  // [G][HD] fp32
+  const bool fused = a.qkv_part != nullptr;
+  const bool append = fused && b1 == nb;  // this CTA writes (then streams) the new token's block
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ producer
+    // streams from the start; only the block holding the new token waits for
+    // the consumers' fused QKV append
+    for (int it = 0; it < b1 - b0; ++it) {
+      const int s = it % S;
+      if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+      if (append && b0 + it == nb - 1) mbar_wait(kv_ready, 0);
+      const char* src = a.kv.arena + (int64_t)ptab[b0 + it] * a.kv.page_bytes + kv_off;
+      const uint32_t dst = smem_u32(smem + (size_t)s * kStageBytes);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int q = lane + 32 * i;  // 16-B chunk of the 8 KB K|V tile
+        const int tile = q >> 8, r = (q >> 4) & 15, c = q & 15;
+        gqa_cp16(dst + tile * 4096 + gqa_swz(r, c), src + (size_t)q * 16);
+      }
+      gqa_cp_arrive(&full[s]);
+    }
+    return;
+  }
+  // ------------------------------------------------------------- consumers
+  if (fused) {  // consumers only (named barrier 1): q into smem, new K/V into the cache
+    attn_qkv_fused<HD, G>(a, kvh, row, append, qsm, threadIdx.x, 128);  // ends with a generic->async proxy fence
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 0 && append) mbar_arrive(kv_ready);
+  }
+  const float* qsrc = fused ? qsm : a.q + ((size_t)row * a.H + kvh * G) * HD;
+  const int g = lane >> 2, t4 = lane & 3;  // fragment row (query head) / column pair
+  // Q A-fragments (rows g < G valid), scaled to the log2 domain, hi/lo split
+  uint32_t qh[8][2], ql[8][2];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      float x0 = 0.f, x1 = 0.f;
+      if (g < G) {
+        const float* qp = qsrc + (size_t)g * HD + ks * 16 + hf * 8 + 2 * t4;
+        x0 = qp[0] * a.scale_log2;
+        x1 = qp[1] * a.scale_log2;
+      }
+      const uint16_t h0 = f2bf(x0), h1 = f2bf(x1);
+      qh[ks][hf] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+      ql[ks][hf] = pack_bf2(x0 - bf2f(h0), x1 - bf2f(h1));
+    }
+  float o[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m = -INFINITY, l = 0.f;  // for query head g (rows g + 8 are padding)
+  // ldmatrix row / chunk of this lane: matrices 0..3 = (rows 0-7 | 8-15) x (chunk c | c+1)
+  const int lr = (lane & 7) + ((lane >> 4) << 3), lc = (lane >> 3) & 1;
+  for (int it = warp; it < b1 - b0; it += 4) {
+    const int s = it % S;
+    mbar_wait(&full[s], (it / S) & 1);
+    const uint32_t kt = smem_u32(smem + (size_t)s * kStageBytes), vt = kt + 4096;
+    // ---- S = Q K^T: n-tile 0 = tokens 0-7, n-tile 1 = tokens 8-15.  A rows g
+    // carry q_hi of head g and rows g + 8 its q_lo, so one MMA per k-step and
+    // n-tile yields both halves (summed below).
+    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t k0, k1, k2, k3;  // (tok 0-7, dims 16ks..+7), (tok 0-7, +8..), (tok 8-15, ..), (tok 8-15, +8..)
+      gqa_ldsm_x4(kt + gqa_swz(lr, 2 * ks + lc), k0, k1, k2, k3);
+      gqa_mma(sc[0], qh[ks][0], ql[ks][0], qh[ks][1], ql[ks][1], k0, k1);
+      gqa_mma(sc[1], qh[ks][0], ql[ks][0], qh[ks][1], ql[ks][1], k2, k3);
+    }
+    // ---- online softmax for head g over this block's 16 tokens
+    const int tok0 = (b0 + it) * BT;
+    // tokens 2t4, 2t4+1, 8+2t4, 9+2t4: hi row + lo row
+    float v4[4] = {sc[0][0] + sc[0][2], sc[0][1] + sc[0][3], sc[1][0] + sc[1][2], sc[1][1] + sc[1][3]};
+    const int tk[4] = {2 * t4, 2 * t4 + 1, 8 + 2 * t4, 9 + 2 * t4};
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (tok0 + tk[e] >= ctx) v4[e] = -INFINITY;
+      mx = fmaxf(mx, v4[e]);
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m, mx);  // finite: every block holds >= 1 valid token
+    const float corr = exp2f(m - mn);
+    float p[4], ps = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      p[e] = exp2f(v4[e] - mn);
+      ps += p[e];
+    }
+    ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+    ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+    l = l * corr + ps;
+    m = mn;
+    const uint32_t pa0 = pack_bf2(p[0], p[1]), pa2 = pack_bf2(p[2], p[3]);
+    // ---- O = O * corr + P V
+#pragma unroll
+    for (int jp = 0; jp < 8; ++jp) {
+      o[2 * jp][0] *= corr;
+      o[2 * jp][1] *= corr;
+      o[2 * jp + 1][0] *= corr;
+      o[2 * jp + 1][1] *= corr;
+      uint32_t v0, v1, v2, v3;  // trans: (tok 0-7, dims 16jp..), (tok 8-15, ..), (tok 0-7, +8), (tok 8-15, +8)
+      const int vr = (lane & 7) + (((lane >> 3) & 1) << 3), vc = 2 * jp + (lane >> 4);
+      gqa_ldsm_x4_t(vt + gqa_swz(vr, vc), v0, v1, v2, v3);
+      gqa_mma(o[2 * jp], pa0, 0u, pa2, 0u, v0, v1);  // rows g + 8 of O stay 0
+      gqa_mma(o[2 * jp + 1], pa0, 0u, pa2, 0u, v2, v3);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  // stash per-warp state: head g < G, dims 8j + 2t4, +1
+  if (g < G) {
+    float* sacc = scratch + ((size_t)warp * G + g) * HD;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      sacc[8 * j + 2 * t4] = o[j][0];
+      sacc[8 * j + 2 * t4 + 1] = o[j][1];
+    }
+    if (t4 == 0) {
+      float* sml = scratch + (size_t)4 * G * HD + ((size_t)warp * G + g) * 2;
+      sml[0] = m;
+      sml[1] = l;
+    }
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const float* smlv = scratch + (size_t)4 * G * HD;
+  for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
+    const int gg = idx / HD, dim = idx - gg * HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, smlv[(w * G + gg) * 2]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float f = exp2f(smlv[(w * G + gg) * 2] - M);
+        L += smlv[(w * G + gg) * 2 + 1] * f;
+        O += scratch[(size_t)(w * G + gg) * HD + dim] * f;
+      }
+    }
+    const int h = kvh * G + gg;
+    const float ov = L > 0.f ? O / L : 0.f;
+    if (a.splits == 1) {
+      const int K = a.H * HD;
+      const size_t off = a.out_packed ? act_off(row, h * HD + dim, K, a.TM) : (size_t)row * K + h * HD + dim;
+      a.out[off] = f2bf(ov);
+    } else {
+      const size_t base = ((size_t)split * a.rows + row) * a.H + h;
+      a.part_o[base * HD + dim] = ov;
+      if (dim == 0) {
+        a.part_ml[base * 2 + 0] = M;
+        a.part_ml[base * 2 + 1] = L;
+      }
+    }
+  }
+}
+
+template <int G>
+static cudaError_t launch_gqa(const AttnArgs& a_in, cudaStream_t stream) {
+  static const int stages = [] {
+    int st = std::max(4, std::min(kAttnMaxStages, attn_env("MS_ATTN_STAGES", 8)));
+    return st / 4 * 4;  // stage s is always consumed by warp s % 4
+  }();
+  AttnArgs a = a_in;
+  a.stages = stages;
+  const size_t smem = (size_t)stages * 8192 + (2 * stages + 1) * 8 + ((size_t)4 * G * 128 + 8 * G + (size_t)G * 128) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_gqa_mma_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid(a.KVH, a.rows, a.splits);
+  cudaError_t e = launch_pdl(attn_gqa_mma_kernel<G>, grid, dim3(160), smem, stream, a);
+  if (e != cudaSuccess || a.splits == 1) return e;
+  return launch_pdl(attn_combine_kernel<128>, dim3(a.rows, a.H), dim3(128), 0, stream, a);
 }
 
 // ---------------------------------------------------------------------------
@@ -768,9 +1016,25 @@ static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
   return launch_pdl(attn_combine_kernel<HD>, dim3(a.rows, a.H), dim3(HD), 0, stream, a);
 }
 
+// MS_ATTN_GQA_MMA=0 (experiments): CUDA-core consumer for GQA as well.
+static bool gqa_mma_enabled() {
+  static const bool v = attn_env("MS_ATTN_GQA_MMA", 1) != 0;
+  return v;
+}
+
 template <int HD>
 static cudaError_t launch_hd(const AttnArgs& a, cudaStream_t stream) {
   const bool persist = a.pws != nullptr && a.pcnt != nullptr && a.splits <= 1 && a.rows <= kPersistRows;
+  if constexpr (HD == 128) {
+    if (!persist && gqa_mma_enabled()) {
+      switch (a.H / a.KVH) {
+        case 2: return launch_gqa<2>(a, stream);
+        case 4: return launch_gqa<4>(a, stream);
+        case 8: return launch_gqa<8>(a, stream);
+        default: break;
+      }
+    }
+  }
   switch (a.H / a.KVH) {
     case 1: return persist ? launch_persist<HD, 1>(a, stream) : launch_g<HD, 1>(a, stream);
     case 2: return persist ? launch_persist<HD, 2>(a, stream) : launch_g<HD, 2>(a, stream);

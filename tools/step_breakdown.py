@@ -22,10 +22,13 @@ MASKS = {"full": 0, "no_rows": 7, "no_qkvpost": 1, "no_norm": 2, "no_silu": 4, "
          "rows_only": 24, "nothing": 31}
 
 
-def child(steps, w4):
+def child(steps, w4, shape):
     import numpy as np
 
     import bench
+    if shape == "8b":  # Llama-3-8B (GQA 32/8), BASELINE configs[2] decode shape
+        from paper_2506_02006_b200.device import LLAMA3_8B
+        bench.SHAPE = dict(LLAMA3_8B)
     dev, table = bench.build_model(0, 4 * steps + 16)
     layers = list(range(32)) if w4 == 32 else bench.W4_LAYERS[:w4]
     for l in layers:
@@ -59,15 +62,17 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--w4", type=int, default=8)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--shape", default="7b", choices=["7b", "8b"])
     ap.add_argument("--masks", default="full,no_rows,no_attn,no_gemm,gemm_only,nothing")
     a = ap.parse_args()
     if a.child:
-        child(a.steps, a.w4)
+        child(a.steps, a.w4, a.shape)
         return
     res = {}
     for name in a.masks.split(","):
         env = dict(os.environ, MS_SKIP=str(MASKS[name]))
-        out = subprocess.run([sys.executable, __file__, "--child", "--steps", str(a.steps), "--w4", str(a.w4)],
+        out = subprocess.run([sys.executable, __file__, "--child", "--steps", str(a.steps), "--w4", str(a.w4),
+                              "--shape", a.shape],
                              env=env, capture_output=True, text=True)
         line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
         res[name] = json.loads(line[-1]) if line else out.stderr[-400:]
