@@ -452,6 +452,11 @@ bool attn_persistent() {
 }
 
 int attn_splits(ms_ctx* c, int rows, int max_ctx) {
+  static const int forced = [] {  // MS_ATTN_SPLITS (experiments)
+    const char* e = std::getenv("MS_ATTN_SPLITS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) return forced;
   const int ctas = rows * c->desc.num_kv_heads;
   const int target = c->num_sms * 4;
   int s = 1;
