@@ -944,8 +944,9 @@ static int pick_stages(bool w4, int TM, int* rstages, size_t* smem_out) {
     if (rs > 16) rs = 16;
     if (rs < 2) rs = 2;
   } else {
+    static const int max_st = w4_env("MS_GEMM_STAGES", 8);  // (experiments) ring depth cap
     st = (int)(budget / stage);
-    if (st > 8) st = 8;
+    if (st > max_st) st = max_st;
     if (st < 2) st = 2;
   }
   *rstages = rs;

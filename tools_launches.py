@@ -18,8 +18,8 @@ def load(path):
         v = float(r[vi].replace(",", ""))
         if r[mi] == "gpu__time_duration.sum":
             d["us"] = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3}.get(r[ui], 1e-3)
-        else:
-            d["MB"] = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(r[ui], 1.0)
+        elif r[mi].startswith("dram__bytes"):  # read + write
+            d["MB"] += v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(r[ui], 1.0)
     return [launch[k] for k in sorted(launch)]
 
 
