@@ -185,6 +185,47 @@ def dev_layer_pages(bits):
     return layer_pages(SHAPE, bits)
 
 
+def serve_arms(dev, wl, arms_csv, rank, world, note, budget_gib=24.0):
+    """Each arm of one bursty trace through the C++ engine on `dev` (GPU clock)."""
+    from paper_2506_02006_b200 import serving as S
+    from paper_2506_02006_b200.replicas import merge_reports
+    cfg = S.device_config(dev, wl, budget_gib=budget_gib, reserve_gib=4.0)
+    out = None
+    for arm in [a for a in arms_csv.split(",") if a]:
+        rep, _ = S.serve(dev, cfg, arm, clock="device")
+        summ = S.summary(rep)
+        if world > 1:
+            import torch.distributed as dist
+            allr = [None] * world
+            dist.all_gather_object(allr, rep)
+            summ["union"] = merge_reports(allr)
+        if out is None:
+            out = dict(summ, arm=arm, workload=wl["gamma"], budget_gib=budget_gib, note=note)
+        else:
+            out.setdefault("baselines", {})[arm] = summ
+    return out
+
+
+def serve_8b(args, local_rank, rank, world):
+    """BASELINE configs[2]: Llama-3-8B shape (GQA 32/8), Gamma-burst trace (CV 2),
+    prompt 1024 / output 512, controller performance defaults
+    (swap up to L/2 layers + KV resize under memory pressure), 24 GiB budget."""
+    from paper_2506_02006_b200.device import LLAMA3_8B, DeviceModel, layer_pages, page_bytes
+    shape = dict(LLAMA3_8B)
+    pb = page_bytes(shape)
+    budget_pages = int(24.0 * (1 << 30)) // pb
+    dev = DeviceModel(shape, device=local_rank, max_batch=128, max_prefill_tokens=2048, max_pos=1024 + 512 + 32,
+                      arena_pages=budget_pages + 2 * layer_pages(shape, 16) + 64)
+    try:
+        dev.weights_synthetic(7)
+        wl = {"gamma": {"seed": 101 + rank, "rps": args.serve8b_rps, "shape": 0.25,
+                        "total_ms": int(args.serve8b_seconds * 1000), "prompt_tokens": 1024, "output_tokens": 512}}
+        return serve_arms(dev, wl, args.serve_arms, rank, world,
+                          "Llama-3-8B shape (BASELINE configs[2]), 24 GiB device budget, measured-GPU-clock engine run")
+    finally:
+        dev.close()
+
+
 def run_ours(args):
     rank, local_rank, world = dist_env()
     import torch
@@ -316,26 +357,11 @@ def run_ours(args):
     # ---- serving: bursty Gamma trace through the engine, measured GPU clock
     serving = None
     if args.serve_seconds > 0:
-        from paper_2506_02006_b200 import serving as S
-        from paper_2506_02006_b200.replicas import merge_reports
         wl = {"gamma": {"seed": 101 + rank, "rps": args.serve_rps, "shape": 0.25,
                         "total_ms": int(args.serve_seconds * 1000), "prompt_tokens": 512, "output_tokens": 128}}
-        cfg = S.device_config(dev, wl, budget_gib=24.0, reserve_gib=4.0)
-        arms = [a for a in args.serve_arms.split(",") if a]
-        for arm in arms:
-            rep, _ = S.serve(dev, cfg, arm, clock="device")
-            summ = S.summary(rep)
-            if world > 1:
-                import torch.distributed as dist
-                allr = [None] * world
-                dist.all_gather_object(allr, rep)
-                summ["union"] = merge_reports(allr)
-            if serving is None:
-                serving = dict(summ, arm=arm, workload=wl["gamma"], budget_gib=24.0,
-                               note="Llama-2-7B shape under a 24 GiB device budget (the paper's L4-class memory "
-                                    "pressure), measured-GPU-clock engine run")
-            else:
-                serving.setdefault("baselines", {})[arm] = summ
+        serving = serve_arms(dev, wl, args.serve_arms, rank, world,
+                             "Llama-2-7B shape under a 24 GiB device budget (the paper's L4-class memory pressure), "
+                             "measured-GPU-clock engine run")
         # the controller and swaps change the layer table: restore the benchmark state
         dev.lib.ms_reset_state(dev.h)
     hbm, peak_kind = peaks()
@@ -379,11 +405,13 @@ def run_ours(args):
                      "share_of_step": attn_ms / ms_prof if ms_prof > 0 else None},
         "clocks": clk.summary(),
     }
+    dev.close()
+    if args.serve8b_seconds > 0:
+        line["serving_8b"] = serve_8b(args, local_rank, rank, world)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    dev.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -400,6 +428,9 @@ def main():
     ap.add_argument("--serve-seconds", type=float, default=8.0, help="bursty serving trace length (0 = skip)")
     ap.add_argument("--serve-rps", type=float, default=20.0)
     ap.add_argument("--serve-arms", default="morph-performance,static-full")
+    ap.add_argument("--serve8b-seconds", type=float, default=8.0,
+                    help="Llama-3-8B bursty serving trace length, BASELINE configs[2] (0 = skip)")
+    ap.add_argument("--serve8b-rps", type=float, default=12.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
