@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -408,14 +409,8 @@ __global__ void attn_combine_kernel(AttnArgs a) {
 // warp stages each block's K and V rows with 16-byte cp.async into an
 // XOR-swizzled layout (chunk c of row r at c ^ (r & 7)) so the ldmatrix
 // fragment loads are bank-conflict free; completion is tracked per stage by an
-// mbarrier (cp.async.mbarrier.arrive.noinc).  About 140 instructions per block
+// mbarrier.  (TMA tensor copies now: one 3-D box per block, 128B-swizzled.)  About 140 instructions per block
 // per warp, versus ~1000 for the CUDA-core consumer with G shuffle reductions.
-__device__ __forceinline__ void gqa_cp16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void gqa_cp_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void gqa_ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -434,14 +429,19 @@ __device__ __forceinline__ void gqa_mma(float (&d)[4], uint32_t a0, uint32_t a1,
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-// byte offset of 16-B chunk c (0..15) of row r (0..15) in a swizzled 16 x 256 B tile
-__device__ __forceinline__ uint32_t gqa_swz(int r, int c) { return (uint32_t)(r * 256 + ((c ^ (r & 7)) * 16)); }
+// byte offset (from the K rows' base) of 16-B chunk c (0..7) of half h of row r in
+// the TMA tile [half][32 rows][128 B] with the 128B swizzle (chunk ^ row % 8)
+__device__ __forceinline__ uint32_t gqa_tsw(int r, int h, int c) {
+  return (uint32_t)(h * 4096 + r * 128 + ((c ^ (r & 7)) * 16));
+}
 
 template <int G>
-__global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   constexpr int HD = 128, BT = 16;
-  constexpr uint32_t kStageBytes = (uint32_t)BT * HD * 2 * 2;  // K tile then V tile, swizzled
-  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr uint32_t kStageBytes = (uint32_t)BT * HD * 2 * 2;  // [half][K rows 0-15 | V rows 16-31][128 B], swizzled
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 128B-swizzled TMA destinations need 1024-B alignment
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int S = a.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * kStageBytes);
   uint64_t* empty = full + S;
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 32);  // the 32 producer lanes' cp.async groups
+      mbar_init(&full[s], 1);  // producer lane 0: expect_tx of the block's tensor copy
       mbar_init(&empty[s], 1);  // the one warp that consumed the block
     }
     mbar_init(kv_ready, 1);
@@ -480,15 +480,18 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
       const int s = it % S;
       if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
       if (append && b0 + it == nb - 1) mbar_wait(kv_ready, 0);
-      const char* src = a.kv.arena + (int64_t)ptab[b0 + it] * a.kv.page_bytes + kv_off;
-      const uint32_t dst = smem_u32(smem + (size_t)s * kStageBytes);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int q = lane + 32 * i;  // 16-B chunk of the 8 KB K|V tile
-        const int tile = q >> 8, r = (q >> 4) & 15, c = q & 15;
-        gqa_cp16(dst + tile * 4096 + gqa_swz(r, c), src + (size_t)q * 16);
+      // one TMA tensor copy per block: the 32 K|V rows of 256 B, as two 128-B
+      // halves, 128B-swizzled by the copy engine (conflict-free ldmatrix)
+      if (lane == 0) {
+        const int64_t row = ((int64_t)ptab[b0 + it] * a.kv.page_bytes + kv_off) >> 8;  // 256-B row of the arena
+        mbar_expect_tx(&full[s], kStageBytes);
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];" ::"r"(smem_u32(smem + (size_t)s * kStageBytes)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"((int)row), "r"(0), "r"(smem_u32(&full[s]))
+            : "memory");
       }
-      gqa_cp_arrive(&full[s]);
+      __syncwarp();
     }
     return;
   }
@@ -525,7 +528,7 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
   for (int it = warp; it < b1 - b0; it += 4) {
     const int s = it % S;
     mbar_wait(&full[s], (it / S) & 1);
-    const uint32_t kt = smem_u32(smem + (size_t)s * kStageBytes), vt = kt + 4096;
+    const uint32_t kt = smem_u32(smem + (size_t)s * kStageBytes), vt = kt + 16 * 128;  // V rows = lines 16..31
     // ---- S = Q K^T: n-tile 0 = tokens 0-7, n-tile 1 = tokens 8-15.  A rows g
     // carry q_hi of head g and rows g + 8 its q_lo, so one MMA per k-step and
     // n-tile yields both halves (summed below).
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       uint32_t k0, k1, k2, k3;  // (tok 0-7, dims 16ks..+7), (tok 0-7, +8..), (tok 8-15, ..), (tok 8-15, +8..)
-      gqa_ldsm_x4(kt + gqa_swz(lr, 2 * ks + lc), k0, k1, k2, k3);
+      gqa_ldsm_x4(kt + gqa_tsw(lr, ks >> 2, 2 * (ks & 3) + lc), k0, k1, k2, k3);
       gqa_mma(sc[0], qh[ks][0], ql[ks][0], qh[ks][1], ql[ks][1], k0, k1);
       gqa_mma(sc[1], qh[ks][0], ql[ks][0], qh[ks][1], ql[ks][1], k2, k3);
     }
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
       o[2 * jp + 1][1] *= corr;
       uint32_t v0, v1, v2, v3;  // trans: (tok 0-7, dims 16jp..), (tok 8-15, ..), (tok 0-7, +8), (tok 8-15, +8)
       const int vr = (lane & 7) + (((lane >> 3) & 1) << 3), vc = 2 * jp + (lane >> 4);
-      gqa_ldsm_x4_t(vt + gqa_swz(vr, vc), v0, v1, v2, v3);
+      gqa_ldsm_x4_t(vt + gqa_tsw(vr, vc >> 3, vc & 7), v0, v1, v2, v3);
       gqa_mma(o[2 * jp], pa0, 0u, pa2, 0u, v0, v1);  // rows g + 8 of O stay 0
       gqa_mma(o[2 * jp + 1], pa0, 0u, pa2, 0u, v2, v3);
     }
@@ -626,6 +629,30 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a) {
   }
 }
 
+// 3-D tensor map over the KV arena viewed as [half 2][row R][64 bf16]: row = one
+// 256-B (K or V token) row, strides 256 B (rows) and 128 B (halves); box
+// {64, 32, 2} = one block's 16 K + 16 V rows.  Encoded once per arena.
+static bool gqa_tensor_map(const KvGeom& kv, int64_t arena_bytes, CUtensorMap* out) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[3] = {64, (cuuint64_t)(arena_bytes / 256), 2};
+  const cuuint64_t strides[2] = {256, 128};  // bytes, dims 1 and 2
+  const cuuint32_t box[3] = {64, 32, 2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, kv.arena, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int G>
 static cudaError_t launch_gqa(const AttnArgs& a_in, cudaStream_t stream) {
   static const int stages = [] {
@@ -634,14 +661,24 @@ static cudaError_t launch_gqa(const AttnArgs& a_in, cudaStream_t stream) {
   }();
   AttnArgs a = a_in;
   a.stages = stages;
-  const size_t smem = (size_t)stages * 8192 + (2 * stages + 1) * 8 + ((size_t)4 * G * 128 + 8 * G + (size_t)G * 128) * 4;
+  static thread_local const char* map_arena = nullptr;
+  static thread_local int64_t map_bytes = 0;
+  static thread_local CUtensorMap tmap;
+  if (a.arena_bytes <= 0) return cudaErrorInvalidValue;
+  if (map_arena != a.kv.arena || map_bytes != a.arena_bytes) {
+    if (!gqa_tensor_map(a.kv, a.arena_bytes, &tmap)) return cudaErrorInvalidValue;
+    map_arena = a.kv.arena;
+    map_bytes = a.arena_bytes;
+  }
+  const size_t smem = 1024 + (size_t)stages * 8192 + 2 * stages * 8 +
+                      ((size_t)4 * G * 128 + 8 * G + (size_t)G * 128) * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_gqa_mma_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   dim3 grid(a.KVH, a.rows, a.splits);
-  cudaError_t e = launch_pdl(attn_gqa_mma_kernel<G>, grid, dim3(160), smem, stream, a);
+  cudaError_t e = launch_pdl(attn_gqa_mma_kernel<G>, grid, dim3(160), smem, stream, a, tmap);
   if (e != cudaSuccess || a.splits == 1) return e;
   return launch_pdl(attn_combine_kernel<128>, dim3(a.rows, a.H), dim3(128), 0, stream, a);
 }
@@ -1026,7 +1063,7 @@ template <int HD>
 static cudaError_t launch_hd(const AttnArgs& a, cudaStream_t stream) {
   const bool persist = a.pws != nullptr && a.pcnt != nullptr && a.splits <= 1 && a.rows <= kPersistRows;
   if constexpr (HD == 128) {
-    if (!persist && gqa_mma_enabled()) {
+    if (!persist && gqa_mma_enabled() && a.arena_bytes > 0) {
       switch (a.H / a.KVH) {
         case 2: return launch_gqa<2>(a, stream);
         case 4: return launch_gqa<4>(a, stream);

@@ -146,6 +146,7 @@ struct AttnArgs {
   float* pws;               // [ctas][2][G][HD + 2] partial (acc, m, l) of items split between CTAs
   int* pcnt;                // [rows * KVH] arrival counters, zero between launches (self-resetting)
   int ctas;                 // persistent grid size (set by attn_decode_launch)
+  int64_t arena_bytes;      // size of kv.arena (GQA tensor-core path: TMA tensor map over the arena)
 };
 // Persistent-grid size and workspace floats the stream-K decode attention needs.
 int attn_persist_ctas(int num_sms);

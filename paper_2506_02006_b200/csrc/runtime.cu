@@ -550,6 +550,7 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       a.out = c->x;
       a.out_packed = 1;
       a.TM = TM;
+      a.arena_bytes = (int64_t)c->desc.arena_pages * c->page_bytes;
       if (!(skip & 8)) CK(ms::attn_decode_launch(a, c->compute));
       c->launches += asplits > 1 ? 2 : 1;
     }
@@ -1393,6 +1394,13 @@ int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int 
     a.out = out;
     a.out_packed = 0;
     a.TM = 16;
+    {  // arena extent for the GQA path's tensor map: pages referenced by the table
+      std::vector<int32_t> hp((size_t)rows * max_blocks);
+      CK(cudaMemcpy(hp.data(), pages, hp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      int32_t mx = 0;
+      for (int32_t v : hp) mx = std::max(mx, v);
+      a.arena_bytes = (int64_t)(mx + 1) * page_bytes;
+    }
     if (a.splits > 1 && !workspace) fail(MS_EVALIDATION, "attn: split-KV needs a workspace");
     if (splits == 0) {  // persistent stream-K kernel (the decode-step path)
       static thread_local float* pws = nullptr;

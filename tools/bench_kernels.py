@@ -20,7 +20,9 @@ import torch  # noqa: E402
 from paper_2506_02006_b200 import _native as N  # noqa: E402
 
 SHAPES = {"qkv": (12288, 4096), "o": (4096, 4096), "gate_up": (22016, 4096), "down": (4096, 11008),
-          "lm_head": (32000, 4096)}
+          "lm_head": (32000, 4096),
+          # Llama-2-13B (BASELINE configs[3] prefill): d 5120, ffn 13824
+          "qkv13": (15360, 5120), "o13": (5120, 5120), "gate_up13": (27648, 5120), "down13": (5120, 13824)}
 
 
 def stream():
@@ -63,7 +65,7 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
     del w
     copies = [wp] + [wp.clone() for _ in range(max(0, -(-300_000_000 // wp.numel() // wp.element_size()) - 1))]
     xp = torch.randint(-2000, 2000, (((M + TM - 1) // TM) * TM * K,), dtype=torch.int16, device="cuda")
-    out = torch.zeros(160 * M * Nn, dtype=torch.float32, device="cuda")
+    out = torch.zeros((160 if M <= 256 else 4) * M * Nn, dtype=torch.float32, device="cuda")
     used = C.c_int()
     i = [0]
 
@@ -74,6 +76,7 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
                             C.c_void_p(out.data_ptr()), C.byref(used), stream()))
     ms = time_it(run, iters=4 * len(copies) if len(copies) > 12 else 48, warm=len(copies) + 2)
     total = wbytes + M * K * 2 + M * Nn * 4
+    tflops = 2.0 * M * Nn * K / (ms * 1e-3) / 1e12
     if int(os.environ.get("MS_GEMM_DEBUG", "0")) & 8:
         torch.cuda.synchronize()
         tl = out[150 * M * Nn:150 * M * Nn + 2 * 8 * 64].view(torch.int64).view(8, 64).cpu().numpy()
@@ -89,8 +92,8 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
         print("chunks", n, "issue->full latency us: first", [round(x, 2) for x in lat[:4]], "mean(after 16)",
               round(float(np.mean(lat[16:])), 2) if len(lat) > 16 else None,
               "full->full gap mean(after 16)", round(float(np.mean(gaps[16:])), 3) if len(gaps) > 16 else None)
-    return {"bits": bits, "N": Nn, "K": K, "M": M, "us": ms * 1e3, "GBps": total / ms / 1e6, "slots": used.value,
-            "copies": len(copies)}
+    return {"bits": bits, "N": Nn, "K": K, "M": M, "us": ms * 1e3, "GBps": total / ms / 1e6, "TFLOPs": tflops,
+            "slots": used.value, "copies": len(copies)}
 
 
 def main():
