@@ -158,7 +158,7 @@ def build_model(local_rank: int, extra_steps: int):
     kv_pages = BATCH * blocks_per_seq
     w_pages = SHAPE["L"] * layer_pages(SHAPE, 16)
     staging = len(W4_LAYERS) * layer_pages(SHAPE, 4) + 64
-    dev = DeviceModel(SHAPE, device=local_rank, max_batch=BATCH, max_prefill_tokens=1024,
+    dev = DeviceModel(SHAPE, device=local_rank, max_batch=128, max_prefill_tokens=1024,
                       max_pos=CTX + extra_steps + 32, arena_pages=kv_pages + w_pages + staging)
     dev.weights_synthetic(7)
     dev.hist_reserve(BATCH, CTX + extra_steps + 33)
@@ -358,7 +358,7 @@ def run_ours(args):
     serving = None
     if args.serve_seconds > 0:
         wl = {"gamma": {"seed": 101 + rank, "rps": args.serve_rps, "shape": 0.25,
-                        "total_ms": int(args.serve_seconds * 1000), "prompt_tokens": 512, "output_tokens": 128}}
+                        "total_ms": int(args.serve_seconds * 1000), "prompt_tokens": 512, "output_tokens": 256}}
         serving = serve_arms(dev, wl, args.serve_arms, rank, world,
                              "Llama-2-7B shape under a 24 GiB device budget (the paper's L4-class memory pressure), "
                              "measured-GPU-clock engine run")
@@ -426,11 +426,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serve-seconds", type=float, default=8.0, help="bursty serving trace length (0 = skip)")
-    ap.add_argument("--serve-rps", type=float, default=20.0)
+    ap.add_argument("--serve-rps", type=float, default=24.0)
     ap.add_argument("--serve-arms", default="morph-performance,static-full")
     ap.add_argument("--serve8b-seconds", type=float, default=8.0,
                     help="Llama-3-8B bursty serving trace length, BASELINE configs[2] (0 = skip)")
-    ap.add_argument("--serve8b-rps", type=float, default=12.0)
+    ap.add_argument("--serve8b-rps", type=float, default=16.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
