@@ -609,7 +609,10 @@ __device__ __forceinline__ uint32_t nib_magic(uint32_t w) {
   return x;
 }
 
-template <int kG>
+// kGPS = 128-wide K groups per pipeline unit (1 or 2): two groups per unit
+// halve the per-unit handshakes (mbarrier round trips, MMA commits, B copies)
+// per weight byte.
+template <int kG, int kGPS>
 __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
                         float* __restrict__ out, int bstages, int rstages, int astages, int dbg, GemmEpi epi) {
@@ -618,8 +621,11 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
   const int nk = plan.nk;
-  const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk; a B stage holds two
-  const uint32_t raw_stage = 8576u;
+  const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk; a B stage holds 2 * kGPS
+  constexpr uint32_t raw_stage = kGPS == 1 ? 8576u : 16896u;
+  constexpr uint32_t raw_bytes = kGPS * (uint32_t)kW4ChunkBytes;
+  constexpr uint32_t a_cols = 64u * kGPS;  // packed bf16x2 TMEM columns of one A stage
+  const int64_t gpr = W.K / 128;           // W4 chunks (K groups) per weight row tile
   const uint32_t tm_cols = TM <= 32 ? 32u : TM <= 64 ? 64u : TM <= 128 ? 128u : 256u;
   const uint32_t acc_bufs = TM <= 128 ? 2u : 1u;
   const uint32_t a_col0 = acc_bufs * tm_cols;
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   };
 
   uint8_t* bbase = smem;
-  uint8_t* rbase = smem + (size_t)bstages * 2 * b_bytes;
+  uint8_t* rbase = smem + (size_t)bstages * 2 * kGPS * b_bytes;
   uint64_t* bfull = reinterpret_cast<uint64_t*>(rbase + (size_t)rstages * raw_stage);
   uint64_t* bempty = bfull + bstages;
   uint64_t* rfull = bempty + bstages;
@@ -644,7 +650,7 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   uint64_t* tfull = aempty + kMaxAStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  auto sB = [&](int s) { return bbase + (size_t)s * 2 * b_bytes; };
+  auto sB = [&](int s) { return bbase + (size_t)s * 2 * kGPS * b_bytes; };
   auto sRaw = [&](int r) { return rbase + (size_t)r * raw_stage; };
 
   if (threadIdx.x == 0) {
@@ -671,14 +677,32 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   // int4 chunks is issued before the TMEM allocation and the CTA barrier.
   uint32_t npre = 0;
   ChunkCursor cur(W, kW4ChunkBytes);
+  // one unit's kGPS consecutive chunks into raw stage r (one copy when they
+  // are contiguous in the same page); leaves the cursor at the next unit
+  auto issue_unit = [&](int r) {
+    mbar_expect_tx(&rfull[r], raw_bytes);
+    const uint8_t* c0 = cur.get();
+    cur.advance();
+    if (kGPS == 1) {
+      bulk_g2s(sRaw(r), c0, kW4ChunkBytes, &rfull[r]);
+      return;
+    }
+    const uint8_t* c1 = cur.get();
+    cur.advance();
+    if (c1 == c0 + kW4ChunkBytes) {
+      bulk_g2s(sRaw(r), c0, 2 * kW4ChunkBytes, &rfull[r]);
+    } else {
+      bulk_g2s(sRaw(r), c0, kW4ChunkBytes, &rfull[r]);
+      bulk_g2s(sRaw(r) + kW4ChunkBytes, c1, kW4ChunkBytes, &rfull[r]);
+    }
+  };
   if (threadIdx.x == 0) {
     SegIter pre(plan, cta);
     int t, k0, k1;
     while (npre < (uint32_t)rstages && pre.next(t, k0, k1)) {
-      cur.seek(W.first_chunk + (int64_t)(t % plan.n_tiles) * nk + k0);
-      for (int k = k0; k < k1 && npre < (uint32_t)rstages; ++k, ++npre, cur.advance()) {
-        mbar_expect_tx(&rfull[npre], kW4ChunkBytes);
-        bulk_g2s(sRaw(npre), cur.get(), kW4ChunkBytes, &rfull[npre]);
+      cur.seek(W.first_chunk + (int64_t)(t % plan.n_tiles) * gpr + (int64_t)k0 * kGPS);
+      for (int k = k0; k < k1 && npre < (uint32_t)rstages; ++k, ++npre) {
+        issue_unit((int)npre);
         stamp(0, npre);
       }
     }
@@ -705,13 +729,13 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
           continue;
         }
         const int n_tile = t % plan.n_tiles;
-        cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
-        for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
-          if (it < npre) continue;
+        const int skip = it < npre ? (int)(npre - it) : 0;  // units of this segment already issued
+        it += (uint32_t)skip;
+        cur.seek(W.first_chunk + (int64_t)n_tile * gpr + (int64_t)(k0 + skip) * kGPS);
+        for (int k = k0 + skip; k < k1; ++k, ++it) {
           const int r = it % rstages;
           mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
-          mbar_expect_tx(&rfull[r], kW4ChunkBytes);
-          bulk_g2s(sRaw(r), cur.get(), kW4ChunkBytes, &rfull[r]);
+          issue_unit(r);
           stamp(0, it);
         }
       }
@@ -735,11 +759,11 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
         mbar_wait(&afull[a], aph);
         tc_fence_after();
         stamp(4, it);
-        const uint64_t db = desc_add(dB0, s * 2u * b_bytes);
-        const uint32_t ta = tmem_base + a_col0 + a * 64u;
+        const uint64_t db = desc_add(dB0, s * 2u * kGPS * b_bytes);
+        const uint32_t ta = tmem_base + a_col0 + a * a_cols;
         if (elect_one()) {
 #pragma unroll
-          for (int sub = 0; sub < 2; ++sub) {
+          for (int sub = 0; sub < 2 * kGPS; ++sub) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               if (!(dbg & 2))
@@ -783,8 +807,8 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
             mbar_expect_tx(&bfull[s], 0);
             continue;
           }
-          mbar_expect_tx(&bfull[s], 2 * b_bytes);
-          bulk_g2s(sB(s), xb + (size_t)(2 * k) * b_bytes, 2 * b_bytes, &bfull[s]);
+          mbar_expect_tx(&bfull[s], 2 * kGPS * b_bytes);
+          bulk_g2s(sB(s), xb + (size_t)(2 * kGPS * k) * b_bytes, 2 * kGPS * b_bytes, &bfull[s]);
           stamp(5, it);
         }
       }
@@ -843,12 +867,16 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
         mbar_wait(&rfull[rs], (it / rstages) & 1);
         if (lane == 0 && quad == 0) stamp(1, it);
         const uint8_t* raw = sRaw(rs);
-        __nv_bfloat162 sc;
-        sc.x = __ushort_as_bfloat16(*reinterpret_cast<const uint16_t*>(raw + 8192 + 2 * row));
-        sc.y = sc.x;
-        uint4 q[4];
+        __nv_bfloat162 sc[kGPS];
+        uint4 q[kGPS][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) q[j] = *reinterpret_cast<const uint4*>(raw + (j * 128 + row) * 16);
+        for (int h = 0; h < kGPS; ++h) {
+          const uint8_t* rh = raw + h * kW4ChunkBytes;
+          sc[h].x = __ushort_as_bfloat16(*reinterpret_cast<const uint16_t*>(rh + 8192 + 2 * row));
+          sc[h].y = sc[h].x;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) q[h][j] = *reinterpret_cast<const uint4*>(rh + (j * 128 + row) * 16);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[rs]);  // raw chunk consumed (values are in registers)
         if (it >= (uint32_t)astages) mbar_wait(&aempty[a], ((it / astages) & 1) ^ 1);
@@ -860,24 +888,26 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
           continue;
         }
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t o[32];
+        for (int h = 0; h < kGPS; ++h)
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const uint4 qq = q[hh * 2 + jj];
-            const uint32_t words[4] = {qq.x, qq.y, qq.z, qq.w};
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t o[32];
 #pragma unroll
-            for (int w = 0; w < 4; ++w)
+            for (int jj = 0; jj < 2; ++jj) {
+              const uint4 qq = q[h][hh * 2 + jj];
+              const uint32_t words[4] = {qq.x, qq.y, qq.z, qq.w};
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint32_t x = nib_magic(words[w] >> (4 * i));
-                __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
-                v = __hmul2(__hsub2(v, bias), sc);  // exact code, then one rounding of code*scale
-                o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
-              }
+              for (int w = 0; w < 4; ++w)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const uint32_t x = nib_magic(words[w] >> (4 * i));
+                  __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
+                  v = __hmul2(__hsub2(v, bias), sc[h]);  // exact code, then one rounding of code*scale
+                  o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
+                }
+            }
+            tmem_st32(lane_base + (uint32_t)a * a_cols + (uint32_t)h * 64u + (uint32_t)hh * 32u, o);
           }
-          tmem_st32(lane_base + (uint32_t)a * 64u + (uint32_t)hh * 32u, o);
-        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -895,12 +925,12 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   if (epi.op != kEpiNone) gemm_tail_gang(epi, plan, M, N, out, smem);
 }
 
-// Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 4).
+// Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 2: measured fastest).
 static int w4_groups() {
   static const int v = [] {
     const char* e = std::getenv("MS_W4_GROUPS");
-    const int g = e ? std::atoi(e) : 4;
-    return g == 2 || g == 3 ? g : 4;
+    const int g = e ? std::atoi(e) : 2;
+    return g == 3 || g == 4 ? g : 2;
   }();
   return v;
 }
@@ -910,20 +940,21 @@ static int w4_env(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-static int pick_w4_stages(int TM, int* rstages, int* astages, size_t* smem_out) {
+static int pick_w4_stages(int TM, int gps, int* rstages, int* astages, size_t* smem_out) {
   const size_t budget = 215 * 1024;
-  const size_t bst = (size_t)TM * 128 * 2;
+  const size_t bst = (size_t)TM * 128 * 2 * gps;
+  const size_t raw_stage = gps == 1 ? 8576 : 16896;
   static const int bs_env = w4_env("MS_W4_BSTAGES", 0), rs_env = w4_env("MS_W4_RSTAGES", 16);
-  int bs = TM <= 64 ? 6 : (TM <= 128 ? 4 : 2);
+  int bs = gps == 1 ? (TM <= 64 ? 6 : (TM <= 128 ? 4 : 2)) : (TM <= 64 ? 3 : (TM <= 128 ? 2 : 1));
   if (bs_env > 0 && (size_t)bs_env * bst <= budget / 2) bs = bs_env;
-  int rs = (int)((budget - bs * bst) / 8576);
+  int rs = (int)((budget - bs * bst) / raw_stage);
   if (rs > rs_env) rs = rs_env;
   if (rs < 2) rs = 2;
   *rstages = rs;
   const int tm_cols = TM <= 32 ? 32 : TM <= 64 ? 64 : TM <= 128 ? 128 : 256;
   const int acc = (TM <= 128 ? 2 : 1) * tm_cols;
-  *astages = std::min(kMaxAStages, (512 - acc) / 64);
-  *smem_out = bs * bst + (size_t)rs * 8576 + (2 * bs + 2 * rs + 2 * kMaxAStages + 4) * 8 + 64;
+  *astages = std::min(kMaxAStages, (512 - acc) / (64 * gps));
+  *smem_out = bs * bst + (size_t)rs * raw_stage + (2 * bs + 2 * rs + 2 * kMaxAStages + 4) * 8 + 64;
   return bs;
 }
 
@@ -954,6 +985,22 @@ static int pick_stages(bool w4, int TM, int* rstages, size_t* smem_out) {
   return st;
 }
 
+// MS_W4_SMEM=1 selects the shared-memory dequant path (A operand in smem).
+static bool w4_tmem_path() {
+  static const bool on = [] {
+    const char* e = std::getenv("MS_W4_SMEM");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+
+// MS_W4_GPS=1 (experiments): one 128-wide K group per W4 pipeline unit.
+static int w4_gps() {
+  static const int v = w4_env("MS_W4_GPS", 2) == 1 ? 1 : 2;
+  return v;
+}
+
 void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages) {
   const int64_t chunks = (int64_t)(w.N / 128) * (w.K / (w4 ? 128 : 64));
   const int64_t p0 = w.first_chunk / w.chunks_per_page;
@@ -969,7 +1016,8 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
   GemmPlanDev p{};
   p.n_tiles = N / 128;
   p.TM = TM;
-  p.nk = K / (w4 ? 128 : 64);
+  // W4 on the TMEM path: two 128-wide K groups per unit when K allows (MS_W4_GPS=1 disables)
+  p.nk = K / (w4 ? (w4_tmem_path() && w4_gps() == 2 && K % 256 == 0 ? 256 : 128) : 64);
   p.tiles = p.n_tiles * ((M + TM - 1) / TM);
   p.T = (int64_t)p.tiles * p.nk;
   p.C = (int)std::min<int64_t>(num_sms, p.T);
@@ -988,26 +1036,29 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
   return p;
 }
 
-// MS_W4_SMEM=1 selects the shared-memory dequant path (A operand in smem).
-static bool w4_tmem_path() {
-  static const bool on = [] {
-    const char* e = std::getenv("MS_W4_SMEM");
-    return !(e && e[0] == '1');
-  }();
-  return on;
-}
-
-template <int kG>
+template <int kG, int kGPS>
 static cudaError_t launch_w4_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                  float* out, int bs, int rs, int as, size_t sm, cudaStream_t stream,
-                                  const GemmEpi& epi) {
+                                  float* out, cudaStream_t stream, const GemmEpi& epi) {
+  int rs = 0, as = 0;
+  size_t sm = 0;
+  const int bs = pick_w4_stages(TM, kGPS, &rs, &as, &sm);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG, kGPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  return launch_pdl(gemm_w4_tmem_kernel<kG>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M, TM, plan,
-                    out, bs, rs, as, gemm_debug(), epi);
+  return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M, TM,
+                    plan, out, bs, rs, as, gemm_debug(), epi);
+}
+
+template <int kGPS>
+static cudaError_t launch_w4_groups(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+                                    float* out, cudaStream_t stream, const GemmEpi& epi) {
+  switch (w4_groups()) {
+    case 3: return launch_w4_tmem<3, kGPS>(w, x, M, TM, plan, out, stream, epi);
+    case 4: return launch_w4_tmem<4, kGPS>(w, x, M, TM, plan, out, stream, epi);
+    default: return launch_w4_tmem<2, kGPS>(w, x, M, TM, plan, out, stream, epi);
+  }
 }
 
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
@@ -1016,14 +1067,9 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
   int rstages = 0;
   const int stages = pick_stages(w4, TM, &rstages, &smem);
   if (w4 && w4_tmem_path()) {
-    int rs = 0, as = 0;
-    size_t sm = 0;
-    const int bs = pick_w4_stages(TM, &rs, &as, &sm);
-    switch (w4_groups()) {
-      case 2: return launch_w4_tmem<2>(w, x, M, TM, plan, out, bs, rs, as, sm, stream, epi);
-      case 3: return launch_w4_tmem<3>(w, x, M, TM, plan, out, bs, rs, as, sm, stream, epi);
-      default: return launch_w4_tmem<4>(w, x, M, TM, plan, out, bs, rs, as, sm, stream, epi);
-    }
+    // the plan fixed the unit: K / nk = 256 -> two K groups per pipeline unit
+    if (w.K / plan.nk == 256) return launch_w4_groups<2>(w, x, M, TM, plan, out, stream, epi);
+    return launch_w4_groups<1>(w, x, M, TM, plan, out, stream, epi);
   }
   if (w4) {
     static bool attr = false;
