@@ -307,9 +307,67 @@ __global__ void __launch_bounds__(512) argmax_kernel(const float* __restrict__ p
   }
 }
 
+// Wide-vocabulary variant: grid (rows, vocab chunks of kArgChunk).  Each CTA
+// reduces its chunk to one 64-bit key (orderable value << 32 | ~index, so
+// atomicMax picks the largest logit and, among equals, the lowest id -- the
+// same tie rule as above, independent of arrival order) and the last CTA of
+// the row to arrive writes the token, then resets the row's key and counter.
+constexpr int kArgChunk = 4096;
+
+__device__ __forceinline__ unsigned long long argmax_key(float v, int i) {
+  uint32_t u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)u << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i);
+}
+
+__global__ void __launch_bounds__(256) argmax_wide_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int V,
+                                                          float* __restrict__ logits_out, int32_t* __restrict__ next_out,
+                                                          int32_t* __restrict__ hist, const int32_t* __restrict__ slot,
+                                                          const int32_t* __restrict__ pos, int hist_stride,
+                                                          unsigned long long* __restrict__ row_key,
+                                                          int* __restrict__ row_cnt) {
+  __shared__ unsigned long long bk[8];
+  __shared__ int last;
+  pdl_wait();
+  pdl_trigger();
+  const int m = blockIdx.x, v0 = blockIdx.y * kArgChunk, v1 = min(V, v0 + kArgChunk);
+  const size_t stride = (size_t)M * V;
+  unsigned long long best = 0;
+  for (int v = v0 + threadIdx.x; v < v1; v += 256) {
+    const float x = sum_slots(part + (size_t)m * V + v, stride, part_slots(plan, m, v));
+    if (logits_out) logits_out[(size_t)m * V + v] = x;
+    const unsigned long long k = argmax_key(x, v);
+    best = k > best ? k : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, best, o);
+    best = ok > best ? ok : best;
+  }
+  if ((threadIdx.x & 31) == 0) bk[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) best = bk[i] > best ? bk[i] : best;
+    atomicMax(row_key + m, best);
+    __threadfence();
+    last = atomicAdd(row_cnt + m, 1) == (int)gridDim.y - 1;
+    if (last) {
+      __threadfence();
+      const unsigned long long k = atomicExch(row_key + m, 0ull);  // read the row's max, reset for the next launch
+      row_cnt[m] = 0;
+      const int besti = (int)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+      if (next_out) next_out[m] = besti;
+      if (hist) hist[(size_t)slot[m] * hist_stride + pos[m] + 1] = besti;
+    }
+  }
+}
+
 cudaError_t argmax_launch(const float* part, const GemmPlanDev& plan, int M, int V, float* logits_out, int32_t* next_out,
                           int32_t* hist, const int32_t* slot, const int32_t* pos, int hist_stride,
-                          cudaStream_t s) {
+                          cudaStream_t s, unsigned long long* row_key, int* row_cnt) {
+  if (row_key && row_cnt && V > 2 * kArgChunk)
+    return launch_pdl(argmax_wide_kernel, dim3(M, (V + kArgChunk - 1) / kArgChunk), dim3(256), 0, s, part, plan, M, V,
+                      logits_out, next_out, hist, slot, pos, hist_stride, row_key, row_cnt);
   return launch_pdl(argmax_kernel, dim3(M), dim3(512), 0, s, part, plan, M, V, logits_out, next_out, hist, slot, pos,
                     hist_stride);
 }

@@ -182,9 +182,11 @@ cudaError_t residual_norm_rows_launch(const float* part, const GemmPlanDev& plan
                                       int norm_row_begin, cudaStream_t s);
 cudaError_t silu_mul_launch(const float* part, const GemmPlanDev& plan, int M, int ffn, uint16_t* x_packed, int TM,
                             cudaStream_t s);
+// row_key / row_cnt ([M] each, zero between launches): per-row scratch of the
+// wide-vocabulary (vocab-chunked) variant; nullptr selects one CTA per row.
 cudaError_t argmax_launch(const float* part, const GemmPlanDev& plan, int M, int V, float* logits_out, int32_t* next_out,
                           int32_t* hist, const int32_t* slot, const int32_t* pos, int hist_stride,
-                          cudaStream_t s);
+                          cudaStream_t s, unsigned long long* row_key = nullptr, int* row_cnt = nullptr);
 cudaError_t gen_weight_launch(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset,
                               uint16_t* out, cudaStream_t s);
 cudaError_t pack_bf16_launch(const uint16_t* w, int N, int K, uint16_t* out, cudaStream_t s);

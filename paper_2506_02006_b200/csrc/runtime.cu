@@ -181,6 +181,8 @@ struct ms_ctx {
   float* attn_ws = nullptr;
   size_t attn_ws_elems = 0;
   uint32_t* gang_ctr = nullptr;          // GEMM tail-gang arrival counters (ring, never reset)
+  unsigned long long* am_key = nullptr;  // wide argmax: per-row best key (self-resetting)
+  int* am_cnt = nullptr;                 // wide argmax: per-row arrival counter (self-resetting)
   std::vector<uint64_t> gang_count;      // host mirror: arrivals so far per counter
   int gang_next = 0;
   int64_t tl_counter = 0;
@@ -595,7 +597,8 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   const ms::GemmPlanDev s = gemm(c, lw, false, Mo, TMo);
   pk_mark(c, MS_PK_LM_HEAD);
   CK(ms::argmax_launch(c->part, s, Mo, D.vocab, want_logits ? c->logits : nullptr, c->next, c->hist,
-                       d_slot + final_row_begin, d_pos + final_row_begin, c->hist_len, c->compute));
+                       d_slot + final_row_begin, d_pos + final_row_begin, c->hist_len, c->compute, c->am_key,
+                       c->am_cnt));
   c->launches += 1;
   pk_mark(c, MS_PK_ARGMAX);
 }
@@ -730,6 +733,10 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
                                        sizeof(int)));
       CK(cudaMemset(c->attn_pcnt, 0, (size_t)std::max(desc->max_batch, desc->max_prefill_tokens) *
                                          desc->num_kv_heads * sizeof(int)));
+      CK(cudaMalloc(&c->am_key, (size_t)c->max_rows * sizeof(unsigned long long)));
+      CK(cudaMemset(c->am_key, 0, (size_t)c->max_rows * sizeof(unsigned long long)));
+      CK(cudaMalloc(&c->am_cnt, (size_t)c->max_rows * sizeof(int)));
+      CK(cudaMemset(c->am_cnt, 0, (size_t)c->max_rows * sizeof(int)));
       CK(cudaMalloc(&c->gang_ctr, kGangCounters * sizeof(uint32_t)));
       CK(cudaMemset(c->gang_ctr, 0, kGangCounters * sizeof(uint32_t)));
       c->gang_count.assign(kGangCounters, 0);
@@ -798,7 +805,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
-                 c->h, c->x, c->part, c->q, c->attn_ws, c->attn_pws, c->attn_pcnt, c->gang_ctr, c->next, c->logits, c->hist};
+                 c->h, c->x, c->part, c->q, c->attn_ws, c->attn_pws, c->attn_pcnt, c->gang_ctr, c->am_key, c->am_cnt, c->next, c->logits, c->hist};
   for (void* p : dev) cudaFree(p);
   cudaFreeHost(c->h_next);
   cudaFreeHost(c->h_logits);
