@@ -35,6 +35,24 @@ static int attn_env(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
+// CTA -> (kv_head, row, split, splits) under the whole/tail item map (AttnArgs).
+__device__ __forceinline__ void attn_item(const AttnArgs& a, int& kvh, int& row, int& split, int& ns) {
+  const int bid = blockIdx.x;
+  int item;
+  if (bid < a.whole_items) {
+    item = bid;
+    split = 0;
+    ns = 1;
+  } else {
+    const int j = bid - a.whole_items;
+    item = a.whole_items + j / a.tail_splits;
+    split = j % a.tail_splits;
+    ns = a.tail_splits;
+  }
+  row = item / a.KVH;
+  kvh = item - row * a.KVH;
+}
+
 // Sum of the first n split-K partial slots of one element (slot order fixed,
 // as elementwise.cu sum_slots: bit-identical to the unfused qkv_post path).
 __device__ __forceinline__ float attn_sum_slots(const float* p, size_t stride, int n) {
@@ -111,11 +129,12 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
 
   pdl_wait();
   pdl_trigger();
-  const int kvh = blockIdx.x, row = blockIdx.y, split = blockIdx.z;
+  int kvh, row, split, nsplit;
+  attn_item(a, kvh, row, split, nsplit);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ctx = a.ctx_len[row];
   const int nb = (ctx + BT - 1) / BT;
-  const int b0 = (int)((int64_t)nb * split / a.splits), b1 = (int)((int64_t)nb * (split + 1) / a.splits);
+  const int b0 = (int)((int64_t)nb * split / nsplit), b1 = (int)((int64_t)nb * (split + 1) / nsplit);
   const int prow = a.page_row ? a.page_row[row] : row;
   const int32_t* ptab = a.pages + (size_t)prow * a.page_stride;
   const int64_t kv_off = a.kv.layer_off(a.layer) + (int64_t)kvh * 2 * a.kv.head_bytes();
@@ -360,7 +379,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
       }
       const int h = kvh * G + g;
       const float o = L > 0.f ? O / L : 0.f;
-      if (a.splits == 1) {
+      if (nsplit == 1) {
         const int K = a.H * HD;
         const size_t off = a.out_packed ? act_off(row, h * HD + dim, K, a.TM) : (size_t)row * K + h * HD + dim;
         a.out[off] = f2bf(o);
@@ -381,11 +400,13 @@ __global__ void attn_combine_kernel(AttnArgs a) {
   pdl_wait();
   pdl_trigger();
   const int row = blockIdx.x, h = blockIdx.y, dim = threadIdx.x;
+  if (row * a.KVH + h / (a.H / a.KVH) < a.whole_items) return;  // written directly by its CTA
+  const int ns = a.tail_splits;
   float M = -INFINITY;
-  for (int s = 0; s < a.splits; ++s) M = fmaxf(M, a.part_ml[(((size_t)s * a.rows + row) * a.H + h) * 2]);
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, a.part_ml[(((size_t)s * a.rows + row) * a.H + h) * 2]);
   float L = 0.f, O = 0.f;
   if (M != -INFINITY) {
-    for (int s = 0; s < a.splits; ++s) {
+    for (int s = 0; s < ns; ++s) {
       const size_t base = ((size_t)s * a.rows + row) * a.H + h;
       const float ms_ = a.part_ml[base * 2], ls = a.part_ml[base * 2 + 1];
       if (ms_ == -INFINITY) continue;
@@ -450,11 +471,12 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
 
   pdl_wait();
   pdl_trigger();
-  const int kvh = blockIdx.x, row = blockIdx.y, split = blockIdx.z;
+  int kvh, row, split, nsplit;
+  attn_item(a, kvh, row, split, nsplit);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ctx = a.ctx_len[row];
   const int nb = (ctx + BT - 1) / BT;
-  const int b0 = (int)((int64_t)nb * split / a.splits), b1 = (int)((int64_t)nb * (split + 1) / a.splits);
+  const int b0 = (int)((int64_t)nb * split / nsplit), b1 = (int)((int64_t)nb * (split + 1) / nsplit);
   const int prow = a.page_row ? a.page_row[row] : row;
   const int32_t* ptab = a.pages + (size_t)prow * a.page_stride;
   const int64_t kv_off = a.kv.layer_off(a.layer) + (int64_t)kvh * 2 * a.kv.head_bytes();
@@ -614,7 +636,7 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
     }
     const int h = kvh * G + gg;
     const float ov = L > 0.f ? O / L : 0.f;
-    if (a.splits == 1) {
+    if (nsplit == 1) {
       const int K = a.H * HD;
       const size_t off = a.out_packed ? act_off(row, h * HD + dim, K, a.TM) : (size_t)row * K + h * HD + dim;
       a.out[off] = f2bf(ov);
@@ -677,9 +699,10 @@ static cudaError_t launch_gqa(const AttnArgs& a_in, cudaStream_t stream) {
     cudaFuncSetAttribute(attn_gqa_mma_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  dim3 grid(a.KVH, a.rows, a.splits);
-  cudaError_t e = launch_pdl(attn_gqa_mma_kernel<G>, grid, dim3(160), smem, stream, a, tmap);
-  if (e != cudaSuccess || a.splits == 1) return e;
+  attn_item_map(a, attn_gqa_mma_kernel<G>, smem);
+  const int ctas = a.whole_items + (a.rows * a.KVH - a.whole_items) * a.tail_splits;
+  cudaError_t e = launch_pdl(attn_gqa_mma_kernel<G>, dim3(ctas), dim3(160), smem, stream, a, tmap);
+  if (e != cudaSuccess || a.whole_items == a.rows * a.KVH) return e;
   return launch_pdl(attn_combine_kernel<128>, dim3(a.rows, a.H), dim3(128), 0, stream, a);
 }
 
@@ -1025,6 +1048,45 @@ static cudaError_t launch_persist(const AttnArgs& a_in, cudaStream_t stream) {
   return launch_pdl(attn_persist_kernel<HD, G, BT>, dim3(a.ctas), dim3(160), smem, stream, a);
 }
 
+// Item map for a launch of `kernel`: whole items fill full waves of the
+// occupancy-limited grid; the remaining (tail) items are split so the last
+// wave is made of short CTAs.  Uniform split-KV (a.splits > 1) is kept as is.
+template <typename K>
+static void attn_item_map(AttnArgs& a, K kernel, size_t smem) {
+  const int items = a.rows * a.KVH;
+  a.whole_items = items;
+  a.tail_splits = 1;
+  if (a.splits > 1) {
+    a.whole_items = 0;
+    a.tail_splits = a.splits;
+    return;
+  }
+  static const bool on = attn_env("MS_ATTN_TAILSPLIT", 0) != 0;  // measured slower on the 7B step: off
+  if (!on || a.part_o == nullptr || a.part_ml == nullptr || a.ws_splits_max < 2) return;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 160, smem) != cudaSuccess || per_sm < 1) return;
+  const int slots = sms * per_sm;
+  const int full = items / slots * slots, tail = items - full;
+  if (full == 0 || tail == 0) return;
+  // splits t minimising the tail's length in item-times: ceil(tail * t / slots) / t
+  int best_t = 1;
+  double best = 1.0;
+  for (int t = 2; t <= a.ws_splits_max; ++t) {
+    if (a.max_blocks_hint > 0 && a.max_blocks_hint / t < 4) break;  // >= 4 blocks per piece
+    const double len = (double)((tail * t + slots - 1) / slots) / t;
+    if (len < best - 1e-9) {
+      best = len;
+      best_t = t;
+    }
+  }
+  if (best_t > 1) {
+    a.whole_items = full;
+    a.tail_splits = best_t;
+  }
+}
+
 template <int HD, int G>
 static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
   constexpr int BT = 16;
@@ -1047,9 +1109,10 @@ static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
     cudaFuncSetAttribute(attn_decode_kernel<HD, G, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  dim3 grid(a.KVH, a.rows, a.splits);
-  cudaError_t e = launch_pdl(attn_decode_kernel<HD, G, BT>, grid, dim3(160), smem, stream, a);
-  if (e != cudaSuccess || a.splits == 1) return e;
+  attn_item_map(a, attn_decode_kernel<HD, G, BT>, smem);
+  const int ctas = a.whole_items + (a.rows * a.KVH - a.whole_items) * a.tail_splits;
+  cudaError_t e = launch_pdl(attn_decode_kernel<HD, G, BT>, dim3(ctas), dim3(160), smem, stream, a);
+  if (e != cudaSuccess || a.whole_items == a.rows * a.KVH) return e;
   return launch_pdl(attn_combine_kernel<HD>, dim3(a.rows, a.H), dim3(HD), 0, stream, a);
 }
 

@@ -147,6 +147,14 @@ struct AttnArgs {
   int* pcnt;                // [rows * KVH] arrival counters, zero between launches (self-resetting)
   int ctas;                 // persistent grid size (set by attn_decode_launch)
   int64_t arena_bytes;      // size of kv.arena (GQA tensor-core path: TMA tensor map over the arena)
+  // CTA -> work item map (set by attn_decode_launch): items (row, kv_head) are
+  // numbered row * KVH + kv_head; the first `whole_items` run as one CTA each,
+  // every later item is split over `tail_splits` CTAs (merged by the combine
+  // kernel) so the last wave of equal-sized items does not leave SMs idle.
+  int whole_items;
+  int tail_splits;
+  int ws_splits_max;        // splits the part_o / part_ml workspace can hold (tail splitting needs >= 2)
+  int max_blocks_hint;      // blocks of the longest row (tail pieces keep >= 4 blocks)
 };
 // Persistent-grid size and workspace floats the stream-K decode attention needs.
 int attn_persist_ctas(int num_sms);

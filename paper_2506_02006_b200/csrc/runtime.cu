@@ -536,7 +536,10 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
       a.splits = asplits;
       a.part_o = c->attn_ws;
-      a.part_ml = c->attn_ws + (size_t)asplits * M * H * hd;
+      // workspace laid out for up to 16 splits (uniform split-KV or tail splitting)
+      a.part_ml = c->attn_ws + (size_t)16 * M * H * hd;
+      a.ws_splits_max = 16;
+      a.max_blocks_hint = (max_ctx + 15) / 16;
       if (fuse_qkv) {
         a.qkv_part = c->part;
         a.qkv_plan = s;
@@ -1398,6 +1401,7 @@ int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int 
     a.splits = splits < 1 ? 1 : splits;
     a.part_o = workspace;
     a.part_ml = workspace ? workspace + (size_t)a.splits * rows * H * hd : nullptr;
+    a.ws_splits_max = a.splits;
     a.out = out;
     a.out_packed = 0;
     a.TM = 16;
