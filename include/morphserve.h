@@ -134,6 +134,13 @@ int ms_decode_step(ms_ctx* ctx, const ms_decode_batch* batch, int32_t* next_out,
  * preemption); next token -> hist[slot][n_tokens] and *next_out. */
 int ms_prefill(ms_ctx* ctx, int32_t slot, int32_t n_tokens, const int64_t* block_ids, int32_t n_blocks,
                int32_t* next_out, float* logits_out);
+/* ms_prefill with the residual stream captured for the offline layer profiler
+ * (the GPU restatement of profiler.cpp's activation trace,
+ * proj/src/profiler.cpp:41-54 / toy_model.cpp forward): h_out (host) receives
+ * [num_layers + 1][n_tokens][hidden] fp32 -- the input of every layer, then the
+ * output of the last one (before the final norm).  logits_out as ms_prefill. */
+int ms_prefill_trace(ms_ctx* ctx, int32_t slot, int32_t n_tokens, const int64_t* block_ids, int32_t n_blocks,
+                     float* h_out, float* logits_out);
 /* Step timing: CUDA events around the last ms_decode_step / ms_prefill. */
 int ms_last_step_ms(ms_ctx* ctx, float* ms);
 /* Fill the listed blocks' KV with synthetic values (bench: "prefilled" context). */

@@ -80,6 +80,8 @@ def lib():
         L.ref_forward.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), i32p, C.c_int, C.c_void_p, i32p]
         L.ref_prefill.argtypes = [C.c_void_p, C.c_void_p, i32p, C.c_int, C.c_void_p]
         L.ref_prefill.restype = C.c_int32
+        L.ref_prefill_trace.argtypes = [C.c_void_p, C.c_void_p, i32p, C.c_int, C.c_void_p, C.c_void_p]
+        L.ref_prefill_trace.restype = C.c_int32
         L.ref_num_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -243,9 +245,73 @@ class RefModel:
                           logits.ctypes.data_as(C.c_void_p) if want_logits else None, nxt)
         return nxt, logits
 
+    def prefill_trace(self, s, tokens):
+        """Prefill returning the residual stream entering each layer and leaving
+        the last one: [L+1, n, d] fp32 (oracle of ms_prefill_trace)."""
+        toks = np.ascontiguousarray(tokens, np.int32)
+        tr = np.empty((self.cfg["L"] + 1, len(toks), self.cfg["d"]), np.float32)
+        lib().ref_prefill_trace(self.h, s, toks, len(toks), None, tr.ctypes.data_as(C.c_void_p))
+        return tr
+
     def prefill(self, s, tokens, want_logits: bool = True):
         toks = np.ascontiguousarray(tokens, np.int32)
         logits = np.empty(self.cfg["V"], np.float32) if want_logits else None
         nxt = lib().ref_prefill(self.h, s, toks, len(toks),
                                 logits.ctypes.data_as(C.c_void_p) if want_logits else None)
         return int(nxt), logits
+
+
+# ------------------------------------------------------- layer profiler oracle
+def _cos64(a, b) -> float:
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    na, nb = np.linalg.norm(a), np.linalg.norm(b)
+    if na == 0.0 or nb == 0.0:
+        return 1.0 if na == nb else 0.0
+    return float(np.dot(a, b) / (na * nb))
+
+
+def lis_greedy(cfg: dict, seed: int, prompts, bits: int = 4, weights=None) -> dict:
+    """CPU restatement of the layer-importance profile (reference
+    proj/src/profiler.cpp:41-139: LTS, LRS, MDS, greedy argmax with ties to the
+    lowest index) over the Llama-style oracle model; the oracle of
+    paper_2506_02006_b200.profiler.GpuProfiler.greedy_sequence."""
+    w = {"alpha1": 0.25, "alpha2": 0.25, "beta": 0.5}
+    w.update(weights or {})
+    m = RefModel(cfg, seed)
+    L = cfg["L"]
+    try:
+        def traces(q):
+            for l in range(L):
+                m.set_precision(l, bits if l in q else 16)
+            out = []
+            for p in prompts:
+                s = m.new_seq(len(p) + 1)
+                out.append(m.prefill_trace(s, p))
+            return out
+        full = traces(set())
+        lts = [float(np.mean([_cos64(h[p + 1], h[p]) for h in full])) for p in range(L)]
+        lrs = []
+        for p in range(L):
+            qt = traces({p})
+            lrs.append(float(np.mean([_cos64(f[p + 1], q[p + 1]) for f, q in zip(full, qt)])))
+        quant, order, per_step = set(), [], []
+        base = [h[L] for h in full]
+        for _ in range(L):
+            best, best_score, best_final = -1, -np.inf, None
+            for j in range(L):
+                if j in quant:
+                    continue
+                cand = [h[L] for h in traces(quant | {j})]
+                mds = float(np.mean([_cos64(b, c) for b, c in zip(base, cand)]))
+                lis = w["alpha1"] * lts[j] + w["alpha2"] * lrs[j] + w["beta"] * mds
+                if lis > best_score:
+                    best, best_score, best_final = j, lis, cand
+            order.append(best)
+            per_step.append(best_score)
+            quant.add(best)
+            base = best_final
+        return {"order": order, "per_step_lis": per_step, "bits": bits, "kind": "lis_greedy", "weights": w,
+                "lts": lts, "lrs": lrs}
+    finally:
+        m.close()

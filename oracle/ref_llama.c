@@ -409,8 +409,19 @@ static inline float silu(float x) { return x / (1.0f + expf(-x)); }
  * seqs[b]->len; its K/V are appended; logits[b][V] (may be NULL) and
  * next[b] = argmax are returned.  This is also the prefill math: a prefill of
  * n tokens is n such positions (causal attention makes them identical). */
+static void forward_impl(ref_model* m, ref_seq** seqs, const int32_t* tokens, int B, float* logits,
+                         int32_t* next, float* trace, int64_t trace_layer_stride);
+
 void ref_forward(ref_model* m, ref_seq** seqs, const int32_t* tokens, int B, float* logits,
                  int32_t* next) {
+  forward_impl(m, seqs, tokens, B, logits, next, NULL, 0);
+}
+
+/* trace (optional): the residual stream [B][d] entering layer l is written at
+ * trace + l * trace_layer_stride, the one leaving the last layer at L * stride
+ * (the activation trace of the layer profiler, profiler.cpp:41-103). */
+static void forward_impl(ref_model* m, ref_seq** seqs, const int32_t* tokens, int B, float* logits,
+                         int32_t* next, float* trace, int64_t trace_layer_stride) {
   const ref_cfg* c = &m->c;
   const int d = c->d, hd = c->hd, H = c->H, KVH = c->KVH, half = hd / 2;
   const int qkv_n = (H + 2 * KVH) * hd;
@@ -424,6 +435,7 @@ void ref_forward(ref_model* m, ref_seq** seqs, const int32_t* tokens, int B, flo
     for (int i = 0; i < d; ++i) h[(int64_t)b * d + i] = bf2f(m->embed[(int64_t)tokens[b] * d + i]);
 
   for (int l = 0; l < c->L; ++l) {
+    if (trace) memcpy(trace + (int64_t)l * trace_layer_stride, h, (size_t)B * d * sizeof(float));
     ref_rmsnorm(h, m->norm1[l], B, d, c->eps, xn);
     ref_gemm_bf16(m->wqkv[l], xn, B, qkv_n, d, y);
     for (int b = 0; b < B; ++b) {
@@ -455,6 +467,7 @@ void ref_forward(ref_model* m, ref_seq** seqs, const int32_t* tokens, int B, flo
     ref_gemm_bf16(m->wd[l], xn, B, d, c->ffn, y);
     for (int64_t i = 0; i < (int64_t)B * d; ++i) h[i] = h[i] + y[i];
   }
+  if (trace) memcpy(trace + (int64_t)c->L * trace_layer_stride, h, (size_t)B * d * sizeof(float));
   for (int b = 0; b < B; ++b) seqs[b]->len += 1;
   ref_rmsnorm(h, m->normf, B, d, c->eps, xn);
   float* lg = logits ? logits : y;
@@ -474,6 +487,16 @@ void ref_forward(ref_model* m, ref_seq** seqs, const int32_t* tokens, int B, flo
 int32_t ref_prefill(ref_model* m, ref_seq* s, const int32_t* tokens, int n, float* logits) {
   int32_t nxt = -1;
   for (int i = 0; i < n; ++i) ref_forward(m, &s, tokens + i, 1, (i == n - 1) ? logits : NULL, &nxt);
+  return nxt;
+}
+
+/* Prefill with the per-layer residual stream: trace [L+1][n][d] (the GPU
+ * counterpart is ms_prefill_trace). */
+int32_t ref_prefill_trace(ref_model* m, ref_seq* s, const int32_t* tokens, int n, float* logits, float* trace) {
+  int32_t nxt = -1;
+  for (int i = 0; i < n; ++i)
+    forward_impl(m, &s, tokens + i, 1, (i == n - 1) ? logits : NULL, &nxt, trace + (int64_t)i * m->c.d,
+                 (int64_t)n * m->c.d);
   return nxt;
 }
 

@@ -77,6 +77,8 @@ SIGNATURES = [
     ("ms_decode_step", C.c_int, [_P, C.POINTER(DecodeBatch), C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
     ("ms_prefill", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.c_int32,
                              C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
+    ("ms_prefill_trace", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.c_int32,
+                                   C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     ("ms_last_step_ms", C.c_int, [_P, C.POINTER(C.c_float)]),
     ("ms_kv_fill_synthetic", C.c_int, [_P, C.POINTER(C.c_int64), C.c_int64, C.c_uint64]),
     ("ms_launch_count", C.c_int64, [_P]),

@@ -185,6 +185,9 @@ struct ms_ctx {
   int* am_cnt = nullptr;                 // wide argmax: per-row arrival counter (self-resetting)
   std::vector<uint64_t> gang_count;      // host mirror: arrivals so far per counter
   int gang_next = 0;
+  float* trace_h = nullptr;  // ms_prefill_trace: device [L+1][n][d] residual stream snapshots (lazy)
+  size_t trace_elems = 0;
+  bool tracing = false;
   int64_t tl_counter = 0;
   float* attn_pws = nullptr;   // persistent attention partials
   int* attn_pcnt = nullptr;    // persistent attention item counters [max_batch * KVH]
@@ -491,6 +494,9 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   pk_mark(c, MS_PK_EMBED);
   const int asplits = attn_splits(c, M, max_ctx);
   for (int l = 0; l < D.num_layers; ++l) {
+    if (c->tracing)  // residual stream entering layer l
+      CK(cudaMemcpyAsync(c->trace_h + (size_t)l * M * d, c->h, (size_t)M * d * sizeof(float), cudaMemcpyDeviceToDevice,
+                         c->compute));
     const bool w4 = c->layers[l].bits == 4;
     const int skip = skip_mask();
     ms::GemmPlanDev s = (skip & 16) ? ms::gemm_plan(1024, 1024, M, TM, false, c->num_sms, c->part_elems)
@@ -592,6 +598,9 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       pk_mark(c, MS_PK_NORM);
     }
   }
+  if (c->tracing)  // after the last layer (before the final norm)
+    CK(cudaMemcpyAsync(c->trace_h + (size_t)D.num_layers * M * d, c->h, (size_t)M * d * sizeof(float),
+                       cudaMemcpyDeviceToDevice, c->compute));
   const int Mo = M - final_row_begin;
   const int TMo = round16(Mo) > 256 ? 256 : round16(Mo);
   ms::GemmWeights lw{c->lm_table, 0, (int64_t)1 << 40, D.vocab, d};
@@ -803,6 +812,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   }
   for (auto e : c->events) cudaEventDestroy(e);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
+  if (c->trace_h) cudaFree(c->trace_h);
   if (c->tm0) cudaEventDestroy(c->tm0);
   if (c->tm1) cudaEventDestroy(c->tm1);
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
@@ -1233,6 +1243,28 @@ int ms_prefill(ms_ctx* c, int32_t slot, int32_t n_tokens, const int64_t* block_i
       if (next_out) *next_out = c->h_next[0];
       if (logits_out) std::memcpy(logits_out, c->h_logits, (size_t)c->desc.vocab * 4);
     }
+  });
+}
+
+int ms_prefill_trace(ms_ctx* c, int32_t slot, int32_t n_tokens, const int64_t* block_ids, int32_t n_blocks,
+                     float* h_out, float* logits_out) {
+  return guard([&] {
+    if (!h_out) fail(MS_EVALIDATION, "prefill_trace: h_out is required");
+    const size_t need = (size_t)(c->desc.num_layers + 1) * n_tokens * c->desc.hidden;
+    if (n_tokens < 1 || n_tokens > c->desc.max_prefill_tokens) fail(MS_EVALIDATION, "prefill length out of range");
+    CK(cudaSetDevice(c->device));
+    if (c->trace_elems < need) {
+      if (c->trace_h) CK(cudaFree(c->trace_h));
+      CK(cudaMalloc(&c->trace_h, need * sizeof(float)));
+      c->trace_elems = need;
+    }
+    c->tracing = true;
+    const int rc = ms_prefill(c, slot, n_tokens, block_ids, n_blocks, nullptr, logits_out);
+    c->tracing = false;
+    if (rc != MS_OK) fail(rc, ms_last_error());
+    // on the compute stream: a plain cudaMemcpy would not wait for the (non-blocking) compute stream
+    CK(cudaMemcpyAsync(h_out, c->trace_h, need * sizeof(float), cudaMemcpyDeviceToHost, c->compute));
+    CK(cudaStreamSynchronize(c->compute));
   });
 }
 

@@ -160,6 +160,15 @@ class DeviceModel:
                                     N.f32p(logits)))
         return nxt.value, logits
 
+    def prefill_trace(self, slot: int, n_tokens: int, block_ids, want_logits: bool = True):
+        """Prefill that also returns the residual stream entering every layer and
+        leaving the last one: ([L+1, n, d] fp32, last-token logits)."""
+        ids = np.ascontiguousarray(block_ids, np.int64)
+        h = np.empty((self.shape["L"] + 1, n_tokens, self.shape["d"]), np.float32)
+        logits = np.empty(self.shape["V"], np.float32) if want_logits else None
+        N.check(self.lib.ms_prefill_trace(self.h, slot, n_tokens, N.i64p(ids), ids.size, N.f32p(h), N.f32p(logits)))
+        return h, logits
+
     def decode(self, slots, positions, block_table, tokens=None, want_next: bool = True,
                want_logits: bool = False):
         slots = np.ascontiguousarray(slots, np.int32)
