@@ -13,6 +13,7 @@
 //   MorphState::complete_swap        proj/src/engine.cpp:30-38      -> ms_swap_commit (pointer flip)
 //   KvBlockPool::attach/detach       proj/src/kv_pool.cpp:77-100    -> ms_kv_attach / ms_kv_detach
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -185,6 +186,17 @@ struct ms_ctx {
   int* am_cnt = nullptr;                 // wide argmax: per-row arrival counter (self-resetting)
   std::vector<uint64_t> gang_count;      // host mirror: arrivals so far per counter
   int gang_next = 0;
+  // decode-step CUDA graphs (MS_GRAPH=1): keyed by staging slot / batch shape, dropped when
+  // anything baked into the kernel parameters changes (layer tables, arena mappings)
+  struct StepGraph {
+    const int32_t* st_d;
+    int n, mb, asplits, want_logits, has_tokens;
+    int64_t launches;
+    cudaGraphExec_t exec;
+  };
+  std::vector<StepGraph> graphs;
+  std::vector<std::array<int64_t, 5>> graph_seen;  // shapes seen once (captured on the second sighting)
+  uint64_t graph_gen = 0, graph_gen_built = 0;
   float* trace_h = nullptr;  // ms_prefill_trace: device [L+1][n][d] residual stream snapshots (lazy)
   size_t trace_elems = 0;
   bool tracing = false;
@@ -448,6 +460,23 @@ void prof_mark(ms_ctx* c) {
 
 // MS_ATTN_PERSIST=1 (experiments): persistent stream-K decode attention
 // instead of one CTA per (kv_head, row, split).
+// Decode steps replay from captured CUDA graphs (MS_GRAPH=0 disables): a shape
+// is captured the second time it is seen, at most kMaxGraphs are kept.
+constexpr size_t kMaxGraphs = 64;
+bool graphs_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("MS_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+void drop_graphs(ms_ctx* c) {
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+  c->graph_seen.clear();
+}
+
 bool attn_persistent() {
   static const bool v = [] {
     const char* e = std::getenv("MS_ATTN_PERSIST");
@@ -811,6 +840,7 @@ int ms_ctx_destroy(ms_ctx* c) {
     if (st.used) cudaEventDestroy(st.used);
   }
   for (auto e : c->events) cudaEventDestroy(e);
+  drop_graphs(c);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   if (c->trace_h) cudaFree(c->trace_h);
   if (c->tm0) cudaEventDestroy(c->tm0);
@@ -930,6 +960,7 @@ void finalize_weights(ms_ctx* c, bool synthetic, uint64_t seed) {
 
 int ms_weights_synthetic(ms_ctx* c, uint64_t seed) {
   return guard([&] {
+    c->graph_gen++;
     CK(cudaSetDevice(c->device));
     finalize_weights(c, true, seed);
   });
@@ -949,6 +980,7 @@ int ms_weights_upload(ms_ctx* c, int layer, int which, const uint16_t* host_bf16
 
 int ms_weights_finalize(ms_ctx* c) {
   return guard([&] {
+    c->graph_gen++;
     CK(cudaSetDevice(c->device));
     finalize_weights(c, false, 0);
   });
@@ -1029,6 +1061,7 @@ int ms_swap_wait(ms_ctx* c, uint64_t ticket, float* upload_ms) {
 
 int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
   return guard([&] {
+    c->graph_gen++;  // layer table changes: captured steps are stale
     Layer& L = ticket_layer(c, ticket);
     CK(cudaSetDevice(c->device));
     // Token-boundary flip: steps launched from now on use the new image; the
@@ -1049,6 +1082,7 @@ int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
 
 int ms_reset_state(ms_ctx* c) {
   return guard([&] {
+    c->graph_gen++;
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->compute));
     CK(cudaStreamSynchronize(c->copy));
@@ -1112,6 +1146,7 @@ int64_t ms_kv_page_of(ms_ctx* c, int64_t id) {
 // ------------------------------------------------------------ token history
 int ms_hist_reserve(ms_ctx* c, int32_t slots, int32_t max_len) {
   return guard([&] {
+    c->graph_gen++;  // the token history is re-allocated
     if (slots < 1 || max_len < 2) fail(MS_EVALIDATION, "bad history shape");
     if (max_len > c->desc.max_pos + 1) fail(MS_EVALIDATION, "history longer than max_pos");
     CK(cudaStreamSynchronize(c->compute));
@@ -1192,7 +1227,52 @@ int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float
       c->launches += 1;
     }
     const int TM = std::min(256, round16(n));
-    forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, logits_out != nullptr);
+    if (graphs_enabled() && !c->prof_attn && !c->prof_all && !c->tracing) {
+      if (c->graph_gen != c->graph_gen_built) {
+        drop_graphs(c);
+        c->graph_gen_built = c->graph_gen;
+      }
+      const int asplits = attn_splits(c, n, max_ctx);
+      const int wl = logits_out != nullptr;
+      ms_ctx::StepGraph* g = nullptr;
+      for (auto& x : c->graphs)
+        if (x.st_d == st.d && x.n == n && x.mb == mb && x.asplits == asplits && x.want_logits == wl &&
+            x.has_tokens == 0)
+          g = &x;
+      bool capture = false;
+      if (!g) {
+        const std::array<int64_t, 5> key{(int64_t)st.d, n, mb, asplits, wl};
+        auto it = std::find(c->graph_seen.begin(), c->graph_seen.end(), key);
+        if (it == c->graph_seen.end()) {
+          if (c->graph_seen.size() >= 4 * kMaxGraphs) c->graph_seen.clear();
+          c->graph_seen.push_back(key);
+        } else {
+          capture = true;
+          if (c->graphs.size() >= kMaxGraphs) drop_graphs(c);
+        }
+      }
+      if (!g && !capture) {
+        forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, wl != 0);
+      } else if (!g) {  // capture the forward once for this shape / staging slot
+        cudaGraph_t graph;
+        const int64_t l0 = c->launches;
+        CK(cudaStreamBeginCapture(c->compute, cudaStreamCaptureModeThreadLocal));
+        forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, wl != 0);
+        CK(cudaStreamEndCapture(c->compute, &graph));
+        cudaGraphExec_t exec;
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        c->graphs.push_back({st.d, n, mb, asplits, wl, 0, c->launches - l0, exec});
+        c->launches = l0;
+        g = &c->graphs.back();
+      }
+      if (g) {
+        CK(cudaGraphLaunch(g->exec, c->compute));
+        c->launches += g->launches;
+      }
+    } else {
+      forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, logits_out != nullptr);
+    }
     CK(cudaEventRecord(c->ev_step1, c->compute));
     if (next_out || logits_out) {
       if (next_out) CK(cudaMemcpyAsync(c->h_next, c->next, (size_t)n * 4, cudaMemcpyDeviceToHost, c->compute));
