@@ -341,18 +341,27 @@ def run_ours(args):
         swaps += dn
     t_noswap, t_swap = float(np.median(t_a)), float(np.median(t_b))
     stall_ms_per_token = max(0.0, t_swap - t_noswap) / (nsw * BATCH)
-    # ---- e2e through the C ABI with host buffers: H2D of the step inputs
-    # (tokens, slots, positions, block table) and D2H of the next tokens.
-    tokens = np.zeros(BATCH, np.int32)
+    # ---- e2e through the C ABI with host buffers: every step stages its inputs
+    # (slots, positions, block table) from pinned host memory and its next
+    # tokens are read back to the host; the engine-style pipelined form keeps
+    # one step in flight while the previous step's tokens are collected.
     barrier()
     dev.sync()
     t0 = time.perf_counter()
+    inflight = 0
     for _ in range(args.e2e_steps):
-        tokens, _ = dev.decode(slots, pos, table, tokens=tokens, want_next=True)
+        dev.decode_submit(slots, pos, table)
         pos = pos + 1
+        inflight += 1
+        if inflight == 2:
+            tokens = dev.decode_collect()
+            inflight -= 1
+    while inflight:
+        tokens = dev.decode_collect()
+        inflight -= 1
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     max_blocks = dev.max_blocks
-    h2d = BATCH * (4 + max_blocks) * 4
+    h2d = BATCH * (4 + max_blocks) * 4  # staged per step: slot, pos, ctx, token + block-table row per sequence
     d2h = BATCH * 4
     # ---- serving: bursty Gamma trace through the engine, measured GPU clock
     serving = None
@@ -422,7 +431,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serve-seconds", type=float, default=8.0, help="bursty serving trace length (0 = skip)")

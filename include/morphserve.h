@@ -129,6 +129,14 @@ typedef struct {
   int32_t max_blocks;
 } ms_decode_batch;
 int ms_decode_step(ms_ctx* ctx, const ms_decode_batch* batch, int32_t* next_out, float* logits_out);
+/* Pipelined form of ms_decode_step: submit enqueues the step (its inputs are
+ * staged at once, its next tokens copied back asynchronously) and returns; the
+ * host may run one step ahead.  collect waits for the OLDEST submitted step and
+ * returns its n next tokens.  At most 2 steps may be uncollected (status 2
+ * otherwise).  Tokens also land in the device history, so a submitted step
+ * can feed the next one without a host round trip. */
+int ms_decode_submit(ms_ctx* ctx, const ms_decode_batch* batch);
+int ms_decode_collect(ms_ctx* ctx, int32_t* next_out, int32_t* n_out);
 /* Single-request prefill of hist[slot][0:n_tokens) (replaces
  * tokens * prefill_ms_per_token at engine.cpp:477-478, incl. re-prefill after
  * preemption); next token -> hist[slot][n_tokens] and *next_out. */

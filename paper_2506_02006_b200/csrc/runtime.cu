@@ -138,6 +138,10 @@ struct Staging {  // one slot of the per-step H2D ring
   int32_t* h = nullptr;   // pinned, mapped
   int32_t* hd = nullptr;  // device alias of h (zero-copy)
   int32_t* d = nullptr;   // device
+  int32_t* next_h = nullptr;  // pinned: next tokens of a submitted (not yet collected) decode step
+  cudaEvent_t done = nullptr;
+  int next_n = 0;
+  bool pending = false;
   size_t words = 0;
   cudaEvent_t used = nullptr;
   bool armed = false;
@@ -186,6 +190,7 @@ struct ms_ctx {
   int* am_cnt = nullptr;                 // wide argmax: per-row arrival counter (self-resetting)
   std::vector<uint64_t> gang_count;      // host mirror: arrivals so far per counter
   int gang_next = 0;
+  std::vector<int> submitted;  // ring slots of submitted decode steps, oldest first
   // decode-step CUDA graphs (MS_GRAPH=1): keyed by staging slot / batch shape, dropped when
   // anything baked into the kernel parameters changes (layer tables, arena mappings)
   struct StepGraph {
@@ -836,6 +841,8 @@ int ms_ctx_destroy(ms_ctx* c) {
   for (auto* p : c->raw) cudaFree(p);
   for (auto& st : c->ring) {
     cudaFreeHost(st.h);
+    if (st.next_h) cudaFreeHost(st.next_h);
+    if (st.done) cudaEventDestroy(st.done);
     cudaFree(st.d);
     if (st.used) cudaEventDestroy(st.used);
   }
@@ -1186,8 +1193,9 @@ int ms_hist_read(ms_ctx* c, int32_t slot, int32_t offset, int32_t* host_out, int
 }
 
 // -------------------------------------------------------------------- steps
-int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float* logits_out) {
-  return guard([&] {
+namespace {
+// Enqueue one decode step; returns the staging slot used.
+int decode_enqueue(ms_ctx* c, const ms_decode_batch* b, bool want_logits) {
     check_ready(c);
     const int n = b->n;
     if (n < 1 || n > c->desc.max_batch) fail(MS_EVALIDATION, "decode batch size out of range");
@@ -1233,7 +1241,7 @@ int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float
         c->graph_gen_built = c->graph_gen;
       }
       const int asplits = attn_splits(c, n, max_ctx);
-      const int wl = logits_out != nullptr;
+      const int wl = want_logits;
       ms_ctx::StepGraph* g = nullptr;
       for (auto& x : c->graphs)
         if (x.st_d == st.d && x.n == n && x.mb == mb && x.asplits == asplits && x.want_logits == wl &&
@@ -1271,9 +1279,17 @@ int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float
         c->launches += g->launches;
       }
     } else {
-      forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, logits_out != nullptr);
+      forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, want_logits);
     }
     CK(cudaEventRecord(c->ev_step1, c->compute));
+    return (int)(&st - c->ring);
+}
+}  // namespace
+
+int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float* logits_out) {
+  return guard([&] {
+    const int n = b->n;
+    decode_enqueue(c, b, logits_out != nullptr);
     if (next_out || logits_out) {
       if (next_out) CK(cudaMemcpyAsync(c->h_next, c->next, (size_t)n * 4, cudaMemcpyDeviceToHost, c->compute));
       if (logits_out)
@@ -1283,6 +1299,36 @@ int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float
       if (next_out) std::memcpy(next_out, c->h_next, (size_t)n * 4);
       if (logits_out) std::memcpy(logits_out, c->h_logits, (size_t)n * c->desc.vocab * 4);
     }
+  });
+}
+
+int ms_decode_submit(ms_ctx* c, const ms_decode_batch* b) {
+  return guard([&] {
+    if ((int)c->submitted.size() >= kRing - 1 || c->ring[c->ring_i].pending)
+      fail(MS_EVALIDATION, "decode_submit: collect the oldest step first (at most 2 in flight)");
+    const int i = decode_enqueue(c, b, false);
+    Staging& st = c->ring[i];
+    if (!st.next_h) {
+      CK(cudaHostAlloc(&st.next_h, (size_t)c->max_rows * sizeof(int32_t), cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
+    }
+    CK(cudaMemcpyAsync(st.next_h, c->next, (size_t)b->n * 4, cudaMemcpyDeviceToHost, c->compute));
+    CK(cudaEventRecord(st.done, c->compute));
+    st.next_n = b->n;
+    st.pending = true;
+    c->submitted.push_back(i);
+  });
+}
+
+int ms_decode_collect(ms_ctx* c, int32_t* next_out, int32_t* n_out) {
+  return guard([&] {
+    if (c->submitted.empty()) fail(MS_EVALIDATION, "decode_collect: no submitted step");
+    Staging& st = c->ring[c->submitted.front()];
+    c->submitted.erase(c->submitted.begin());
+    CK(cudaEventSynchronize(st.done));
+    if (next_out) std::memcpy(next_out, st.next_h, (size_t)st.next_n * 4);
+    if (n_out) *n_out = st.next_n;
+    st.pending = false;
   });
 }
 

@@ -182,6 +182,22 @@ class DeviceModel:
         N.check(self.lib.ms_decode_step(self.h, C.byref(b), N.i32p(nxt), N.f32p(logits)))
         return nxt, logits
 
+    def decode_submit(self, slots, positions, block_table, tokens=None):
+        """Enqueue a decode step (ms_decode_submit); collect its tokens later."""
+        slots = np.ascontiguousarray(slots, np.int32)
+        pos = np.ascontiguousarray(positions, np.int32)
+        bt = np.ascontiguousarray(block_table, np.int64)
+        tok = np.ascontiguousarray(tokens, np.int32) if tokens is not None else None
+        b = N.DecodeBatch(slots.size, N.i32p(slots), N.i32p(pos), N.i32p(tok), N.i64p(bt), bt.shape[1])
+        N.check(self.lib.ms_decode_submit(self.h, C.byref(b)))
+
+    def decode_collect(self) -> np.ndarray:
+        """Next tokens of the oldest submitted step (waits for it)."""
+        out = np.empty(self.desc.max_batch, np.int32)
+        n = C.c_int32()
+        N.check(self.lib.ms_decode_collect(self.h, N.i32p(out), C.byref(n)))
+        return out[: n.value].copy()
+
     def last_step_ms(self) -> float:
         ms = C.c_float()
         N.check(self.lib.ms_last_step_ms(self.h, C.byref(ms)))

@@ -108,3 +108,41 @@ def test_tiny_decode_matches_oracle(dev):
     h = dev.hist_read(0, 0, P + steps + 1)
     assert np.array_equal(h[:P], prompts[0])
     ref.close()
+
+
+def test_pipelined_decode_matches_synchronous(dev):
+    """ms_decode_submit / ms_decode_collect (one step in flight) produce the
+    same tokens as ms_decode_step on the same inputs."""
+    table = np.arange(200, 216, dtype=np.int64).reshape(2, 8)
+    dev.kv_attach(200, 16)
+    try:
+        prompts = (np.arange(2 * 20, dtype=np.int32).reshape(2, 20) * 31) % TINY["V"]
+        dev.hist_reserve(2, 128)
+        for b in range(2):
+            dev.hist_write(b, 0, prompts[b])
+            dev.prefill(b, 20, table[b])
+        pos = np.full(2, 20, np.int32)
+        sync = []
+        for _ in range(5):
+            t, _ = dev.decode(np.arange(2), pos, table)
+            sync.append(t)
+            pos = pos + 1
+        # replay the same positions pipelined (history rewritten by the same tokens)
+        for b in range(2):
+            dev.hist_write(b, 0, prompts[b])
+            dev.prefill(b, 20, table[b])
+        pos = np.full(2, 20, np.int32)
+        got, inflight = [], 0
+        for _ in range(5):
+            dev.decode_submit(np.arange(2), pos, table)
+            pos = pos + 1
+            inflight += 1
+            if inflight == 2:
+                got.append(dev.decode_collect())
+                inflight -= 1
+        while inflight:
+            got.append(dev.decode_collect())
+            inflight -= 1
+        assert all(np.array_equal(a, b) for a, b in zip(sync, got))
+    finally:
+        dev.kv_detach(list(range(200, 216)))
