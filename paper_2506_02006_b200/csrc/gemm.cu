@@ -925,12 +925,12 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   if (epi.op != kEpiNone) gemm_tail_gang(epi, plan, M, N, out, smem);
 }
 
-// Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 2: measured fastest).
+// Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 3: fastest in the 7B step with 32 W4 layers).
 static int w4_groups() {
   static const int v = [] {
     const char* e = std::getenv("MS_W4_GROUPS");
-    const int g = e ? std::atoi(e) : 2;
-    return g == 3 || g == 4 ? g : 2;
+    const int g = e ? std::atoi(e) : 3;
+    return g == 2 || g == 4 ? g : 3;
   }();
   return v;
 }
@@ -1054,7 +1054,11 @@ static cudaError_t launch_w4_tmem(const GemmWeights& w, const uint16_t* x, int M
 template <int kGPS>
 static cudaError_t launch_w4_groups(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                                     float* out, cudaStream_t stream, const GemmEpi& epi) {
-  switch (w4_groups()) {
+  // no more dequantiser groups than TMEM A stages (a group holds one stage)
+  int rs = 0, as = 0;
+  size_t sm = 0;
+  pick_w4_stages(TM, kGPS, &rs, &as, &sm);
+  switch (std::min(w4_groups(), as)) {
     case 3: return launch_w4_tmem<3, kGPS>(w, x, M, TM, plan, out, stream, epi);
     case 4: return launch_w4_tmem<4, kGPS>(w, x, M, TM, plan, out, stream, epi);
     default: return launch_w4_tmem<2, kGPS>(w, x, M, TM, plan, out, stream, epi);
