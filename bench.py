@@ -226,6 +226,57 @@ def serve_8b(args, local_rank, rank, world):
         dev.close()
 
 
+def prefill_13b(args, local_rank):
+    """BASELINE configs[3]: Llama-2-13B shape, one 8192-token prompt prefilled
+    (TTFT of the long-context burst's requests), all-BF16 and with 10 of 40
+    layers W4A16 (LIS order of the reference profile).  Reports the prefill
+    time (CUDA events around ms_prefill), tokens/s and the linear layers'
+    TFLOP/s against the measured dense bf16 peak."""
+    from paper_2506_02006_b200.device import LLAMA2_13B, DeviceModel, layer_pages
+    shape = dict(LLAMA2_13B)
+    n = args.prefill_tokens
+    nb = (n + 15) // 16
+    pages = shape["L"] * layer_pages(shape, 16) + 10 * layer_pages(shape, 4) + nb + 64
+    dev = DeviceModel(shape, device=local_rank, max_batch=8, max_prefill_tokens=n, max_pos=n + 32, arena_pages=pages)
+    try:
+        dev.weights_synthetic(7)
+        dev.hist_reserve(1, n + 2)
+        dev.kv_attach(0, nb)
+        ids = np.arange(nb, dtype=np.int64)
+        rng = np.random.default_rng(5)
+        dev.hist_write(0, 0, rng.integers(0, shape["V"], size=n).astype(np.int32))
+        d, ffn, H, hd = shape["d"], shape["ffn"], shape["H"], shape["hd"]
+        lin = 2.0 * n * shape["L"] * d * ((H + 2 * shape["KVH"]) * hd + H * hd + 2 * ffn) + 2.0 * n * shape["L"] * ffn * d
+        attn = 2.0 * 2.0 * shape["L"] * H * hd * n * (n + 1) / 2.0  # causal QK^T and PV
+        out = {"workload": f"llama2-13b-shape prefill of one {n}-token prompt", "linear_tflop": lin / 1e12,
+               "attention_tflop": attn / 1e12}
+        order = [int(x) for x in json.load(open(os.path.join(ROOT, "configs", "sequence_lis_40.json")))["order"]]
+        for label, w4 in (("bf16", []), ("w4_10_layers", order[:10])):
+            for l in w4:
+                t = dev.swap_begin(l, 4)
+                dev.swap_wait(t)
+                dev.swap_commit(t)
+            dev.prefill(0, n, ids)  # warm-up
+            dev.sync()
+            ms = []
+            for _ in range(args.prefill_reps):
+                dev.prefill(0, n, ids)
+                ms.append(dev.last_step_ms())
+            t_ms = float(np.median(ms))
+            out[label] = {"ttft_ms": t_ms, "prefill_tok_s": n / (t_ms * 1e-3),
+                          "tflops_total": (lin + attn) / (t_ms * 1e-3) / 1e12}
+        try:
+            with open(PEAKS) as f:
+                peak = float(json.load(f)["bf16_tflops_sustained"])
+        except Exception:
+            peak = 1380.0
+        out["bf16_tflops_peak_sustained"] = peak
+        out["frac_of_peak_bf16"] = out["bf16"]["tflops_total"] / peak
+        return out
+    finally:
+        dev.close()
+
+
 def run_ours(args):
     rank, local_rank, world = dist_env()
     import torch
@@ -417,6 +468,8 @@ def run_ours(args):
     dev.close()
     if args.serve8b_seconds > 0:
         line["serving_8b"] = serve_8b(args, local_rank, rank, world)
+    if args.prefill_tokens > 0:
+        line["prefill_13b"] = prefill_13b(args, local_rank)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
@@ -440,6 +493,9 @@ def main():
     ap.add_argument("--serve8b-seconds", type=float, default=8.0,
                     help="Llama-3-8B bursty serving trace length, BASELINE configs[2] (0 = skip)")
     ap.add_argument("--serve8b-rps", type=float, default=16.0)
+    ap.add_argument("--prefill-tokens", type=int, default=8192,
+                    help="Llama-2-13B long-prompt prefill, BASELINE configs[3] (0 = skip)")
+    ap.add_argument("--prefill-reps", type=int, default=3)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -21,7 +21,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("env", [{"MS_FUSE_ROWS": "1"}, {"MS_ATTN_PERSIST": "1"}, {"MS_W4_SMEM": "1"},
-                                 {"MS_W4_GROUPS": "4"}, {"MS_ATTN_SPLITS": "3"}])
+                                 {"MS_W4_GROUPS": "2"}, {"MS_W4_GROUPS": "4"}, {"MS_W4_GPS": "1"},
+                                 {"MS_GRAPH": "0"}, {"MS_ATTN_SPLITS": "3"}])
 def test_variant_smoke_matches_oracle(env):
     r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=ROOT,
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
