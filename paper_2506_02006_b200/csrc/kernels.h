@@ -173,6 +173,8 @@ struct PrefillAttnArgs {
   int TM;
 };
 cudaError_t prefill_attn_launch(const PrefillAttnArgs& a, cudaStream_t stream);
+// tcgen05 / TMEM variant (head_dim 128); cudaErrorNotSupported otherwise.
+cudaError_t prefill_attn_tc_launch(const PrefillAttnArgs& a, cudaStream_t stream);
 
 // elementwise / row kernels (elementwise.cu)
 cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, const int32_t* hist,

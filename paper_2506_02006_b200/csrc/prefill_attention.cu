@@ -14,6 +14,7 @@
 // (log2 domain).  Q is split q = hi + lo (two bf16 MMAs) so the scores keep
 // fp32-level accuracy (the oracle computes q.k in fp32).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -250,6 +251,15 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
 
 cudaError_t prefill_attn_launch(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.kv.block_tokens != 16) return cudaErrorInvalidValue;
+  // head_dim 128: the tcgen05 kernel (prefill_attention_tc.cu); MS_PREFILL_TC=0 keeps mma.sync
+  static const bool tc = [] {
+    const char* e = std::getenv("MS_PREFILL_TC");
+    return !(e && e[0] == '0');
+  }();
+  if (tc && a.kv.head_dim == 128) {
+    const cudaError_t e = prefill_attn_tc_launch(a, stream);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const int qtiles = (a.n + kQTile - 1) / kQTile;
   const int max_blocks = (a.n + 15) / 16;
   auto smem_for = [&](int hd) { return (size_t)kQTile * hd * 2 * 2 + (size_t)2 * 2 * kKTile * hd * 2 + max_blocks * 4 + 16; };
