@@ -171,6 +171,7 @@ struct PrefillAttnArgs {
   float scale_log2;
   uint16_t* out;          // packed activation image (TM > 0) or row-major [n][H*hd] (TM == 0)
   int TM;
+  int64_t arena_bytes;    // arena extent (tensor map of the tcgen05 kernel); 0 = unknown
 };
 cudaError_t prefill_attn_launch(const PrefillAttnArgs& a, cudaStream_t stream);
 // tcgen05 / TMEM variant (head_dim 128); cudaErrorNotSupported otherwise.

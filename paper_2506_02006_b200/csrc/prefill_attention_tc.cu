@@ -3,26 +3,35 @@
 //
 // Part of `start_prefill` (reference proj/src/engine.cpp:472-485, priced as
 // tokens * prefill_ms_per_token at :477-478): the long-prompt prefill of
-// BASELINE.json configs[3] (Llama-2-13B, 8k tokens) spends ~40% of its time in
-// attention.  prefill_attention.cu does it with mma.sync (m16n8k16); this
-// kernel issues tcgen05.mma with 128x128 tiles.
+// BASELINE.json configs[3] (Llama-2-13B, 8k tokens) spends a large share of its
+// time in attention.  prefill_attention.cu does it with mma.sync (m16n8k16);
+// this kernel issues tcgen05.mma with 128x128 tiles.
 //
-// CTA = (128-query tile, query head), 8 warps.  Per 128-key tile of the
-// sequence's paged KV:
-//   all threads   cp.async the K rows into the UMMA canonical K-major layout
-//                 (double buffered) and the V rows as they are; transpose V
-//                 into a canonical V^T (keys = K dimension) in shared memory
-//   one lane      S = Q_hi K^T + Q_lo K^T into TMEM (16 MMAs M128 N128 K16;
-//                 q = hi + lo bf16 keeps fp32-level score accuracy, as the
-//                 mma.sync kernel and the decode paths do)
-//   warps 0..7    thread = (query row = TMEM lane, half of the keys): masked
-//                 online softmax (log2 domain), P (bf16) written to TMEM
-//   one lane      O_tile = P V into TMEM (A = P from tensor memory)
-//   warps 0..7    O (registers, 64 columns per thread) = O * corr + O_tile
-// Software pipelined: S of tile k+1 runs on the tensor cores during tile k's
-// softmax, P V of tile k during tile k+1's V transpose, and the loads of tile
-// k+2 during both (S and V^T double buffered in TMEM / shared memory).
+// CTA = (128-query tile, query head), 10 warps, warp specialised:
+//   warp 8   TMA producer: per 128-key tile, 8 paged KV blocks x 2 column
+//            halves of K and of V with SWIZZLE_128B boxes {64 dims, 16 keys}
+//            from a 2-D tensor map over the arena (rows of 256 B).  That image
+//            is directly a K-major SW128 operand for K (S = Q K^T) and an
+//            MN-major SW128 operand for V (O += P V): no transpose, no
+//            per-thread copies.  K and V each double buffered.
+//   warp 9   MMA issuer (one elected lane of a converged warp):
+//            S(kt) = Q_hi K^T + Q_lo K^T (16 MMAs M128 N128 K16 into one of two
+//            TMEM S buffers; q = hi + lo bf16 keeps fp32-level score accuracy
+//            as the mma.sync kernel and the decode paths do), then
+//            O += P(kt) V (8 MMAs, A = P read from TMEM, B = V MN-major).
+//            Order S(0), S(1), PV(0), S(2), PV(1), ...: S(kt+1) runs on the
+//            tensor cores while the softmax of tile kt runs.
+//   warps 0-7 softmax: thread = (query row = TMEM lane, half of the 128 keys);
+//            the halves of a row exchange maxima through shared memory under a
+//            pairwise named barrier.  Online softmax in the log2 domain (scale
+//            folded into q) with lazy rescaling: the running max moves only
+//            when a tile's max exceeds it by more than 2^8, so O (in TMEM) is
+//            rescaled a handful of times per row instead of every tile; the
+//            result is the same softmax (exact up to fp32 rounding).
+// TMEM: S [0,256) (two buffers), P [256,384) (two bf16 buffers), O [384,512).
 #include <cstdint>
+#include <cstdlib>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -35,286 +44,367 @@ namespace {
 
 constexpr int kTcTile = 128;           // queries per CTA and keys per KV tile
 constexpr uint32_t kOpBytes = 32768;   // one 128 x 128 bf16 operand
-constexpr uint32_t kTmemS = 0, kTmemP = 256, kTmemO = 384;  // S double-buffered: [0,128) and [128,256)
+constexpr uint32_t kHalfBytes = 16384; // one 64-column half of it (SW128 image)
+constexpr uint32_t kTmemS = 0, kTmemP = 256, kTmemO = 384;
+constexpr int kThreads = 320;
+constexpr float kRescaleLog2 = 8.f;    // lazy rescale threshold (log2 domain)
 
-__device__ __forceinline__ void tc_cp16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void tc_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void tc_cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// byte offset of the 16-B chunk (row r, k-chunk c) of a [128 rows][128 k] canonical K-major operand
+// byte offset of the 16-B chunk (row r, k-chunk c) of a [128 rows][128 k] canonical
+// K-major no-swizzle operand (core matrices 8 rows x 16 B; LBO 128, SBO 2048)
 __device__ __forceinline__ uint32_t canon(int r, int c) {
   return (uint32_t)((((r >> 3) * 16 + c) << 7) + ((r & 7) << 4));
+}
+// SWIZZLE_128B shared-memory descriptor (layout type 2 at bits [61,64))
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return umma_desc(addr, lbo, sbo) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32p(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+      "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t cvt_bf2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(256, 1) prefill_attn_tc_kernel(PrefillAttnArgs a) {
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_attn_tc_kernel(PrefillAttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   constexpr int HD = 128;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQh = smem;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // SW128 atoms: 1024-B aligned
+  uint8_t* sQh = smem;                   // canonical no-swizzle (written by threads)
   uint8_t* sQl = sQh + kOpBytes;
-  uint8_t* sK = sQl + kOpBytes;         // [2] canonical K tiles
-  uint8_t* sV = sK + 2 * kOpBytes;      // raw V rows [key][dim] of the next tile
-  uint8_t* sVt = sV + kOpBytes;         // [2] canonical V^T (dims as rows, keys as k)
-  float* sRed = reinterpret_cast<float*>(sVt + 2 * kOpBytes);       // [2][128] row max / sum halves
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 2 * kTcTile);  // [0,1] S(kt) done per buffer, [2] O_tile done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint8_t* sK = sQl + kOpBytes;          // [2] SW128 images [dim half][key][128 B]
+  uint8_t* sV = sK + 2 * kOpBytes;       // [2] same
+  float* sRed = reinterpret_cast<float*>(sV + 2 * kOpBytes);  // [2 parity][2 half][128] row maxima
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 4 * kTcTile);
+  uint64_t* kfull = bar;       // [2]
+  uint64_t* vfull = bar + 2;   // [2]
+  uint64_t* kempty = bar + 4;  // [2]
+  uint64_t* vempty = bar + 6;  // [2]
+  uint64_t* sfull = bar + 8;   // [2] S(kt) in TMEM buffer kt & 1
+  uint64_t* pfull = bar + 10;  // [2] P(kt) in TMEM buffer kt & 1 (8 softmax warps)
+  uint64_t* odone = bar + 12;  // PV(kt) accumulated into O
+  uint64_t* ofinal = bar + 13; // every MMA done (single phase)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
-  pdl_wait();
-  pdl_trigger();
-  const int qt = blockIdx.x, h = blockIdx.y;
+  const int qtiles = gridDim.y;
+  const int qt = qtiles - 1 - (int)blockIdx.y;  // longest rows first
+  const int h = blockIdx.x;
   const int kvh = h / (a.H / a.KVH);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = qt * kTcTile, n = a.n;
   const int q_last = min(q0 + kTcTile, n) - 1;
   const int n_ktiles = q_last / kTcTile + 1;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
-    fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  const int last_blk = q_last >> 4;
+  const int64_t head_row = (a.kv.layer_off(a.layer) + (int64_t)kvh * 2 * a.kv.head_bytes()) >> 8;
+  const int64_t rows_per_page = a.kv.page_bytes >> 8;
+  const int v_rows = (int)(a.kv.head_bytes() >> 8);
 
-  // ---- Q tile: fp32 -> (hi, lo) bf16, canonical layout
-  for (int idx = threadIdx.x; idx < kTcTile * 16; idx += blockDim.x) {
-    const int r = idx >> 4, c = idx & 15;
-    const int q = q0 + r;
-    uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-    if (q < n) {
-      const float4* src = reinterpret_cast<const float4*>(a.q + ((size_t)q * a.H + h) * HD + c * 8);
-      const float4 x0 = src[0], x1 = src[1];
-      const float sl = a.scale_log2;  // scores come out of the MMA already in the log2 domain
-      const float v[8] = {x0.x * sl, x0.y * sl, x0.z * sl, x0.w * sl, x1.x * sl, x1.y * sl, x1.z * sl, x1.w * sl};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint16_t h0 = f2bf(v[2 * e]), h1 = f2bf(v[2 * e + 1]);
-        hi[e] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-        lo[e] = pack_bf2(v[2 * e] - bf2f(h0), v[2 * e + 1] - bf2f(h1));
-      }
+  pdl_wait();
+  pdl_trigger();
+  // K or V of tile kt: 8 blocks (clamped to the last block: keys past the row
+  // are masked, and a clamped duplicate keeps them finite) x 2 column halves
+  auto load = [&](int kt, bool is_v) {
+    const int s = kt & 1;
+    uint64_t* fb = is_v ? &vfull[s] : &kfull[s];
+    const uint32_t dst = smem_u32((is_v ? sV : sK) + s * kOpBytes);
+    mbar_expect_tx(fb, kOpBytes);
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+      const int blk = min(kt * 8 + j, last_blk);
+      const int row = (int)(__ldg(a.pages + blk) * rows_per_page + head_row) + (is_v ? v_rows : 0);
+      tma2d(dst + j * 2048, &tmap, 0, row, fb);
+      tma2d(dst + kHalfBytes + j * 2048, &tmap, 64, row, fb);
     }
-    *reinterpret_cast<uint4*>(sQh + canon(r, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4*>(sQl + canon(r, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-  }
-  const int64_t head_off = a.kv.layer_off(a.layer) + (int64_t)kvh * 2 * a.kv.head_bytes();
-  // loads: thread = (token row, half of its 16 chunks); one page-id load per thread
-  auto load_tile = [&](int kt) {
-    const int r = threadIdx.x >> 1, c0 = (threadIdx.x & 1) * 8;
-    int t = kt * kTcTile + r;
-    if (t > q_last) t = q_last;  // masked anyway; keeps the address valid
-    const char* base = a.kv.arena + (int64_t)__ldg(a.pages + (t >> 4)) * a.kv.page_bytes + head_off +
-                       (t & 15) * HD * 2 + c0 * 16;
-    const uint32_t k_u = smem_u32(sK + (kt & 1) * kOpBytes) + canon(r, c0);
-    const uint32_t v_u = smem_u32(sV) + (uint32_t)(r * 256 + c0 * 16);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      tc_cp16(k_u + c * 128, base + c * 16);
-      tc_cp16(v_u + c * 16, base + a.kv.head_bytes() + c * 16);
-    }
-    tc_cp_commit();
   };
-  // raw V (landed) -> canonical V^T buffer `buf`: item = (dim pair, key chunk)
-  auto transpose_v = [&](int buf) {
-    uint8_t* dst = sVt + buf * kOpBytes;
-    for (int it = threadIdx.x; it < 64 * 16; it += blockDim.x) {
-      const int dp = it & 63, c = it >> 6;
-      uint32_t w[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) w[j] = *reinterpret_cast<const uint32_t*>(sV + (c * 8 + j) * 256 + dp * 4);
-      uint32_t lo4[4], hi4[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        lo4[j] = __byte_perm(w[2 * j], w[2 * j + 1], 0x5410);  // dim 2dp: keys 2j, 2j+1
-        hi4[j] = __byte_perm(w[2 * j], w[2 * j + 1], 0x7632);  // dim 2dp+1
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int i = 0; i < 14; ++i) mbar_init(&bar[i], (i == 10 || i == 11) ? 8 : 1);
+      fence_mbar_init();
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      for (int kt = 0; kt < min(2, n_ktiles); ++kt) {
+        load(kt, false);
+        load(kt, true);
       }
-      *reinterpret_cast<uint4*>(dst + canon(2 * dp, c)) = make_uint4(lo4[0], lo4[1], lo4[2], lo4[3]);
-      *reinterpret_cast<uint4*>(dst + canon(2 * dp + 1, c)) = make_uint4(hi4[0], hi4[1], hi4[2], hi4[3]);
+    }
+    __syncwarp();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+
+  // ---- Q tile (softmax warps): fp32 * scale_log2 -> (hi, lo) bf16, canonical layout
+  if (warp < 8) {
+    for (int idx = threadIdx.x; idx < kTcTile * 16; idx += 256) {
+      const int r = idx >> 4, c = idx & 15;
+      const int q = q0 + r;
+      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+      if (q < n) {
+        const float4* src = reinterpret_cast<const float4*>(a.q + ((size_t)q * a.H + h) * HD + c * 8);
+        const float4 x0 = src[0], x1 = src[1];
+        const float sl = a.scale_log2;  // scores come out of the MMA already in the log2 domain
+        const float v[8] = {x0.x * sl, x0.y * sl, x0.z * sl, x0.w * sl, x1.x * sl, x1.y * sl, x1.z * sl, x1.w * sl};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint16_t h0 = f2bf(v[2 * e]), h1 = f2bf(v[2 * e + 1]);
+          hi[e] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+          lo[e] = pack_bf2(v[2 * e] - bf2f(h0), v[2 * e + 1] - bf2f(h1));
+        }
+      }
+      *reinterpret_cast<uint4*>(sQh + canon(r, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(sQl + canon(r, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
     fence_proxy_async_smem();
-  };
-  load_tile(0);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = umma_idesc_bf16(128, 128);
-  const uint64_t dQh = umma_desc(smem_u32(sQh), 128u, 2048u), dQl = umma_desc(smem_u32(sQl), 128u, 2048u);
-  auto issue_s = [&](int kt) {  // S[kt & 1] = Q_hi K^T + Q_lo K^T
-    if (warp == 0) {
+
+  if (warp == 8) {
+    // ---------------------------------------------------------- producer
+    if (lane == 0) {
+      for (int kt = 2; kt < n_ktiles; ++kt) {
+        const uint32_t par = ((kt >> 1) - 1) & 1;
+        mbar_wait(&kempty[kt & 1], par);  // S(kt - 2) read K buffer kt & 1
+        load(kt, false);
+        mbar_wait(&vempty[kt & 1], par);  // PV(kt - 2) read V buffer kt & 1
+        load(kt, true);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    // ---------------------------------------------------------- MMA issuer
+    const uint32_t idesc = umma_idesc_bf16(128, 128);
+    const uint32_t idesc_pv = idesc | (1u << 16);  // B (= V) MN-major
+    const uint64_t dQh = umma_desc(smem_u32(sQh), 128u, 2048u), dQl = umma_desc(smem_u32(sQl), 128u, 2048u);
+    auto issue_s = [&](int kt) {
+      const int s = kt & 1;
+      mbar_wait(&kfull[s], (kt >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint64_t dK = umma_desc(smem_u32(sK + (kt & 1) * kOpBytes), 128u, 2048u);
-        const uint32_t d = tmem + kTmemS + (uint32_t)(kt & 1) * 128u;
+        const uint64_t dK = desc_sw128(smem_u32(sK + s * kOpBytes), 16u, 1024u);
+        const uint32_t d = tmem + kTmemS + (uint32_t)s * 128u;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-          umma_bf16(d, desc_add(dQh, ks * 256u), desc_add(dK, ks * 256u), idesc, ks ? 1u : 0u);
-          umma_bf16(d, desc_add(dQl, ks * 256u), desc_add(dK, ks * 256u), idesc, 1u);
+          const uint64_t dk = desc_add(dK, (uint32_t)(ks >> 2) * kHalfBytes + (uint32_t)(ks & 3) * 32u);
+          umma_bf16(d, desc_add(dQh, ks * 256u), dk, idesc, ks ? 1u : 0u);
+          umma_bf16(d, desc_add(dQl, ks * 256u), dk, idesc, 1u);
         }
-        umma_commit(&bar[kt & 1]);
+        umma_commit(&sfull[s]);
+        umma_commit(&kempty[s]);
       }
       __syncwarp();
-    }
-  };
-  auto issue_pv = [&](int kt) {  // O_tile = P V(kt)
-    if (warp == 0) {
+    };
+    issue_s(0);
+    for (int kt = 0; kt < n_ktiles; ++kt) {
+      if (kt + 1 < n_ktiles) issue_s(kt + 1);  // S buffer (kt+1)&1 was released by P(kt-1)
+      const int s = kt & 1;
+      mbar_wait(&pfull[s], (kt >> 1) & 1);
+      mbar_wait(&vfull[s], (kt >> 1) & 1);
+      const int r0 = q_last + 1 - kt * kTcTile;
+      if (kt == n_ktiles - 1 && r0 < kTcTile) {
+        // keys past the row (the rest of its last block and the clamped
+        // duplicates): zero their V rows -- P is 0 there, but the arena bytes
+        // past the sequence are arbitrary and 0 * NaN would not be 0
+        uint8_t* vb = sV + s * kOpBytes;
+        for (int i = lane; i < (kTcTile - r0) * 16; i += 32) {
+          const int r = r0 + (i >> 4), c = i & 15;
+          *reinterpret_cast<uint4*>(vb + (c >> 3) * kHalfBytes + r * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+      }
       tc_fence_after();
       if (elect_one()) {
-        const uint64_t dVt = umma_desc(smem_u32(sVt + (kt & 1) * kOpBytes), 128u, 2048u);
+        const uint64_t dV = desc_sw128(smem_u32(sV + s * kOpBytes), kHalfBytes, 1024u);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          umma_bf16_ts(tmem + kTmemO, tmem + kTmemP + ks * 8u, desc_add(dVt, ks * 256u), idesc, ks ? 1u : 0u);
-        umma_commit(&bar[2]);
+          umma_bf16_ts(tmem + kTmemO, tmem + kTmemP + (uint32_t)s * 64u + ks * 8u, desc_add(dV, ks * 2048u),
+                       idesc_pv, (kt | ks) ? 1u : 0u);
+        umma_commit(&vempty[s]);
+        umma_commit(odone);
+        if (kt == n_ktiles - 1) umma_commit(ofinal);
       }
       __syncwarp();
     }
-  };
-
-  // softmax state and O: thread = (query row = TMEM lane, half of the key / dim columns)
-  const int row = (warp & 3) * 32 + lane;
-  const int half = warp >> 2;
-  const int qrow = q0 + row;
-  float m_run = -INFINITY, l_run = 0.f, prev_corr = 1.f;
-  float o[64];
-#pragma unroll
-  for (int j = 0; j < 64; ++j) o[j] = 0.f;
-  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-  auto o_update = [&]() {  // O = O * corr + O_tile (PV done)
-#pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem + lane_off + kTmemO + (uint32_t)(half * 64 + c0), v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) o[c0 + j] = o[c0 + j] * prev_corr + __uint_as_float(v[j]);
-    }
-  };
-
-  // prologue: tile 0 -> V^T[0], S(0) in flight, tile 1 loading
-  tc_cp_wait<0>();
-  __syncthreads();
-  transpose_v(0);
-  __syncthreads();
-  issue_s(0);
-  if (n_ktiles > 1) load_tile(1);
-
-  for (int kt = 0; kt < n_ktiles; ++kt) {
-    // 1. previous tile's P V done: fold it into O (frees O_tile, P and V^T[(kt+1) & 1])
-    if (kt > 0) {
-      mbar_wait(&bar[2], (kt - 1) & 1);
+  } else {
+    // ---------------------------------------------------------- softmax
+    const int row = (warp & 3) * 32 + lane;
+    const int half = warp >> 2;
+    const int qrow = q0 + row;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int pair_bar = 1 + (warp & 3);
+    float m_run = -INFINITY, l_half = 0.f;
+    for (int kt = 0; kt < n_ktiles; ++kt) {
+      const int s = kt & 1;
+      mbar_wait(&sfull[s], (kt >> 1) & 1);
       tc_fence_after();
-      o_update();
-    }
-    // 2. next tile: V^T, then its S on the tensor cores while this tile's softmax runs
-    if (kt + 1 < n_ktiles) {
-      tc_cp_wait<0>();
-      tc_fence_before();
-      __syncthreads();
-      transpose_v((kt + 1) & 1);
-      __syncthreads();
-      issue_s(kt + 1);
-    }
-    // 3. this tile's S
-    mbar_wait(&bar[kt & 1], (kt >> 1) & 1);
-    tc_fence_after();
-    // 4. the K buffer S(kt) read and the raw V buffer are free: load tile kt + 2
-    if (kt + 2 < n_ktiles) load_tile(kt + 2);
-    // 5. softmax: the two halves of a row (warps w and w + 4) meet through
-    // shared memory under a pairwise named barrier; masking only on the
-    // diagonal tile (earlier tiles hold keys < q0 <= every query row)
-    {
-      const int key0 = kt * kTcTile + half * 64;
+      uint32_t v[64];
+      const uint32_t scol = tmem + lane_off + kTmemS + (uint32_t)s * 128u + (uint32_t)(half * 64);
+      tmem_ld32(scol, v);
+      tmem_ld32(scol + 32, v + 32);
+      tmem_ld_wait();
       const bool diag = kt == n_ktiles - 1;
-      const uint32_t scol = tmem + lane_off + kTmemS + (uint32_t)(kt & 1) * 128u + (uint32_t)(half * 64);
-      const int pair_bar = 1 + (warp & 3);
-      float mx = -INFINITY;
+      if (diag) {  // earlier tiles hold keys < q0 <= every query row
+        const int key0 = kt * kTcTile + half * 64;
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(scol + c0, v);
-        tmem_ld_wait();
-        if (diag) {
+        for (int j = 0; j < 64; ++j)
+          if (key0 + j > qrow || key0 + j >= n) v[j] = __float_as_uint(-INFINITY);
+      }
+      float mx = __uint_as_float(v[0]);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int key = key0 + c0 + j;
-            mx = fmaxf(mx, (key > qrow || key >= n) ? -INFINITY : __uint_as_float(v[j]));
-          }
-        } else {
+      for (int j = 1; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
+      float* red = sRed + s * 2 * kTcTile;
+      red[half * kTcTile + row] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+      const float m_tile = fmaxf(red[row], red[kTcTile + row]);
+      const bool move = m_tile > m_run + kRescaleLog2;  // false while both are -inf
+      const float m_new = move ? m_tile : m_run;
+      const float corr = (move && m_run != -INFINITY) ? ex2(m_run - m_new) : 1.f;
+      if (kt > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
+        // O holds PV(0 .. kt-1): wait for the last of them, then rescale this row half
+        mbar_wait(odone, (kt - 1) & 1);
+        tc_fence_after();
+        const uint32_t ocol = tmem + lane_off + kTmemO + (uint32_t)(half * 64);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld32(ocol + c0, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * corr);
+          tmem_st32p(ocol + c0, o);
         }
       }
-      sRed[half * kTcTile + row] = mx;
-      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-      const float m_new = fmaxf(m_run, fmaxf(sRed[row], sRed[kTcTile + row]));
-      const float corr = m_new == -INFINITY ? 1.f : exp2f(m_run - m_new);
+      m_run = m_new;
       const float msub = m_new == -INFINITY ? 0.f : m_new;
       float psum = 0.f;
       uint32_t pk[32];
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(scol + c0, v);
-        tmem_ld_wait();
+      for (int j = 0; j < 64; j += 2) {
+        const float p0 = ex2(__uint_as_float(v[j]) - msub);
+        const float p1 = ex2(__uint_as_float(v[j + 1]) - msub);
+        psum += p0 + p1;
+        pk[j >> 1] = cvt_bf2(p0, p1);
+      }
+      l_half = l_half * corr + psum;
+      tmem_st32p(tmem + lane_off + kTmemP + (uint32_t)s * 64u + (uint32_t)(half * 32), pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[s]);
+    }
+    // ---- epilogue: O / l
+    mbar_wait(ofinal, 0);
+    tc_fence_after();
+    float* lsum = sRed + (((n_ktiles - 1) & 1) ? 0 : 2 * kTcTile);  // the parity buffer the last tile did not use
+    lsum[half * kTcTile + row] = l_half;
+    asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+    const float l = lsum[row] + lsum[kTcTile + row];
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const int K = a.H * HD;
+    const uint32_t ocol = tmem + lane_off + kTmemO + (uint32_t)(half * 64);
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          float p2[2];
+    for (int c0 = 0; c0 < 64; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld32(ocol + c0, o);
+      tmem_ld_wait();
+      if (qrow < n) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = key0 + c0 + j + e;
-            float p = exp2f(__uint_as_float(v[j + e]) - msub);
-            if (diag && (key > qrow || key >= n)) p = 0.f;
-            p2[e] = p;
-            psum += p;
-          }
-          pk[(c0 + j) >> 1] = pack_bf2(p2[0], p2[1]);
+        for (int j = 0; j < 32; j += 8) {
+          const int dim = half * 64 + c0 + j;
+          uint4 w;
+          w.x = cvt_bf2(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
+          w.y = cvt_bf2(__uint_as_float(o[j + 2]) * inv, __uint_as_float(o[j + 3]) * inv);
+          w.z = cvt_bf2(__uint_as_float(o[j + 4]) * inv, __uint_as_float(o[j + 5]) * inv);
+          w.w = cvt_bf2(__uint_as_float(o[j + 6]) * inv, __uint_as_float(o[j + 7]) * inv);
+          const size_t off = a.TM > 0 ? act_off(qrow, h * HD + dim, K, a.TM) : (size_t)qrow * K + h * HD + dim;
+          *reinterpret_cast<uint4*>(a.out + off) = w;
         }
       }
-      tmem_st32(tmem + lane_off + kTmemP + (uint32_t)(half * 32), pk);
-      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // both halves read the maxima
-      sRed[half * kTcTile + row] = psum;
-      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-      l_run = l_run * corr + sRed[row] + sRed[kTcTile + row];
-      m_run = m_new;
-      prev_corr = corr;
-      tmem_st_wait();
-    }
-    // 6. this tile's P V (P in TMEM)
-    tc_fence_before();
-    __syncthreads();
-    issue_pv(kt);
-  }
-  mbar_wait(&bar[2], (n_ktiles - 1) & 1);
-  tc_fence_after();
-  o_update();
-  if (qrow < n) {
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    const int K = a.H * HD;
-#pragma unroll
-    for (int j = 0; j < 64; j += 2) {
-      const int dim = half * 64 + j;
-      const uint32_t v = pack_bf2(o[j] * inv, o[j + 1] * inv);
-      const size_t off = a.TM > 0 ? act_off(qrow, h * HD + dim, K, a.TM) : (size_t)qrow * K + h * HD + dim;
-      *reinterpret_cast<uint32_t*>(a.out + off) = v;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 512);
+  if (warp == 9) tmem_dealloc(tmem, 512);
+}
+
+// 2-D map over the arena as rows of 256 B (one token of one KV head), boxes of
+// {64 dims, 16 tokens} = one column half of one KV block, 128-B swizzled.
+static bool prefill_tensor_map(const KvGeom& kv, int64_t arena_bytes, CUtensorMap* out) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[2] = {128, (cuuint64_t)(arena_bytes / 256)};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {64, 16};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.arena, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t prefill_attn_tc_launch(const PrefillAttnArgs& a, cudaStream_t stream) {
-  if (a.kv.block_tokens != 16 || a.kv.head_dim != 128) return cudaErrorNotSupported;
+  if (a.kv.block_tokens != 16 || a.kv.head_dim != 128 || a.arena_bytes <= 0) return cudaErrorNotSupported;
+  if (a.arena_bytes / 256 >= (int64_t)1 << 31) return cudaErrorNotSupported;  // TMA row coordinate is int32
+  static thread_local const char* map_arena = nullptr;
+  static thread_local int64_t map_bytes = 0;
+  static thread_local CUtensorMap tmap;
+  if (map_arena != a.kv.arena || map_bytes != a.arena_bytes) {
+    if (!prefill_tensor_map(a.kv, a.arena_bytes, &tmap)) return cudaErrorInvalidValue;
+    map_arena = a.kv.arena;
+    map_bytes = a.arena_bytes;
+  }
   const int qtiles = (a.n + kTcTile - 1) / kTcTile;
-  const size_t smem = 7 * (size_t)kOpBytes + 2 * kTcTile * 4 + 4 * 8 + 16;
-  if (smem > 227 * 1024) return cudaErrorNotSupported;
+  const size_t smem = 1024 + 6 * (size_t)kOpBytes + 4 * kTcTile * 4 + 16 * 8;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  return launch_pdl(prefill_attn_tc_kernel, dim3(qtiles, a.H), dim3(256), smem, stream, a);
+  return launch_pdl(prefill_attn_tc_kernel, dim3(a.H, qtiles), dim3(kThreads), smem, stream, a, tmap);
 }
 
 }  // namespace ms

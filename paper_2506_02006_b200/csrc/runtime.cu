@@ -559,6 +559,7 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       pa.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
       pa.out = c->x;
       pa.TM = TM;
+      pa.arena_bytes = (int64_t)c->desc.arena_pages * c->page_bytes;
       if (!(skip & 8)) CK(ms::prefill_attn_launch(pa, c->compute));
       c->launches += 1;
     } else {
@@ -1605,6 +1606,13 @@ int ms_k_attn_prefill(const float* q, const void* arena, int64_t page_bytes, int
     a.out = out;
     a.TM = 0;
     if (n < 1 || H % KVH) fail(MS_EVALIDATION, "attn_prefill: bad shape");
+    {  // arena extent for the tensor map: pages the sequence references
+      std::vector<int32_t> hp((size_t)(n + 15) / 16);
+      CK(cudaMemcpy(hp.data(), pages, hp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      int32_t mx = 0;
+      for (int32_t v : hp) mx = std::max(mx, v);
+      a.arena_bytes = (int64_t)(mx + 1) * page_bytes;
+    }
     CK(ms::prefill_attn_launch(a, (cudaStream_t)stream));
   });
 }

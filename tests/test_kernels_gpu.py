@@ -171,10 +171,14 @@ def test_paged_attention(H, KVH, hd, ctxs, splits):
         np.testing.assert_allclose(got[r], ref32, rtol=1e-2, atol=2e-3)
 
 
-@pytest.mark.parametrize("H,KVH,hd,n", [(4, 2, 64, 1), (4, 2, 64, 77), (8, 8, 128, 130), (32, 8, 128, 300),
-                                        (8, 1, 128, 64)])
-def test_prefill_attention(H, KVH, hd, n):
-    """Causal prefill attention over paged KV vs the oracle, query by query."""
+@pytest.mark.parametrize("H,KVH,hd,n,qscale", [(4, 2, 64, 1, 1.0), (4, 2, 64, 77, 1.0), (8, 8, 128, 130, 1.0),
+                                               (32, 8, 128, 300, 1.0), (8, 1, 128, 64, 1.0),
+                                               (4, 4, 128, 700, 1.0), (4, 2, 128, 640, 1.0),
+                                               (4, 4, 128, 555, 40.0), (2, 2, 128, 1030, 12.0)])
+def test_prefill_attention(H, KVH, hd, n, qscale):
+    """Causal prefill attention over paged KV vs the oracle, query by query.
+    qscale > 1 spreads the scores over many powers of two, so the running
+    max moves mid-sequence (the tcgen05 kernel's lazy O rescale)."""
     N = _native()
     L, layer = 2, 1
     page_bytes = 16 * L * KVH * 2 * hd * 2
@@ -183,7 +187,9 @@ def test_prefill_attention(H, KVH, hd, n):
     rng = np.random.default_rng(5)
     arena = O.f32_to_bf16(rng.uniform(-1, 1, n_pages * page_bytes // 2).astype(np.float32))
     pages = rng.permutation(n_pages).astype(np.int32)[:nb]
-    q = rng.uniform(-1, 1, (n, H, hd)).astype(np.float32)
+    q = (rng.uniform(-1, 1, (n, H, hd)) * qscale).astype(np.float32)
+    if qscale > 1:  # rising score scale along the sequence: later keys/queries dominate
+        q *= np.linspace(0.2, 1.0, n, dtype=np.float32)[:, None, None]
     d_arena = dev_u16(arena)
     d_q = torch.from_numpy(q).cuda()
     d_pages = torch.from_numpy(pages.copy()).cuda()
@@ -202,7 +208,7 @@ def test_prefill_attention(H, KVH, hd, n):
             off = base + kh * 2 * head_elems + (t % 16) * hd
             k[t, kh] = arena[off: off + hd]
             v[t, kh] = arena[off + head_elems: off + head_elems + hd]
-    for qi in sorted({0, n // 3, n // 2, n - 1}):
+    for qi in sorted({0, n // 3, n // 2, n - 1, min(n - 1, 127), min(n - 1, 128), min(n - 1, 255), n - 2 if n > 1 else 0}):
         _, ref32 = O.attention(q[qi].reshape(-1), k[: qi + 1], v[: qi + 1], H, KVH, hd)
         # P is rounded to bf16 for the PV MMA (scores keep fp32 accuracy via the q hi/lo split)
         np.testing.assert_allclose(got[qi], ref32, rtol=2e-2, atol=4e-3)
