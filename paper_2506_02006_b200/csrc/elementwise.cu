@@ -27,6 +27,13 @@ __device__ __forceinline__ float sum_slots(const float* p, size_t stride, int n)
   for (int s = 8; s < n; ++s) acc += __ldcg(p + s * stride);
   return acc;
 }
+__device__ __forceinline__ float4 sum_slots4(const float4* p, size_t stride4, int n);
+// the GEMM output at (m, col): one slot for whole-tile plans (every long
+// prefill), the stream-K partial slots otherwise
+__device__ __forceinline__ float4 part_ld4(const GemmPlanDev& plan, const float4* p, size_t stride4, int m, int col) {
+  if (plan.aligned) return __ldcg(p);
+  return sum_slots4(p, stride4, part_slots(plan, m, col));
+}
 __device__ __forceinline__ float4 sum_slots4(const float4* p, size_t stride4, int n) {
   float4 v[6];
 #pragma unroll
@@ -104,65 +111,74 @@ cudaError_t embed_norm_launch(const uint16_t* embed, const int32_t* tokens, cons
 }
 
 // --------------------------------- QKV: split-K sum, RoPE, q out, K/V -> KV pages
-// grid (rows, head groups of 8), block (hd/2, 8): one thread per rotation pair
-// (i, i + hd/2) of one head.  Few fat CTAs: thousands of 64-thread CTAs are
-// bound by the CTA launch rate, not by the (tiny) data.
-constexpr int kQkvHeadsPerCta = 8;
-__global__ void qkv_post_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int H, int KVH, int hd,
-                                const float* __restrict__ rc, const float* __restrict__ rs,
-                                const int32_t* __restrict__ pos, KvGeom kv, int layer,
-                                const int32_t* __restrict__ pages, const int32_t* __restrict__ page_row,
-                                int page_stride, float* __restrict__ q_out) {
+// One CTA per row; thread item = (head, 4 consecutive rotation pairs): float4
+// reads of both halves, float4 q stores, 8-B K/V stores (no per-element index
+// arithmetic; a long prefill has M = thousands of rows).
+__global__ void __launch_bounds__(256) qkv_post_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int H,
+                                                       int KVH, int hd, const float* __restrict__ rc,
+                                                       const float* __restrict__ rs, const int32_t* __restrict__ pos,
+                                                       KvGeom kv, int layer, const int32_t* __restrict__ pages,
+                                                       const int32_t* __restrict__ page_row, int page_stride,
+                                                       float* __restrict__ q_out) {
   pdl_wait();
   pdl_trigger();
-  const int m = blockIdx.x, hs = blockIdx.y * kQkvHeadsPerCta + threadIdx.y, i = threadIdx.x;
-  if (hs >= H + 2 * KVH) return;
-  const int N = (H + 2 * KVH) * hd;
-  const int half = hd >> 1;
-  const int p = pos[m];
-  const size_t stride = (size_t)M * N;
-  const int c0 = hs * hd + i;
-  const float* src = part + (size_t)m * N + c0;
-  float x0 = sum_slots(src, stride, part_slots(plan, m, c0));
-  float x1 = sum_slots(src + half, stride, part_slots(plan, m, c0 + half));
-  if (hs < H + KVH) {  // q and k heads are rotated
-    const float c = rc[(size_t)p * half + i], sn = rs[(size_t)p * half + i];
-    const float y0 = x0 * c - x1 * sn;
-    const float y1 = x1 * c + x0 * sn;
-    x0 = y0;
-    x1 = y1;
+  const int heads = H + 2 * KVH;
+  const int half = hd >> 1, g_per = half >> 2;
+  const int N = heads * hd;
+  const size_t stride4 = (size_t)M * N / 4;
+  for (int m = blockIdx.x; m < M; m += gridDim.x) {
+    const int p = pos[m];
+    const int prow = page_row ? page_row[m] : m;
+    const int32_t page = pages[(size_t)prow * page_stride + p / kv.block_tokens];
+    const int slot = p % kv.block_tokens;
+    char* kv_base = kv.arena + (int64_t)page * kv.page_bytes + kv.layer_off(layer) + (int64_t)slot * hd * 2;
+    const float4* row4 = reinterpret_cast<const float4*>(part + (size_t)m * N);
+    for (int u = threadIdx.x; u < heads * g_per; u += blockDim.x) {
+      const int hs = u / g_per, i = (u - hs * g_per) * 4;
+      const int c0 = hs * hd + i;
+      float4 x0 = part_ld4(plan, row4 + (c0 >> 2), stride4, m, c0);
+      float4 x1 = part_ld4(plan, row4 + ((c0 + half) >> 2), stride4, m, c0 + half);
+      if (hs < H + KVH) {  // q and k heads are rotated
+        const float4 c = *reinterpret_cast<const float4*>(rc + (size_t)p * half + i);
+        const float4 sn = *reinterpret_cast<const float4*>(rs + (size_t)p * half + i);
+        const float4 y0 = make_float4(x0.x * c.x - x1.x * sn.x, x0.y * c.y - x1.y * sn.y, x0.z * c.z - x1.z * sn.z,
+                                      x0.w * c.w - x1.w * sn.w);
+        x1 = make_float4(x1.x * c.x + x0.x * sn.x, x1.y * c.y + x0.y * sn.y, x1.z * c.z + x0.z * sn.z,
+                         x1.w * c.w + x0.w * sn.w);
+        x0 = y0;
+      }
+      if (hs < H) {
+        float* q = q_out + ((size_t)m * H + hs) * hd;
+        *reinterpret_cast<float4*>(q + i) = x0;
+        *reinterpret_cast<float4*>(q + i + half) = x1;
+        continue;
+      }
+      const bool is_v = hs >= H + KVH;
+      const int kh = is_v ? hs - H - KVH : hs - H;
+      uint16_t* dst = reinterpret_cast<uint16_t*>(kv_base + (int64_t)kh * 2 * kv.head_bytes() +
+                                                  (is_v ? kv.head_bytes() : 0));
+      *reinterpret_cast<uint2*>(dst + i) = make_uint2(pack_bf2(x0.x, x0.y), pack_bf2(x0.z, x0.w));
+      *reinterpret_cast<uint2*>(dst + i + half) = make_uint2(pack_bf2(x1.x, x1.y), pack_bf2(x1.z, x1.w));
+    }
   }
-  if (hs < H) {
-    float* q = q_out + ((size_t)m * H + hs) * hd;
-    q[i] = x0;
-    q[i + half] = x1;
-    return;
-  }
-  const int prow = page_row ? page_row[m] : m;
-  const int32_t page = pages[(size_t)prow * page_stride + p / kv.block_tokens];
-  const int slot = p % kv.block_tokens;
-  const bool is_v = hs >= H + KVH;
-  const int kh = is_v ? hs - H - KVH : hs - H;
-  uint16_t* dst = reinterpret_cast<uint16_t*>(kv.arena + (int64_t)page * kv.page_bytes + kv.layer_off(layer) +
-                                              (int64_t)kh * 2 * kv.head_bytes() + (is_v ? kv.head_bytes() : 0)) +
-                  slot * hd;
-  dst[i] = f2bf(x0);
-  dst[i + half] = f2bf(x1);
 }
 
 cudaError_t qkv_post_launch(const float* part, const GemmPlanDev& plan, int M, int H, int KVH, int hd, const float* rope_cos,
                             const float* rope_sin, const int32_t* pos, const KvGeom& kv, int layer,
                             const int32_t* pages, const int32_t* page_row, int page_stride, float* q_out,
                             cudaStream_t s) {
-  const int heads = H + 2 * KVH;
-  return launch_pdl(qkv_post_kernel, dim3(M, (heads + kQkvHeadsPerCta - 1) / kQkvHeadsPerCta),
-                    dim3(hd / 2, kQkvHeadsPerCta), 0, s, part, plan, M, H, KVH, hd, rope_cos, rope_sin, pos, kv, layer,
-                    pages, page_row, page_stride, q_out);
+  if (hd % 8) return cudaErrorInvalidValue;
+  const int items = (H + 2 * KVH) * (hd / 8);
+  const int threads = items >= 256 ? 256 : (items + 31) / 32 * 32;
+  return launch_pdl(qkv_post_kernel, dim3(M < 65535 ? M : 65535), dim3(threads), 0, s, part, plan, M, H, KVH, hd,
+                    rope_cos, rope_sin, pos, kv, layer, pages, page_row, page_stride, q_out);
 }
 
 // ----------------------------------- residual add (split-K sum) + RMSNorm + pack
-// One CTA per row, float4 per thread; the normalised row is written straight
-// into the packed activation image of the next GEMM.
+// One CTA per row; each thread keeps its (up to 8) float4 of the row in
+// registers between the sum of squares and the normalised write, which goes
+// straight into the packed activation image of the next GEMM.
+constexpr int kNormPer = 8;
 __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __restrict__ part, GemmPlanDev plan, int M,
                                                              int d, float* __restrict__ h,
                                                              const uint16_t* __restrict__ w, float eps,
@@ -175,16 +191,21 @@ __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __rest
   const int d4 = d >> 2;
   float4* hr = reinterpret_cast<float4*>(h + (size_t)m * d);
   const float4* pr = reinterpret_cast<const float4*>(part + (size_t)m * d);
+  float4 v[kNormPer];
   float ss = 0.f;
-  for (int i4 = threadIdx.x; i4 < d4; i4 += blockDim.x) {
-    float4 v = hr[i4];
-    const float4 a = sum_slots4(pr + i4, stride / 4, part_slots(plan, m, i4 * 4));
-    v.x += a.x;
-    v.y += a.y;
-    v.z += a.z;
-    v.w += a.w;
-    hr[i4] = v;
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int k = 0; k < kNormPer; ++k) {
+    const int i4 = threadIdx.x + k * blockDim.x;
+    if (i4 < d4) {
+      v[k] = hr[i4];
+      const float4 a = part_ld4(plan, pr + i4, stride / 4, m, i4 * 4);
+      v[k].x += a.x;
+      v[k].y += a.y;
+      v[k].z += a.z;
+      v[k].w += a.w;
+      hr[i4] = v[k];
+      ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+    }
   }
   if (w == nullptr || m < norm_row_begin) return;  // uniform per block
   // block reduction
@@ -201,24 +222,29 @@ __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __rest
   const float r = 1.0f / sqrtf(red[0] / (float)d + eps);
   const int mo = m - norm_row_begin;
   const uint2* w4 = reinterpret_cast<const uint2*>(w);
-  for (int i4 = threadIdx.x; i4 < d4; i4 += blockDim.x) {
-    const float4 v = hr[i4];
-    const uint2 wv = w4[i4];
-    uint2 o;
-    o.x = pack_bf2((v.x * r) * __uint_as_float(wv.x << 16), (v.y * r) * __uint_as_float(wv.x & 0xFFFF0000u));
-    o.y = pack_bf2((v.z * r) * __uint_as_float(wv.y << 16), (v.w * r) * __uint_as_float(wv.y & 0xFFFF0000u));
-    *reinterpret_cast<uint2*>(x + act_off(mo, i4 * 4, d, TM)) = o;
+  uint16_t* xrow = x + act_row_off(mo, d, TM);
+#pragma unroll
+  for (int k = 0; k < kNormPer; ++k) {
+    const int i4 = threadIdx.x + k * blockDim.x;
+    if (i4 < d4) {
+      const uint2 wv = w4[i4];
+      uint2 o;
+      o.x = pack_bf2((v[k].x * r) * __uint_as_float(wv.x << 16), (v[k].y * r) * __uint_as_float(wv.x & 0xFFFF0000u));
+      o.y = pack_bf2((v[k].z * r) * __uint_as_float(wv.y << 16), (v[k].w * r) * __uint_as_float(wv.y & 0xFFFF0000u));
+      *reinterpret_cast<uint2*>(xrow + act_col_off(i4 * 4, TM)) = o;
+    }
   }
 }
 
-static int norm_threads(int d) {
-  int t = d / 4;
+static int norm_threads(int d) {  // 4 float4 per thread (at most kNormPer)
+  int t = (d / 4 + 3) / 4;
   if (t > 1024) t = 1024;
   return (t + 31) / 32 * 32;
 }
 
 cudaError_t residual_norm_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h, const uint16_t* norm_w,
                                  float eps, uint16_t* x_packed, int TM, cudaStream_t s) {
+  if (d / 4 > kNormPer * 1024) return cudaErrorInvalidValue;
   return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d)), 0, s, part, plan, M, d, h, norm_w, eps,
                     x_packed, TM, 0);
 }
@@ -226,38 +252,49 @@ cudaError_t residual_norm_launch(const float* part, const GemmPlanDev& plan, int
 cudaError_t residual_norm_rows_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h,
                                       const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
                                       int norm_row_begin, cudaStream_t s) {
+  if (d / 4 > kNormPer * 1024) return cudaErrorInvalidValue;
   return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d)), 0, s, part, plan, M, d, h, norm_w, eps,
                     x_packed, TM, norm_row_begin);
 }
 
 // ------------------------------------------------------------- SiLU(gate)*up
+// grid (column blocks, row groups): thread = 4 consecutive columns of `rows`
+// rows (8 for a long prefill, which would otherwise launch ~10^5 tiny CTAs;
+// 1 for a decode step, where latency wants the widest grid).
 __global__ void silu_mul_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int ffn,
-                                uint16_t* __restrict__ x, int TM) {
+                                uint16_t* __restrict__ x, int TM, int rows) {
   pdl_wait();
   pdl_trigger();
   const int f4 = ffn >> 2;
-  const size_t total = (size_t)M * f4;
+  const int j4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j4 >= f4) return;
   const size_t stride4 = (size_t)M * 2 * ffn / 4;
   const float4* p4 = reinterpret_cast<const float4*>(part);
-  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-    const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
-    float4 g = make_float4(0.f, 0.f, 0.f, 0.f), u = g;
+  const int m_end = min(M, (int)(blockIdx.y + 1) * rows);
+  const size_t col = act_col_off(j4 * 4, TM);
+  // silu(g) = g / (1 + e^-g) with the fast exp / divide (a few ulp of fp32,
+  // far below the bf16 rounding of the result)
+  auto silu = [](float g) { return __fdividef(g, 1.0f + __expf(-g)); };
+#pragma unroll 2
+  for (int m = blockIdx.y * rows; m < m_end; ++m) {
     const size_t base = (size_t)m * 2 * f4 + j4;
-    g = sum_slots4(p4 + base, stride4, part_slots(plan, m, j4 * 4));
-    u = sum_slots4(p4 + base + f4, stride4, part_slots(plan, m, ffn + j4 * 4));
+    const float4 g = part_ld4(plan, p4 + base, stride4, m, j4 * 4);
+    const float4 u = part_ld4(plan, p4 + base + f4, stride4, m, ffn + j4 * 4);
     uint2 o;
-    o.x = pack_bf2((g.x / (1.0f + expf(-g.x))) * u.x, (g.y / (1.0f + expf(-g.y))) * u.y);
-    o.y = pack_bf2((g.z / (1.0f + expf(-g.z))) * u.z, (g.w / (1.0f + expf(-g.w))) * u.w);
-    *reinterpret_cast<uint2*>(x + act_off(m, j4 * 4, ffn, TM)) = o;
+    o.x = pack_bf2(silu(g.x) * u.x, silu(g.y) * u.y);
+    o.y = pack_bf2(silu(g.z) * u.z, silu(g.w) * u.w);
+    *reinterpret_cast<uint2*>(x + act_row_off(m, ffn, TM) + col) = o;
   }
 }
 
 cudaError_t silu_mul_launch(const float* part, const GemmPlanDev& plan, int M, int ffn, uint16_t* x_packed, int TM,
                             cudaStream_t s) {
-  const size_t total = (size_t)M * ffn / 4;
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  return launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, s, part, plan, M, ffn, x_packed, TM);
+  const int f4 = ffn / 4;
+  const int rows = M >= 1024 ? 8 : 1;
+  const int gy = (M + rows - 1) / rows;
+  if (gy > 65535) return cudaErrorInvalidValue;
+  return launch_pdl(silu_mul_kernel, dim3((f4 + 255) / 256, gy), dim3(256), 0, s, part, plan, M, ffn, x_packed, TM,
+                    rows);
 }
 
 // ------------------------------------------------------ logits + greedy argmax

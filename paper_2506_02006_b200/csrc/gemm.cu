@@ -311,8 +311,9 @@ __device__ void gemm_tail_gang(const GemmEpi& e, const GemmPlanDev& plan, int M,
         if (idx >= i1) continue;
         const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
         uint2 o;
-        o.x = pack_bf2((g[j].x / (1.0f + expf(-g[j].x))) * u[j].x, (g[j].y / (1.0f + expf(-g[j].y))) * u[j].y);
-        o.y = pack_bf2((g[j].z / (1.0f + expf(-g[j].z))) * u[j].z, (g[j].w / (1.0f + expf(-g[j].w))) * u[j].w);
+        auto silu = [](float v) { return __fdividef(v, 1.0f + __expf(-v)); };  // as silu_mul_kernel
+        o.x = pack_bf2(silu(g[j].x) * u[j].x, silu(g[j].y) * u[j].y);
+        o.y = pack_bf2(silu(g[j].z) * u[j].z, silu(g[j].w) * u[j].w);
         *reinterpret_cast<uint2*>(e.x + act_off(m, j4 * 4, ffn, e.tm_out)) = o;
       }
     }

@@ -7,28 +7,32 @@
 // time in attention.  prefill_attention.cu does it with mma.sync (m16n8k16);
 // this kernel issues tcgen05.mma with 128x128 tiles.
 //
-// CTA = (128-query tile, query head), 10 warps, warp specialised:
-//   warp 8   TMA producer: per 128-key tile, 8 paged KV blocks x 2 column
-//            halves of K and of V with SWIZZLE_128B boxes {64 dims, 16 keys}
+// CTA = (128-query tile, query head), 11 warps, warp specialised:
+//   warps 8, 10  TMA producers for K and for V: per 128-key tile, 8 paged KV
+//            blocks x 2 column halves, SWIZZLE_128B boxes {64 dims, 16 keys}
 //            from a 2-D tensor map over the arena (rows of 256 B).  That image
 //            is directly a K-major SW128 operand for K (S = Q K^T) and an
 //            MN-major SW128 operand for V (O += P V): no transpose, no
-//            per-thread copies.  K and V each double buffered.
+//            per-thread copies.  K has 3 buffers (freed when S(kt) completes),
+//            V 2 (freed when PV(kt) completes); separate warps so neither
+//            queue waits behind the other.
 //   warp 9   MMA issuer (one elected lane of a converged warp):
-//            S(kt) = Q_hi K^T + Q_lo K^T (16 MMAs M128 N128 K16 into one of two
-//            TMEM S buffers; q = hi + lo bf16 keeps fp32-level score accuracy
-//            as the mma.sync kernel and the decode paths do), then
+//            S(kt) = Q_hi K^T + Q_lo K^T (16 MMAs M128 N128 K16 into one of
+//            three TMEM S buffers; q = hi + lo bf16 keeps fp32-level score
+//            accuracy as the mma.sync kernel and the decode paths do), then
 //            O += P(kt) V (8 MMAs, A = P read from TMEM, B = V MN-major).
-//            Order S(0), S(1), PV(0), S(2), PV(1), ...: S(kt+1) runs on the
-//            tensor cores while the softmax of tile kt runs.
+//            Order S(0), S(1), [S(kt+2), PV(kt)]...: the tensor cores run up to
+//            two S tiles ahead of the softmax.
 //   warps 0-7 softmax: thread = (query row = TMEM lane, half of the 128 keys);
 //            the halves of a row exchange maxima through shared memory under a
 //            pairwise named barrier.  Online softmax in the log2 domain (scale
 //            folded into q) with lazy rescaling: the running max moves only
 //            when a tile's max exceeds it by more than 2^8, so O (in TMEM) is
 //            rescaled a handful of times per row instead of every tile; the
-//            result is the same softmax (exact up to fp32 rounding).
-// TMEM: S [0,256) (two buffers), P [256,384) (two bf16 buffers), O [384,512).
+//            result is the same softmax (exact up to fp32 rounding).  P (bf16)
+//            is written over its own S columns.
+// TMEM: S/P [0,384) (three buffers), O [384,512).  CTAs run head-major,
+// longest query tiles first, so the K/V of the heads in flight stay in L2.
 #include <cstdint>
 #include <cstdlib>
 #include <cuda.h>
@@ -45,8 +49,11 @@ namespace {
 constexpr int kTcTile = 128;           // queries per CTA and keys per KV tile
 constexpr uint32_t kOpBytes = 32768;   // one 128 x 128 bf16 operand
 constexpr uint32_t kHalfBytes = 16384; // one 64-column half of it (SW128 image)
-constexpr uint32_t kTmemS = 0, kTmemP = 256, kTmemO = 384;
-constexpr int kThreads = 320;
+constexpr int kKStages = 3, kVStages = 2, kSBufs = 3;  // K / V tile buffers, S (and P) TMEM buffers
+constexpr uint32_t kTmemS = 0, kTmemO = 384;            // S: [0, 384), O: [384, 512)
+constexpr int kBars = kKStages * 2 + kVStages * 2 + kSBufs * 2 + 2;
+constexpr uint32_t kCtrlBytes = 2 * kTcTile * 4 + kBars * 8 + 16;  // row maxima, barriers, TMEM slot
+constexpr int kThreads = 352;
 constexpr float kRescaleLog2 = 8.f;    // lazy rescale threshold (log2 domain)
 
 // byte offset of the 16-B chunk (row r, k-chunk c) of a [128 rows][128 k] canonical
@@ -105,26 +112,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefill_attn_tc_kernel(PrefillAttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   constexpr int HD = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // SW128 atoms: 1024-B aligned
-  uint8_t* sQh = smem;                   // canonical no-swizzle (written by threads)
+  float* sRed = reinterpret_cast<float*>(smem_raw);  // [2 half][128] row maxima / sums
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 2 * kTcTile);
+  uint64_t* kfull = bar;                 // [kKStages]
+  uint64_t* kempty = kfull + kKStages;   // [kKStages]
+  uint64_t* vfull = kempty + kKStages;   // [kVStages]
+  uint64_t* vempty = vfull + kVStages;   // [kVStages]
+  uint64_t* sfull = vempty + kVStages;   // [kSBufs] S(kt) in TMEM buffer kt % kSBufs
+  uint64_t* pfull = sfull + kSBufs;      // [kSBufs] P(kt) written over S(kt) (8 softmax warps)
+  uint64_t* odone = pfull + kSBufs;      // PV(kt) accumulated into O
+  uint64_t* ofinal = odone + 1;          // every MMA done (single phase)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kBars);
+  // operands: 1024-B aligned (SW128 atoms)
+  uint8_t* ops = smem_raw + (((smem_u32(smem_raw) + kCtrlBytes + 1023u) & ~1023u) - smem_u32(smem_raw));
+  uint8_t* sQh = ops;                         // canonical no-swizzle, written by the softmax warps
   uint8_t* sQl = sQh + kOpBytes;
-  uint8_t* sK = sQl + kOpBytes;          // [2] SW128 images [dim half][key][128 B]
-  uint8_t* sV = sK + 2 * kOpBytes;       // [2] same
-  float* sRed = reinterpret_cast<float*>(sV + 2 * kOpBytes);  // [2 parity][2 half][128] row maxima
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 4 * kTcTile);
-  uint64_t* kfull = bar;       // [2]
-  uint64_t* vfull = bar + 2;   // [2]
-  uint64_t* kempty = bar + 4;  // [2]
-  uint64_t* vempty = bar + 6;  // [2]
-  uint64_t* sfull = bar + 8;   // [2] S(kt) in TMEM buffer kt & 1
-  uint64_t* pfull = bar + 10;  // [2] P(kt) in TMEM buffer kt & 1 (8 softmax warps)
-  uint64_t* odone = bar + 12;  // PV(kt) accumulated into O
-  uint64_t* ofinal = bar + 13; // every MMA done (single phase)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint8_t* sK = sQl + kOpBytes;               // [kKStages] SW128 images [dim half][key][128 B]
+  uint8_t* sV = sK + kKStages * kOpBytes;     // [kVStages] same
 
-  const int qtiles = gridDim.y;
-  const int qt = qtiles - 1 - (int)blockIdx.y;  // longest rows first
-  const int h = blockIdx.x;
+  // head-major, longest query tiles of a head first: the CTAs in flight share
+  // the K/V of two or three heads, which stay in L2
+  const int qtiles = (a.n + kTcTile - 1) / kTcTile;
+  const int h = (int)blockIdx.x / qtiles;
+  const int qt = qtiles - 1 - ((int)blockIdx.x - h * qtiles);
   const int kvh = h / (a.H / a.KVH);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = qt * kTcTile, n = a.n;
@@ -137,45 +147,63 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   pdl_wait();
   pdl_trigger();
-  // K or V of tile kt: 8 blocks (clamped to the last block: keys past the row
-  // are masked, and a clamped duplicate keeps them finite) x 2 column halves
-  auto load = [&](int kt, bool is_v) {
-    const int s = kt & 1;
+  // K or V of tile kt (whole producer warp): lane j < 8 holds the arena row of
+  // the tile's block j (clamped to the last block: keys past the row are
+  // masked) and issues its two column-half boxes.  The page ids of a tile are
+  // fetched one tile ahead, eight in parallel.
+  auto tile_row = [&](int kt) {
+    const int blk = min(kt * 8 + (lane & 7), last_blk);
+    return (int)(__ldg(a.pages + blk) * rows_per_page + head_row);
+  };
+  auto load = [&](int kt, bool is_v, int row) {
+    const int s = is_v ? kt % kVStages : kt % kKStages;
     uint64_t* fb = is_v ? &vfull[s] : &kfull[s];
-    const uint32_t dst = smem_u32((is_v ? sV : sK) + s * kOpBytes);
-    mbar_expect_tx(fb, kOpBytes);
-#pragma unroll 1
-    for (int j = 0; j < 8; ++j) {
-      const int blk = min(kt * 8 + j, last_blk);
-      const int row = (int)(__ldg(a.pages + blk) * rows_per_page + head_row) + (is_v ? v_rows : 0);
-      tma2d(dst + j * 2048, &tmap, 0, row, fb);
-      tma2d(dst + kHalfBytes + j * 2048, &tmap, 64, row, fb);
+    const uint32_t dst = smem_u32((is_v ? sV : sK) + s * kOpBytes) + (uint32_t)lane * 2048u;
+    if (lane == 0) mbar_expect_tx(fb, kOpBytes);
+    __syncwarp();
+    if (lane < 8) {
+      const int r = row + (is_v ? v_rows : 0);
+      tma2d(dst, &tmap, 0, r, fb);
+      tma2d(dst + kHalfBytes, &tmap, 64, r, fb);
     }
   };
+  int row_k = 0, row_v = 0;  // producers: page rows of the next K / V tile to load
   if (warp == 8) {
     if (lane == 0) {
-      for (int i = 0; i < 14; ++i) mbar_init(&bar[i], (i == 10 || i == 11) ? 8 : 1);
+      for (int i = 0; i < kBars; ++i) mbar_init(&bar[i], (&bar[i] >= pfull && &bar[i] < pfull + kSBufs) ? 8 : 1);
       fence_mbar_init();
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-      for (int kt = 0; kt < min(2, n_ktiles); ++kt) {
-        load(kt, false);
-        load(kt, true);
-      }
     }
     __syncwarp();
+    for (int kt = 0; kt < min(kKStages, n_ktiles); ++kt) {
+      const int row = tile_row(kt);
+      load(kt, false, row);
+      if (kt < kVStages) load(kt, true, row);
+    }
+    if (n_ktiles > kKStages) row_k = tile_row(kKStages);
   }
+  if (warp == 10 && n_ktiles > kVStages) row_v = tile_row(kVStages);
   if (warp == 9) tmem_alloc<512>(tmem_slot);
 
-  // ---- Q tile (softmax warps): fp32 * scale_log2 -> (hi, lo) bf16, canonical layout
+  // ---- Q tile (softmax warps): fp32 * scale_log2 -> (hi, lo) bf16, canonical layout;
+  // all 16 loads of a thread in flight at once (the CTA's first S waits on this)
   if (warp < 8) {
-    for (int idx = threadIdx.x; idx < kTcTile * 16; idx += 256) {
-      const int r = idx >> 4, c = idx & 15;
-      const int q = q0 + r;
+    float4 x[8][2];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int idx = threadIdx.x + it * 256, r = idx >> 4, c = idx & 15;
+      const int q = min(q0 + r, n - 1);
+      const float4* src = reinterpret_cast<const float4*>(a.q + ((size_t)q * a.H + h) * HD + c * 8);
+      x[it][0] = __ldg(src);
+      x[it][1] = __ldg(src + 1);
+    }
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int idx = threadIdx.x + it * 256, r = idx >> 4, c = idx & 15;
       uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
-      if (q < n) {
-        const float4* src = reinterpret_cast<const float4*>(a.q + ((size_t)q * a.H + h) * HD + c * 8);
-        const float4 x0 = src[0], x1 = src[1];
+      if (q0 + r < n) {
         const float sl = a.scale_log2;  // scores come out of the MMA already in the log2 domain
+        const float4 x0 = x[it][0], x1 = x[it][1];
         const float v[8] = {x0.x * sl, x0.y * sl, x0.z * sl, x0.w * sl, x1.x * sl, x1.y * sl, x1.z * sl, x1.w * sl};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -195,15 +223,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 8) {
-    // ---------------------------------------------------------- producer
-    if (lane == 0) {
-      for (int kt = 2; kt < n_ktiles; ++kt) {
-        const uint32_t par = ((kt >> 1) - 1) & 1;
-        mbar_wait(&kempty[kt & 1], par);  // S(kt - 2) read K buffer kt & 1
-        load(kt, false);
-        mbar_wait(&vempty[kt & 1], par);  // PV(kt - 2) read V buffer kt & 1
-        load(kt, true);
-      }
+    // ------------------------------------------------------ K producer
+    // K(kt) as soon as S(kt - kKStages) released its buffer
+    for (int kt = kKStages; kt < n_ktiles; ++kt) {
+      const int rw = row_k;
+      if (kt + 1 < n_ktiles) row_k = tile_row(kt + 1);
+      mbar_wait(&kempty[kt % kKStages], ((kt / kKStages) - 1) & 1);
+      load(kt, false, rw);
+    }
+    __syncwarp();
+  } else if (warp == 10) {
+    // ------------------------------------------------------ V producer
+    // V(kt) as soon as PV(kt - kVStages) released its buffer
+    for (int kt = kVStages; kt < n_ktiles; ++kt) {
+      const int rw = row_v;
+      if (kt + 1 < n_ktiles) row_v = tile_row(kt + 1);
+      mbar_wait(&vempty[kt % kVStages], ((kt / kVStages) - 1) & 1);
+      load(kt, true, rw);
     }
     __syncwarp();
   } else if (warp == 9) {
@@ -211,36 +247,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc = umma_idesc_bf16(128, 128);
     const uint32_t idesc_pv = idesc | (1u << 16);  // B (= V) MN-major
     const uint64_t dQh = umma_desc(smem_u32(sQh), 128u, 2048u), dQl = umma_desc(smem_u32(sQl), 128u, 2048u);
-    auto issue_s = [&](int kt) {
-      const int s = kt & 1;
-      mbar_wait(&kfull[s], (kt >> 1) & 1);
+    auto issue_s = [&](int kt) {  // S(kt) = Q_hi K^T + Q_lo K^T into S buffer kt % kSBufs
+      const int s = kt % kKStages;
+      mbar_wait(&kfull[s], (kt / kKStages) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint64_t dK = desc_sw128(smem_u32(sK + s * kOpBytes), 16u, 1024u);
-        const uint32_t d = tmem + kTmemS + (uint32_t)s * 128u;
+        const uint32_t d = tmem + kTmemS + (uint32_t)(kt % kSBufs) * 128u;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           const uint64_t dk = desc_add(dK, (uint32_t)(ks >> 2) * kHalfBytes + (uint32_t)(ks & 3) * 32u);
           umma_bf16(d, desc_add(dQh, ks * 256u), dk, idesc, ks ? 1u : 0u);
           umma_bf16(d, desc_add(dQl, ks * 256u), dk, idesc, 1u);
         }
-        umma_commit(&sfull[s]);
+        umma_commit(&sfull[kt % kSBufs]);
         umma_commit(&kempty[s]);
       }
       __syncwarp();
     };
-    issue_s(0);
+    for (int kt = 0; kt < min(kSBufs - 1, n_ktiles); ++kt) issue_s(kt);
     for (int kt = 0; kt < n_ktiles; ++kt) {
-      if (kt + 1 < n_ktiles) issue_s(kt + 1);  // S buffer (kt+1)&1 was released by P(kt-1)
-      const int s = kt & 1;
-      mbar_wait(&pfull[s], (kt >> 1) & 1);
-      mbar_wait(&vfull[s], (kt >> 1) & 1);
+      // S buffer (kt+2) % 3 held P(kt-1): its softmax finished (pfull waited
+      // last iteration) and PV(kt-1), which reads it, was issued before --
+      // tcgen05 MMAs of one CTA execute in issue order
+      if (kt + kSBufs - 1 < n_ktiles) issue_s(kt + kSBufs - 1);
+      const int sb = kt % kSBufs, sv = kt % kVStages;
+      mbar_wait(&pfull[sb], (kt / kSBufs) & 1);
+      mbar_wait(&vfull[sv], (kt / kVStages) & 1);
       const int r0 = q_last + 1 - kt * kTcTile;
       if (kt == n_ktiles - 1 && r0 < kTcTile) {
         // keys past the row (the rest of its last block and the clamped
         // duplicates): zero their V rows -- P is 0 there, but the arena bytes
         // past the sequence are arbitrary and 0 * NaN would not be 0
-        uint8_t* vb = sV + s * kOpBytes;
+        uint8_t* vb = sV + sv * kOpBytes;
         for (int i = lane; i < (kTcTile - r0) * 16; i += 32) {
           const int r = r0 + (i >> 4), c = i & 15;
           *reinterpret_cast<uint4*>(vb + (c >> 3) * kHalfBytes + r * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
@@ -250,12 +289,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_after();
       if (elect_one()) {
-        const uint64_t dV = desc_sw128(smem_u32(sV + s * kOpBytes), kHalfBytes, 1024u);
+        const uint64_t dV = desc_sw128(smem_u32(sV + sv * kOpBytes), kHalfBytes, 1024u);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          umma_bf16_ts(tmem + kTmemO, tmem + kTmemP + (uint32_t)s * 64u + ks * 8u, desc_add(dV, ks * 2048u),
+          umma_bf16_ts(tmem + kTmemO, tmem + kTmemS + (uint32_t)sb * 128u + ks * 8u, desc_add(dV, ks * 2048u),
                        idesc_pv, (kt | ks) ? 1u : 0u);
-        umma_commit(&vempty[s]);
+        umma_commit(&vempty[sv]);
         umma_commit(odone);
         if (kt == n_ktiles - 1) umma_commit(ofinal);
       }
@@ -270,11 +309,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int pair_bar = 1 + (warp & 3);
     float m_run = -INFINITY, l_half = 0.f;
     for (int kt = 0; kt < n_ktiles; ++kt) {
-      const int s = kt & 1;
-      mbar_wait(&sfull[s], (kt >> 1) & 1);
+      const int sb = kt % kSBufs;
+      mbar_wait(&sfull[sb], (kt / kSBufs) & 1);
       tc_fence_after();
       uint32_t v[64];
-      const uint32_t scol = tmem + lane_off + kTmemS + (uint32_t)s * 128u + (uint32_t)(half * 64);
+      const uint32_t scol = tmem + lane_off + kTmemS + (uint32_t)sb * 128u + (uint32_t)(half * 64);
       tmem_ld32(scol, v);
       tmem_ld32(scol + 32, v + 32);
       tmem_ld_wait();
@@ -285,13 +324,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 64; ++j)
           if (key0 + j > qrow || key0 + j >= n) v[j] = __float_as_uint(-INFINITY);
       }
-      float mx = __uint_as_float(v[0]);
+      float m4[4];  // four independent chains
 #pragma unroll
-      for (int j = 1; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
-      float* red = sRed + s * 2 * kTcTile;
-      red[half * kTcTile + row] = mx;
+      for (int k = 0; k < 4; ++k) m4[k] = __uint_as_float(v[k]);
+#pragma unroll
+      for (int j = 4; j < 64; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      if (kt > 0) asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // partner read the last maxima
+      sRed[half * kTcTile + row] = mx;
       asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-      const float m_tile = fmaxf(red[row], red[kTcTile + row]);
+      const float m_tile = fmaxf(sRed[row], sRed[kTcTile + row]);
       const bool move = m_tile > m_run + kRescaleLog2;  // false while both are -inf
       const float m_new = move ? m_tile : m_run;
       const float corr = (move && m_run != -INFINITY) ? ex2(m_run - m_new) : 1.f;
@@ -312,29 +354,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       m_run = m_new;
       const float msub = m_new == -INFINITY ? 0.f : m_new;
-      float psum = 0.f;
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[32];
 #pragma unroll
       for (int j = 0; j < 64; j += 2) {
         const float p0 = ex2(__uint_as_float(v[j]) - msub);
         const float p1 = ex2(__uint_as_float(v[j + 1]) - msub);
-        psum += p0 + p1;
+        ps[(j >> 1) & 3] += p0 + p1;
         pk[j >> 1] = cvt_bf2(p0, p1);
       }
-      l_half = l_half * corr + psum;
-      tmem_st32p(tmem + lane_off + kTmemP + (uint32_t)s * 64u + (uint32_t)(half * 32), pk);
+      l_half = l_half * corr + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
+      tmem_st32p(tmem + lane_off + kTmemS + (uint32_t)sb * 128u + (uint32_t)(half * 32), pk);  // P over S
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[s]);
+      if (lane == 0) mbar_arrive(&pfull[sb]);
     }
     // ---- epilogue: O / l
     mbar_wait(ofinal, 0);
     tc_fence_after();
-    float* lsum = sRed + (((n_ktiles - 1) & 1) ? 0 : 2 * kTcTile);  // the parity buffer the last tile did not use
-    lsum[half * kTcTile + row] = l_half;
+    asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // partner read the last maxima
+    sRed[half * kTcTile + row] = l_half;
     asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-    const float l = lsum[row] + lsum[kTcTile + row];
+    const float l = sRed[row] + sRed[kTcTile + row];
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const int K = a.H * HD;
     const uint32_t ocol = tmem + lane_off + kTmemO + (uint32_t)(half * 64);
@@ -398,13 +440,14 @@ cudaError_t prefill_attn_tc_launch(const PrefillAttnArgs& a, cudaStream_t stream
     map_bytes = a.arena_bytes;
   }
   const int qtiles = (a.n + kTcTile - 1) / kTcTile;
-  const size_t smem = 1024 + 6 * (size_t)kOpBytes + 4 * kTcTile * 4 + 16 * 8;
+  const size_t smem = kCtrlBytes + 1024 + (size_t)(2 + kKStages + kVStages) * kOpBytes;
+  if (smem > 227 * 1024) return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  return launch_pdl(prefill_attn_tc_kernel, dim3(a.H, qtiles), dim3(kThreads), smem, stream, a, tmap);
+  return launch_pdl(prefill_attn_tc_kernel, dim3(a.H * qtiles), dim3(kThreads), smem, stream, a, tmap);
 }
 
 }  // namespace ms

@@ -201,6 +201,15 @@ __device__ __forceinline__ float warp_sum(float v) {
 // Packed activation layout (GEMM B operand image): element (m, k)
 // of an [M x K] matrix lives in chunk (m/TM, k/64) of TM*64 elements, at
 // [row_group (m%TM)/8][k_chunk (k%64)/8][row m%8][k%8].
+// act_off(m, k) = act_row_off(m) + act_col_off(k): the row part once per row,
+// the column part once per thread, in the row kernels' inner loops.
+__device__ __forceinline__ size_t act_row_off(int m, int K, int TM) {
+  const int mt = m / TM, r = m - mt * TM;
+  return (size_t)mt * (K >> 6) * TM * 64 + (size_t)((r >> 3) * 512 + (r & 7) * 8);
+}
+__device__ __forceinline__ size_t act_col_off(int k, int TM) {
+  return (size_t)(k >> 6) * TM * 64 + (size_t)(((k & 63) >> 3) * 64 + (k & 7));
+}
 __device__ __forceinline__ size_t act_off(int m, int k, int K, int TM) {
   const int mt = m / TM, r = m - mt * TM, kb = k >> 6, kk = k & 63;
   return ((size_t)mt * (K >> 6) + kb) * (size_t)TM * 64 + (size_t)((((r >> 3) * 8 + (kk >> 3)) * 8 + (r & 7)) * 8 + (kk & 7));
