@@ -112,6 +112,18 @@ def cpu_sample(batch: int, ctx: int, w4: bool):
     return layer_s, lm.value, L.ref_num_threads()
 
 
+def ncu_traffic():
+    """DRAM bytes per attention launch from the committed ncu --set full capture
+    of this workload (profiles/attn_decode_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "attn_decode_traffic.json")) as f:
+            t = json.load(f)
+        return {"bytes_per_launch": t["dram_bytes_read_per_launch"] + t["dram_bytes_write_per_launch"],
+                "source": t["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def cpu_baseline():
     ls16, lm, threads = cpu_sample(BATCH, CTX, False)
     ls4, _, _ = cpu_sample(BATCH, CTX, True)
@@ -459,9 +471,12 @@ def run_ours(args):
         "e2e": {"value": BATCH * args.e2e_steps * world / e2e_s, "unit": "tok/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "attn_decode_kernel (paged GQA decode attention)",
+        "roofline": {"bound": "hbm", "kernel": "attn_decode_kernel (paged decode attention, MHA warp-per-block)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_kind": peak_kind, "traffic": None,
+                     "peak_kind": peak_kind, "traffic": (ncu_traffic() or {}).get("bytes_per_launch"),
+                     "traffic_unit": "bytes per launch (ncu dram read + write)",
+                     "algorithmic_bytes_per_launch": attn_bytes / max(attn_n, 1),
+                     "traffic_source": (ncu_traffic() or {}).get("source"),
                      "share_of_step": attn_ms / ms_prof if ms_prof > 0 else None},
         "clocks": clk.summary(),
     }

@@ -236,8 +236,10 @@ __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __rest
   }
 }
 
-static int norm_threads(int d) {  // 4 float4 per thread (at most kNormPer)
-  int t = (d / 4 + 3) / 4;
+// A long prefill (thousands of rows) wants 4 float4 per thread; a decode step
+// (tens of rows) wants the widest CTA: one float4 per thread.
+static int norm_threads(int d, int M) {
+  int t = M >= 1024 ? (d / 4 + 3) / 4 : d / 4;
   if (t > 1024) t = 1024;
   return (t + 31) / 32 * 32;
 }
@@ -245,7 +247,7 @@ static int norm_threads(int d) {  // 4 float4 per thread (at most kNormPer)
 cudaError_t residual_norm_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h, const uint16_t* norm_w,
                                  float eps, uint16_t* x_packed, int TM, cudaStream_t s) {
   if (d / 4 > kNormPer * 1024) return cudaErrorInvalidValue;
-  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d)), 0, s, part, plan, M, d, h, norm_w, eps,
+  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d, M)), 0, s, part, plan, M, d, h, norm_w, eps,
                     x_packed, TM, 0);
 }
 
@@ -253,7 +255,7 @@ cudaError_t residual_norm_rows_launch(const float* part, const GemmPlanDev& plan
                                       const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
                                       int norm_row_begin, cudaStream_t s) {
   if (d / 4 > kNormPer * 1024) return cudaErrorInvalidValue;
-  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d)), 0, s, part, plan, M, d, h, norm_w, eps,
+  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d, M)), 0, s, part, plan, M, d, h, norm_w, eps,
                     x_packed, TM, norm_row_begin);
 }
 
