@@ -197,7 +197,7 @@ def dev_layer_pages(bits):
     return layer_pages(SHAPE, bits)
 
 
-def serve_arms(dev, wl, arms_csv, rank, world, note, budget_gib=24.0):
+def serve_arms(dev, wl, arms_csv, rank, world, note, budget_gib=24.0, wl_key="gamma"):
     """Each arm of one bursty trace through the C++ engine on `dev` (GPU clock)."""
     from paper_2506_02006_b200 import serving as S
     from paper_2506_02006_b200.replicas import merge_reports
@@ -212,7 +212,7 @@ def serve_arms(dev, wl, arms_csv, rank, world, note, budget_gib=24.0):
             dist.all_gather_object(allr, rep)
             summ["union"] = merge_reports(allr)
         if out is None:
-            out = dict(summ, arm=arm, workload=wl["gamma"], budget_gib=budget_gib, note=note)
+            out = dict(summ, arm=arm, workload=wl[wl_key], budget_gib=budget_gib, note=note)
         else:
             out.setdefault("baselines", {})[arm] = summ
     return out
@@ -234,6 +234,34 @@ def serve_8b(args, local_rank, rank, world):
                         "total_ms": int(args.serve8b_seconds * 1000), "prompt_tokens": 1024, "output_tokens": 512}}
         return serve_arms(dev, wl, args.serve_arms, rank, world,
                           "Llama-3-8B shape (BASELINE configs[2]), 24 GiB device budget, measured-GPU-clock engine run")
+    finally:
+        dev.close()
+
+
+def serve_13b(args, local_rank, rank, world):
+    """BASELINE configs[3] as a serving burst: Llama-2-13B shape, Poisson arrivals (16 rps)
+    with 8192-token prompts arriving within 1 s (reference synth_burst), 128
+    output tokens, under a 44 GiB device budget (two 8k contexts fit beside the
+    BF16 weights).  Every prefill and decode step is a real B200 step (GPU
+    clock); the morph arm swaps layers to W4A16 and carves the freed pages into
+    KV blocks, the static arm keeps all 40 layers BF16."""
+    from paper_2506_02006_b200.device import LLAMA2_13B, DeviceModel, layer_pages, page_bytes
+    shape = dict(LLAMA2_13B)
+    pb = page_bytes(shape)
+    budget_gib = 44.0
+    budget_pages = int(budget_gib * (1 << 30)) // pb
+    n_max = 8192 + 128 + 16
+    dev = DeviceModel(shape, device=local_rank, max_batch=32, max_prefill_tokens=n_max, max_pos=n_max + 32,
+                      arena_pages=budget_pages + 2 * layer_pages(shape, 16) + 64)
+    try:
+        dev.weights_synthetic(7)
+        wl = {"synth": {"seed": 101 + rank, "base_rps": 0.001, "burst_rps": float(args.serve13b_rps),
+                        "burst_start_ms": 0, "burst_len_ms": 1000, "total_ms": 1000,
+                        "prompt_tokens": 8192, "output_tokens": 128}}
+        out = serve_arms(dev, wl, args.serve_arms, rank, world,
+                         "Llama-2-13B shape (BASELINE configs[3]), 8k-prompt burst, 44 GiB device budget, "
+                         "measured-GPU-clock engine run", budget_gib=budget_gib, wl_key="synth")
+        return out
     finally:
         dev.close()
 
@@ -485,6 +513,8 @@ def run_ours(args):
         line["serving_8b"] = serve_8b(args, local_rank, rank, world)
     if args.prefill_tokens > 0:
         line["prefill_13b"] = prefill_13b(args, local_rank)
+    if args.serve13b_rps > 0:
+        line["serving_13b"] = serve_13b(args, local_rank, rank, world)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
@@ -511,6 +541,8 @@ def main():
     ap.add_argument("--prefill-tokens", type=int, default=8192,
                     help="Llama-2-13B long-prompt prefill, BASELINE configs[3] (0 = skip)")
     ap.add_argument("--prefill-reps", type=int, default=3)
+    ap.add_argument("--serve13b-rps", type=float, default=16.0,
+                    help="Llama-2-13B 8k-prompt burst: Poisson arrivals at this rate for 1 s, BASELINE configs[3] (0 = skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -1094,15 +1094,10 @@ int ms_reset_state(ms_ctx* c) {
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->compute));
     CK(cudaStreamSynchronize(c->copy));
-    for (int l = 0; l < c->desc.num_layers; ++l) {
-      Layer& L = c->layers[l];
-      if (L.in_flight) fail(MS_ELOGIC, "reset: swap in flight");
-      if (L.bits == 16) continue;
-      uint64_t t = 0;
-      if (ms_swap_begin(c, l, 16, &t) != MS_OK) fail(MS_ERUNTIME, g_err);
-      CK(cudaStreamSynchronize(c->copy));
-      if (ms_swap_commit(c, t, nullptr) != MS_OK) fail(MS_ERUNTIME, g_err);
-    }
+    for (int l = 0; l < c->desc.num_layers; ++l)
+      if (c->layers[l].in_flight) fail(MS_ELOGIC, "reset: swap in flight");
+    // KV pages first: the BF16 restores below may need the pages the KV
+    // resizer carved out of the W4 layers' freed images
     std::vector<int32_t> pages;
     for (auto& p : c->id_page)
       if (p >= 0) {
@@ -1110,6 +1105,14 @@ int ms_reset_state(ms_ctx* c) {
         p = -1;
       }
     give_pages(c, pages, compute_fence(c));
+    CK(cudaStreamSynchronize(c->compute));
+    for (int l = 0; l < c->desc.num_layers; ++l) {
+      if (c->layers[l].bits == 16) continue;
+      uint64_t t = 0;
+      if (ms_swap_begin(c, l, 16, &t) != MS_OK) fail(MS_ERUNTIME, g_err);
+      CK(cudaStreamSynchronize(c->copy));
+      if (ms_swap_commit(c, t, nullptr) != MS_OK) fail(MS_ERUNTIME, g_err);
+    }
     CK(cudaStreamSynchronize(c->compute));
   });
 }
