@@ -146,3 +146,37 @@ def test_pipelined_decode_matches_synchronous(dev):
         assert all(np.array_equal(a, b) for a, b in zip(sync, got))
     finally:
         dev.kv_detach(list(range(200, 216)))
+
+
+def test_long_prefill_w4_layers_dequant_path():
+    """A prefill of >= 512 tokens runs W4A16 layers as BF16 GEMMs over a
+    dequantised copy of each matrix (runtime.cu w4_as_bf16); the weights are
+    the same bf16(code * scale), so the logits match the oracle with those
+    layers at W4."""
+    from paper_2506_02006_b200.device import DeviceModel
+    P = 700
+    m = DeviceModel(TINY, max_batch=4, max_prefill_tokens=1024, max_pos=1024, arena_pages=512)
+    try:
+        m.weights_synthetic(7)
+        ref = O.RefModel(dict(TINY, max_pos=1024), 7)
+        for l in (0, 2):
+            t = m.swap_begin(l, 4)
+            m.swap_wait(t)
+            m.swap_commit(t)
+            ref.set_precision(l, 4)
+        rng = np.random.default_rng(11)
+        prompt = rng.integers(0, TINY["V"], size=P).astype(np.int32)
+        m.hist_reserve(1, 1024)
+        nb = 1024 // 16
+        m.kv_attach(0, nb)
+        table = np.arange(nb, dtype=np.int64)[::-1].copy()
+        m.hist_write(0, 0, prompt)
+        tok, logits = m.prefill(0, P, table, want_logits=True)
+        seq = ref.new_seq(1024)
+        rtok, rlog = ref.prefill(seq, prompt)
+        _check_logits(logits, rlog)
+        if tok != rtok:
+            assert rlog[rtok] - rlog[tok] <= 2e-3 * np.max(np.abs(rlog))
+        ref.close()
+    finally:
+        m.close()
