@@ -93,21 +93,51 @@ struct ChunkCursor {
 };
 
 // Segment walker shared by every role so they all see the same sequence.
+// Stream-K plans: CTA c takes the contiguous k-step range [T c / C, T (c+1) / C).
+// Whole-tile plans (long prefills): CTA c takes logical tiles c, c + C, ...,
+// so the C tiles in flight at any time are C consecutive logical tiles, and
+// logical tiles are rastered in groups of kRasterM token tiles (all weight
+// tiles of a group before the next): the tiles in flight then share ~8 token
+// tiles and ~C/8 weight tiles, whose k-slices stay in L2 (group size = the
+// plan's `aligned` field, MS_GEMM_RASTER, default 8) (contiguous ranges
+// per CTA had every CTA streaming its own A and B from DRAM: 6-8 GB per
+// prefill GEMM instead of ~0.5 GB).
 struct SegIter {
   int64_t g, g1;
   int nk;
-  __device__ SegIter(const GemmPlanDev& p, int c) : nk(p.nk) {
-    if (p.aligned) {
-      const int64_t t0 = (int64_t)p.tiles * c / p.C, t1 = (int64_t)p.tiles * (c + 1) / p.C;
-      g = t0 * p.nk;
-      g1 = t1 * p.nk;
+  int u, tiles, C, n_tiles, m_tiles, rm;
+  bool al;
+  __device__ SegIter(const GemmPlanDev& p, int c) : nk(p.nk), al(p.aligned != 0) {
+    if (al) {
+      rm = p.aligned;  // raster group: token tiles per group
+      u = c;
+      tiles = p.tiles;
+      C = p.C;
+      n_tiles = p.n_tiles;
+      m_tiles = p.tiles / p.n_tiles;
+      g = g1 = 0;
     } else {
       g = p.T * c / p.C;
       g1 = p.T * (c + 1) / p.C;
     }
   }
+  __device__ int raster(int v) const {
+    const int grp = v / (rm * n_tiles);
+    const int r = v - grp * rm * n_tiles;
+    const int gm = min(rm, m_tiles - grp * rm);
+    const int nt = r / gm;
+    return (grp * rm + (r - nt * gm)) * n_tiles + nt;
+  }
   // next segment: tile t, k-steps [k0, k1)
   __device__ bool next(int& t, int& k0, int& k1) {
+    if (al) {
+      if (u >= tiles) return false;
+      t = raster(u);
+      k0 = 0;
+      k1 = nk;
+      u += C;
+      return true;
+    }
     if (g >= g1) return false;
     t = (int)(g / nk);
     k0 = (int)(g - (int64_t)t * nk);
@@ -1028,8 +1058,17 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
   const bool fits32 = (p.T + 1) * (int64_t)p.C < ((int64_t)1 << 31);
   if (fits32)
     for (int t = 0; t < p.tiles; ++t) max_slots = std::max(max_slots, plan_count(p, t));
-  if (!fits32 || (size_t)max_slots * M * N > part_elems) {  // fall back to whole tiles per CTA
-    p.aligned = 1;
+  // whole tiles per CTA when stream-K cannot hold its partial slots, or when
+  // there are >= 4 waves of tiles: the partial last wave then costs little,
+  // and the round-robin raster (SegIter) keeps the tiles in flight in L2,
+  // where contiguous stream-K ranges spread them over the whole matrix
+  if (!fits32 || (size_t)max_slots * M * N > part_elems || p.tiles >= 4 * num_sms) {
+    static const int raster = [] {
+      const char* e = std::getenv("MS_GEMM_RASTER");
+      const int v = e ? std::atoi(e) : 8;
+      return v < 1 ? 1 : v;
+    }();
+    p.aligned = raster;
     p.C = std::min(num_sms, p.tiles);
     max_slots = 1;
   }

@@ -66,7 +66,7 @@ void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages);
 // contiguous ranges (one persistent CTA each).  CTA c covers global k-steps
 // [floor(c*T/C), floor((c+1)*T/C)); a tile t touched by several CTAs gets one
 // fp32 partial slot per CTA (slot = c - first CTA of t).  `aligned` = whole
-// tiles per CTA (one slot).  Consumers sum part_slots() slots of [slot][M][N]
+// tiles per CTA (one slot; the value is the raster group, see SegIter).  Consumers sum part_slots() slots of [slot][M][N]
 // in slot order, so the result is deterministic.
 struct GemmPlanDev {
   int64_t T;
