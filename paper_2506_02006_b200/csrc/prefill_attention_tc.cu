@@ -51,7 +51,7 @@ constexpr uint32_t kOpBytes = 32768;   // one 128 x 128 bf16 operand
 constexpr uint32_t kHalfBytes = 16384; // one 64-column half of it (SW128 image)
 constexpr int kKStages = 3, kVStages = 2, kSBufs = 3;  // K / V tile buffers, S (and P) TMEM buffers
 constexpr uint32_t kTmemS = 0, kTmemO = 384;            // S: [0, 384), O: [384, 512)
-constexpr int kBars = kKStages * 2 + kVStages * 2 + kSBufs * 2 + 2;
+constexpr int kBars = kKStages * 2 + kVStages * 2 + kSBufs * 2 + 3;
 constexpr uint32_t kCtrlBytes = 2 * kTcTile * 4 + kBars * 8 + 16;  // row maxima, barriers, TMEM slot
 constexpr int kThreads = 352;
 constexpr float kRescaleLog2 = 8.f;    // lazy rescale threshold (log2 domain)
@@ -120,8 +120,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* vempty = vfull + kVStages;   // [kVStages]
   uint64_t* sfull = vempty + kVStages;   // [kSBufs] S(kt) in TMEM buffer kt % kSBufs
   uint64_t* pfull = sfull + kSBufs;      // [kSBufs] P(kt) written over S(kt) (8 softmax warps)
-  uint64_t* odone = pfull + kSBufs;      // PV(kt) accumulated into O
-  uint64_t* ofinal = odone + 1;          // every MMA done (single phase)
+  // [2] PV(kt) accumulated into O, on odone[kt & 1]: S(kt) is issued before
+  // PV(kt-2), so when the softmax of tile kt runs PV(kt-2) may still be in
+  // flight -- a single barrier could then be two phases behind and its parity
+  // wait for PV(kt-1) would pass early; per parity it is at most one behind
+  uint64_t* odone = pfull + kSBufs;
+  uint64_t* ofinal = odone + 2;          // every MMA done (single phase)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kBars);
   // operands: 1024-B aligned (SW128 atoms)
   uint8_t* ops = smem_raw + (((smem_u32(smem_raw) + kCtrlBytes + 1023u) & ~1023u) - smem_u32(smem_raw));
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_bf16_ts(tmem + kTmemO, tmem + kTmemS + (uint32_t)sb * 128u + ks * 8u, desc_add(dV, ks * 2048u),
                        idesc_pv, (kt | ks) ? 1u : 0u);
         umma_commit(&vempty[sv]);
-        umma_commit(odone);
+        umma_commit(&odone[kt & 1]);
         if (kt == n_ktiles - 1) umma_commit(ofinal);
       }
       __syncwarp();
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float corr = (move && m_run != -INFINITY) ? ex2(m_run - m_new) : 1.f;
       if (kt > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
         // O holds PV(0 .. kt-1): wait for the last of them, then rescale this row half
-        mbar_wait(odone, (kt - 1) & 1);
+        mbar_wait(&odone[(kt - 1) & 1], ((kt - 1) >> 1) & 1);
         tc_fence_after();
         const uint32_t ocol = tmem + lane_off + kTmemO + (uint32_t)(half * 64);
 #pragma unroll
