@@ -96,7 +96,10 @@ def _run_gemm(bits, W, X, TM, splits=0):
 
 @pytest.mark.parametrize("Nn,K,M,TM,splits", [
     (128, 128, 1, 16, 1), (256, 256, 4, 16, 0), (512, 768, 33, 48, 3), (1024, 4096, 64, 64, 0),
-    (384, 1024, 300, 256, 1), (128, 128, 16, 16, 2)])
+    (384, 1024, 300, 256, 1), (128, 128, 16, 16, 2),
+    # >= 4 waves of tiles: whole tiles per CTA, round-robin through the grouped
+    # raster (gemm.cu SegIter), including a partial last group of token tiles
+    (512, 256, 2500, 256, 3), (5120, 128, 4096, 256, 0)])
 def test_gemm_bf16(Nn, K, M, TM, splits):
     W = O.gen_weight(21, 1, Nn * K, 1 / np.sqrt(K)).reshape(Nn, K)
     X = O.gen_weight(21, 2, M * K, 1.0).reshape(M, K)
@@ -108,7 +111,8 @@ def test_gemm_bf16(Nn, K, M, TM, splits):
 
 
 @pytest.mark.parametrize("Nn,K,M,TM,splits", [
-    (128, 128, 1, 16, 1), (256, 768, 4, 16, 0), (512, 1024, 64, 64, 0), (256, 256, 200, 208, 1)])
+    (128, 128, 1, 16, 1), (256, 768, 4, 16, 0), (512, 1024, 64, 64, 0), (256, 256, 200, 208, 1),
+    (512, 256, 2500, 256, 3)])
 def test_gemm_w4(Nn, K, M, TM, splits):
     W = O.gen_weight(22, 1, Nn * K, 1 / np.sqrt(K)).reshape(Nn, K)
     X = O.gen_weight(22, 2, M * K, 1.0).reshape(M, K)
