@@ -176,7 +176,7 @@ __device__ void gemm_tail_gang(const GemmEpi& e, const GemmPlanDev& plan, int M,
   };
   if (threadIdx.x == 0) {
     __threadfence();  // this CTA's partial stores before its arrival
-    s_rank = atomicAdd(e.ctr, 1u) - e.base;
+    s_rank = atomicAdd(&e.ctr[0], 1u);
     if (e.tl) e.tl[blockIdx.x * 4 + 1] = gt();
   }
   __syncthreads();
@@ -186,8 +186,15 @@ __device__ void gemm_tail_gang(const GemmEpi& e, const GemmPlanDev& plan, int M,
   if (rank < C - nh) return;
   const int hid = rank - (C - nh);
   if (threadIdx.x == 0) {
-    while ((int)(*reinterpret_cast<volatile uint32_t*>(e.ctr) - e.base) < C) __nanosleep(64);
+    while ((int)*reinterpret_cast<volatile uint32_t*>(&e.ctr[0]) < C) __nanosleep(64);
     __threadfence();
+    // the pair resets itself for its next use once every helper is past the
+    // wait (every CTA has arrived by then); nothing host-side tracks counts, so
+    // the same launch replays correctly from a CUDA graph
+    if (atomicAdd(&e.ctr[1], 1u) == (uint32_t)nh - 1) {
+      atomicExch(&e.ctr[1], 0u);
+      atomicExch(&e.ctr[0], 0u);
+    }
     if (e.tl) e.tl[blockIdx.x * 4 + 2] = gt();
   }
   __syncthreads();

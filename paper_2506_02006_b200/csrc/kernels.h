@@ -99,8 +99,7 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
 enum { kEpiNone = 0, kEpiResidualNorm = 1, kEpiSiluMul = 2 };
 struct GemmEpi {
   int op = kEpiNone;
-  uint32_t* ctr = nullptr;
-  uint32_t base = 0;
+  uint32_t* ctr = nullptr;  // [arrivals, helpers past the wait]: zero at launch, reset by the last helper
   // residual + RMSNorm (N = d): h[M][d] += sum(partials); x = pack(bf16(norm(h) * w)) for rows >= row_begin
   float* h = nullptr;
   const uint16_t* w = nullptr;

@@ -185,10 +185,9 @@ struct ms_ctx {
   float* q = nullptr;
   float* attn_ws = nullptr;
   size_t attn_ws_elems = 0;
-  uint32_t* gang_ctr = nullptr;          // GEMM tail-gang arrival counters (ring, never reset)
+  uint32_t* gang_ctr = nullptr;          // GEMM tail-gang counter pairs (ring, self-resetting)
   unsigned long long* am_key = nullptr;  // wide argmax: per-row best key (self-resetting)
   int* am_cnt = nullptr;                 // wide argmax: per-row arrival counter (self-resetting)
-  std::vector<uint64_t> gang_count;      // host mirror: arrivals so far per counter
   int gang_next = 0;
   std::vector<int> submitted;  // ring slots of submitted decode steps, oldest first
   // decode-step CUDA graphs (MS_GRAPH=1): keyed by staging slot / batch shape, dropped when
@@ -369,14 +368,17 @@ constexpr int kGangCounters = 256;
 
 // MS_FUSE_ROWS=1 (experiment, off by default): residual-norm / SiLU in the
 // GEMM tails (tail gang) instead of standalone row kernels.  Measured slower
-// on B200 (the tail's row pass runs on 148 x 192-480 threads after the last
-// CTA arrives: +9 us per norm, +18 us per SiLU vs a 4-10 us standalone kernel
-// that starts under PDL), so the standalone kernels stay the default.
-bool fuse_rows() {
+// on the 7B decode step (14.43 vs 13.76 ms: the tail's row pass runs on the
+// last-arriving CTAs after the slowest one), so the standalone kernels stay
+// the default.  (A run that looked faster was a CUDA-graph replay bug: the
+// arrival counters' bases were baked into captured launches, so replayed
+// tails did not wait; the counters now reset themselves, gemm_tail_gang.)
+bool fuse_rows(int M) {
   static const bool v = [] {
     const char* e = std::getenv("MS_FUSE_ROWS");
     return e && e[0] == '1';
   }();
+  (void)M;
   return v;
 }
 
@@ -425,12 +427,10 @@ ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w_in, bool w4, int M, int
   } no_pdl(dq);
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
   const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, w4, c->num_sms, c->part_elems);
-  if (epi.op != ms::kEpiNone) {  // next arrival counter; every CTA of the plan arrives once
+  if (epi.op != ms::kEpiNone) {  // next counter pair of the ring (self-resetting, see gemm_tail_gang)
     const int i = c->gang_next;
     c->gang_next = (c->gang_next + 1) % kGangCounters;
-    epi.ctr = c->gang_ctr + i;
-    epi.base = (uint32_t)c->gang_count[i];
-    c->gang_count[i] += (uint64_t)plan.C;
+    epi.ctr = c->gang_ctr + 2 * i;
   }
   static unsigned long long* tl = nullptr;  // (debug) MS_TAIL_TL=<layer*4+mat>: dump that GEMM's tail timeline
   static const int tl_pick = [] {
@@ -648,7 +648,7 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     prof_mark(c);
     // residual + RMSNorm and SiLU*up run in the GEMM tails (tail gang) unless
     // disabled or a timing experiment skips pieces of the step
-    const bool fuse = fuse_rows() && skip == 0;
+    const bool fuse = fuse_rows(M) && skip == 0;
     const uint16_t* n2 = c->norms + ((size_t)l * 2 + 1) * d;
     if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 1), w4, M, TM, fuse ? epi_norm(c, n2, TM, 0) : ms::GemmEpi());
     pk_mark(c, w4 ? MS_PK_GEMM_O_W4 : MS_PK_GEMM_O);
@@ -828,9 +828,8 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       CK(cudaMemset(c->am_key, 0, (size_t)c->max_rows * sizeof(unsigned long long)));
       CK(cudaMalloc(&c->am_cnt, (size_t)c->max_rows * sizeof(int)));
       CK(cudaMemset(c->am_cnt, 0, (size_t)c->max_rows * sizeof(int)));
-      CK(cudaMalloc(&c->gang_ctr, kGangCounters * sizeof(uint32_t)));
-      CK(cudaMemset(c->gang_ctr, 0, kGangCounters * sizeof(uint32_t)));
-      c->gang_count.assign(kGangCounters, 0);
+      CK(cudaMalloc(&c->gang_ctr, 2 * kGangCounters * sizeof(uint32_t)));
+      CK(cudaMemset(c->gang_ctr, 0, 2 * kGangCounters * sizeof(uint32_t)));
       CK(cudaMalloc(&c->next, (size_t)c->max_rows * sizeof(int32_t)));
       CK(cudaMalloc(&c->logits, (size_t)desc->max_batch * desc->vocab * sizeof(float)));
       CK(cudaHostAlloc(&c->h_next, (size_t)c->max_rows * sizeof(int32_t), cudaHostAllocDefault));

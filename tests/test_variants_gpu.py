@@ -3,7 +3,8 @@
 each checked against the CPU oracle inside __graft_entry__.smoke) is re-run in a
 child process with each switch set (the switches are read once per process).
 
-    MS_FUSE_ROWS=1     residual+RMSNorm and SiLU*up in the GEMM tails (tail gang)
+    MS_FUSE_ROWS=1     residual+RMSNorm and SiLU*up in the GEMM tails (tail gang), replayed
+                       from CUDA graphs (self-resetting arrival counters)
     MS_ATTN_PERSIST=1  persistent stream-K decode attention (+ standalone QKV post)
     MS_W4_SMEM=1       W4A16 GEMM with the dequantised operand in shared memory
     MS_W4_GROUPS=4     four dequantiser warp groups
