@@ -1122,6 +1122,7 @@ cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M,
     if (w.K / plan.nk == 256) return launch_w4_groups<2>(w, x, M, TM, plan, out, stream, epi);
     return launch_w4_groups<1>(w, x, M, TM, plan, out, stream, epi);
   }
+  if (!w4 && epi.op == kEpiNone && gemm_2sm_ok(w, TM, plan)) return gemm_2sm_launch(w, x, M, plan, out, stream);
   if (w4) {
     static bool attr = false;
     if (!attr) {

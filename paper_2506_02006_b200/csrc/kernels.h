@@ -112,6 +112,10 @@ struct GemmEpi {
 };
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                         float* out, cudaStream_t stream, const GemmEpi& epi = GemmEpi());
+// CTA-pair (cta_group::2) BF16 GEMM for whole-tile long-prefill plans (gemm2sm.cu)
+bool gemm_2sm_ok(const GemmWeights& w, int TM, const GemmPlanDev& plan);
+cudaError_t gemm_2sm_launch(const GemmWeights& w, const uint16_t* x, int M, const GemmPlanDev& plan, float* out,
+                            cudaStream_t stream);
 
 // Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
 // every layer): [layer][kv_head][K|V][token][head_dim] bf16.

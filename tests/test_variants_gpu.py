@@ -80,3 +80,12 @@ def test_hd128_decode_matches_oracle(shape):
     finally:
         ref.close()
         dev.close()
+
+
+def test_gemm_2sm_variant_matches_reference():
+    """MS_GEMM_2SM=1: whole-tile BF16 plans run on CTA pairs (tcgen05
+    cta_group::2, gemm2sm.cu); the GEMM parity cases must still hold."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_kernels_gpu.py", "-k", "gemm_bf16", "-q", "-x",
+                        "-p", "no:cacheprovider"], cwd=ROOT, env=dict(os.environ, MS_GEMM_2SM="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
