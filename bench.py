@@ -98,6 +98,10 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU oracle
+WORKLOAD = ("llama2-7b-shape decode, batch 64, ctx 2048->2048+steps, 8/32 layers W4A16 (LIS order[0..7]), "
+            "16-token paged KV")
+
+
 def cpu_sample(batch: int, ctx: int, w4: bool):
     """One layer-step + lm_head of the 7B decode on the host (oracle port)."""
     import oracle as O
@@ -143,22 +147,24 @@ def run_reference(args):
     for _ in range(args.warmup):
         cpu_sample(8, 256, False)
     times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        ls, lm, threads = cpu_sample(BATCH, CTX, False)
-        wall = time.perf_counter() - t0
-        times.append(SHAPE["L"] * ls + lm)
+    threads = 1
+    for _ in range(args.steps):  # each step: the mixed 24 BF16 + 8 W4 decode step, sampled per layer kind
+        ls16, lm, threads = cpu_sample(BATCH, CTX, False)
+        ls4, _, _ = cpu_sample(BATCH, CTX, True)
+        times.append((SHAPE["L"] - len(W4_LAYERS)) * ls16 + len(W4_LAYERS) * ls4 + lm)
     step_s = float(np.mean(times))
     v = BATCH / step_s
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights/activations, fp64 accumulate",
-            "data": "synthetic", "config": {"workload": "llama2-7b-shape decode, batch 64, ctx 2048, BF16",
-                                           "global_batch": BATCH, "seq_len": CTX, "parallelism": "cpu"},
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16 activations, mixed W4A16-g128 / BF16 weights, fp64 accumulate",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": BATCH, "seq_len": CTX,
+                                           "parallelism": "cpu (all host threads)"},
             "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "port",
-                             "sample": "each step: one layer-step + lm_head of the B=64 ctx=2048 7B decode "
-                                       "on all host threads, extrapolated x32 layers (the reference simulator "
-                                       "prices this step instead of computing it, SPEC.md:14)"},
+                             "sample": f"each step: one BF16 and one W4 layer-step + lm_head of the B={BATCH} "
+                                       f"ctx={CTX} 7B decode on all host threads, extrapolated to "
+                                       f"{SHAPE['L'] - len(W4_LAYERS)} BF16 + {len(W4_LAYERS)} W4 layers (the "
+                                       "reference simulator prices this step instead of computing it, SPEC.md:14)"},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -487,8 +493,7 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16 activations, mixed W4A16-g128 / BF16 weights, fp32 accumulate",
         "data": "synthetic (random-init weights, synthetic 2048-token KV context)",
-        "config": {"workload": "llama2-7b-shape decode, batch 64, ctx 2048->2048+steps, 8/32 layers W4A16 "
-                               "(LIS order[0..7]), 16-token paged KV",
+        "config": {"workload": WORKLOAD,
                    "global_batch": BATCH * world, "seq_len": CTX,
                    "parallelism": f"replicas x{world}" if world > 1 else "single replica",
                    "l2": "inputs larger than L2 (13.2 GB weights + 68.7 GB KV per step)"},
