@@ -443,8 +443,11 @@ def run_ours(args):
     # (slots, positions, block table) from pinned host memory and its next
     # tokens are read back to the host; the engine-style pipelined form keeps
     # one step in flight while the previous step's tokens are collected.
-    # untimed warm-up of this path first: its steps use their own staging
-    # slots, whose decode graphs are captured on first reuse
+    # same context length as the headline loop (it starts at CTX - 1 after W
+    # warm-up steps; the swap test above advanced the positions), then an
+    # untimed warm-up of this path: its steps use their own staging slots,
+    # whose decode graphs are captured on first reuse
+    pos = np.full(BATCH, CTX - 1 - max(args.warmup, 8) + args.warmup, dtype=np.int32)
     for _ in range(max(args.warmup, 8)):
         dev.decode_submit(slots, pos, table)
         pos = pos + 1
