@@ -417,7 +417,12 @@ ms::GemmWeights w4_as_bf16(ms_ctx* c, const ms::GemmWeights& w4w) {
 }
 
 ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w_in, bool w4, int M, int TM, ms::GemmEpi epi = ms::GemmEpi()) {
-  const bool dq = w4 && w4_dequant_rows() > 0 && M >= w4_dequant_rows() && epi.op == ms::kEpiNone;
+  bool dq = w4 && w4_dequant_rows() > 0 && M >= w4_dequant_rows() && epi.op == ms::kEpiNone;
+  if (dq) {  // never while a decode step is being captured (the scratch may need allocating)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->compute, &cs));
+    dq = cs == cudaStreamCaptureStatusNone;
+  }
   const ms::GemmWeights w = dq ? w4_as_bf16(c, w_in) : w_in;
   if (dq) w4 = false;
   struct NoPdl {  // the GEMM's producer must not pre-issue weight loads before the dequant finished
