@@ -155,14 +155,20 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
 
   float m[G], l[G], acc[G][VEC];
   if (warp == 4) {
-    if (lane == 0) {
-      for (int it = 0; it < b1 - b0; ++it) {
+    // page ids of the next 32 blocks in one warp-wide load, handed to lane 0
+    // by shuffle (no dependent global load in front of each copy)
+    int pid = 0;
+    for (int it = 0; it < b1 - b0; ++it) {
+      if ((it & 31) == 0) pid = it + lane < b1 - b0 ? __ldg(ptab + b0 + it + lane) : 0;
+      const int page = __shfl_sync(0xffffffffu, pid, it & 31);
+      if (lane == 0) {
         const int s = it % kAttnStages;
         if (it >= kAttnStages) mbar_wait(&empty[s], ((it / kAttnStages) & 1) ^ 1);
-        const char* src = a.kv.arena + (int64_t)ptab[b0 + it] * a.kv.page_bytes + kv_off;
+        const char* src = a.kv.arena + (int64_t)page * a.kv.page_bytes + kv_off;
         mbar_expect_tx(&full[s], kStageBytes);
         bulk_g2s(smem + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
       }
+      __syncwarp();
     }
   } else if constexpr (kWarpPerBlock) {
     // ---- MHA consumer: one warp per 16-token block (blocks it = warp, warp+4, ...).
@@ -498,14 +504,17 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
     // ------------------------------------------------------------ producer
     // streams from the start; only the block holding the new token waits for
     // the consumers' fused QKV append
+    int pid = 0;  // page ids of the next 32 blocks, one warp-wide load
     for (int it = 0; it < b1 - b0; ++it) {
+      if ((it & 31) == 0) pid = it + lane < b1 - b0 ? __ldg(ptab + b0 + it + lane) : 0;
+      const int page = __shfl_sync(0xffffffffu, pid, it & 31);
       const int s = it % S;
       if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
       if (append && b0 + it == nb - 1) mbar_wait(kv_ready, 0);
       // one TMA tensor copy per block: the 32 K|V rows of 256 B, as two 128-B
       // halves, 128B-swizzled by the copy engine (conflict-free ldmatrix)
       if (lane == 0) {
-        const int64_t row = ((int64_t)ptab[b0 + it] * a.kv.page_bytes + kv_off) >> 8;  // 256-B row of the arena
+        const int64_t row = ((int64_t)page * a.kv.page_bytes + kv_off) >> 8;  // 256-B row of the arena
         mbar_expect_tx(&full[s], kStageBytes);
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
