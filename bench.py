@@ -526,9 +526,11 @@ def run_ours(args):
     dev.close()
     if args.serve8b_seconds > 0:
         line["serving_8b"] = serve_8b(args, local_rank, rank, world)
-    if args.prefill_tokens > 0:
+    # the Llama-2-13B legs (BASELINE configs[3]) are single-GPU workloads; at
+    # N > 1 they would only repeat per replica (and pin ~33 GB of host images each)
+    if args.prefill_tokens > 0 and world == 1:
         line["prefill_13b"] = prefill_13b(args, local_rank)
-    if args.serve13b_rps > 0:
+    if args.serve13b_rps > 0 and world == 1:
         line["serving_13b"] = serve_13b(args, local_rank, rank, world)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
