@@ -105,6 +105,10 @@ int ms_kv_attach(ms_ctx* ctx, int64_t first_id, int64_t n);
 int ms_kv_detach(ms_ctx* ctx, const int64_t* ids, int64_t n);
 int64_t ms_free_pages(ms_ctx* ctx);
 int64_t ms_kv_page_of(ms_ctx* ctx, int64_t block_id);
+/* Copies the KV page of one mapped block (every layer, layout
+ * [layer][kv_head][K|V][16 tok][head_dim] bf16, ms_page_bytes() bytes) to host
+ * memory, ordered after every step already launched (inspection / tests). */
+int ms_kv_export(ms_ctx* ctx, int64_t block_id, void* host_out, int64_t bytes);
 
 /* ------------------------------------------------------- token history */
 int ms_hist_reserve(ms_ctx* ctx, int32_t slots, int32_t max_len);
@@ -159,6 +163,9 @@ int ms_kv_fill_synthetic(ms_ctx* ctx, const int64_t* block_ids, int64_t n, uint6
  * compute stream, and per-launch timing of the paged attention kernel (events
  * bracketing each attention launch on its own stream). */
 int64_t ms_launch_count(ms_ctx* ctx);
+/* Decode-step CUDA graphs captured so far (a swap commit does not force a
+ * re-capture of shapes already captured at that precision vector). */
+int64_t ms_graph_captures(ms_ctx* ctx);
 int ms_timer_start(ms_ctx* ctx);
 int ms_timer_stop(ms_ctx* ctx, float* ms);
 /* Per-kernel-category device time of the decode/prefill steps launched while

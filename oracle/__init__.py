@@ -82,6 +82,12 @@ def lib():
         L.ref_prefill.restype = C.c_int32
         L.ref_prefill_trace.argtypes = [C.c_void_p, C.c_void_p, i32p, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_prefill_trace.restype = C.c_int32
+        L.ref_prefill_rows.argtypes = [C.c_void_p, C.c_void_p, i32p, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                       C.c_void_p]
+        L.ref_prefill_rows.restype = C.c_int32
+        L.ref_seq_set_len.argtypes = [C.c_void_p, C.c_int]
+        L.ref_seq_fill_pages.argtypes = [C.c_void_p, C.c_void_p, np.ctypeslib.ndpointer(np.int64, flags="C"),
+                                         C.c_int, C.c_uint64]
         L.ref_num_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -252,6 +258,34 @@ class RefModel:
         tr = np.empty((self.cfg["L"] + 1, len(toks), self.cfg["d"]), np.float32)
         lib().ref_prefill_trace(self.h, s, toks, len(toks), None, tr.ctypes.data_as(C.c_void_p))
         return tr
+
+    def prefill_rows(self, s, tokens, rows=None, want_logits: bool = True, want_trace: bool = False):
+        """Batched prefill (bit-identical to ``prefill`` / ``prefill_trace``).
+        ``rows``: token rows carried through the last layer (sorted, unique;
+        must contain the last token for logits).  Returns (next, logits,
+        trace [L+1, n, d] or None; in the last layer slice only ``rows`` are
+        defined)."""
+        toks = np.ascontiguousarray(tokens, np.int32)
+        n = len(toks)
+        r = None if rows is None else np.ascontiguousarray(np.unique(np.asarray(rows, np.int32)))
+        logits = np.empty(self.cfg["V"], np.float32) if want_logits else None
+        tr = np.zeros((self.cfg["L"] + 1, n, self.cfg["d"]), np.float32) if want_trace else None
+        nxt = lib().ref_prefill_rows(self.h, s, toks, n, None if r is None else r.ctypes.data_as(C.c_void_p),
+                                     0 if r is None else len(r),
+                                     logits.ctypes.data_as(C.c_void_p) if want_logits else None,
+                                     tr.ctypes.data_as(C.c_void_p) if want_trace else None)
+        return int(nxt), logits, tr
+
+    def seq_fill_pages(self, s, page_index, seed: int):
+        """Fill the sequence's KV cache with the device's synthetic fill
+        (ms_kv_fill_synthetic): block j = the page_index[j]-th page of the fill
+        list; sets the sequence length to 16 * len(page_index)."""
+        pi = np.ascontiguousarray(page_index, np.int64)
+        lib().ref_seq_fill_pages(self.h, s, pi, len(pi), seed)
+        lib().ref_seq_set_len(s, 16 * len(pi))
+
+    def seq_set_len(self, s, n: int):
+        lib().ref_seq_set_len(s, n)
 
     def prefill(self, s, tokens, want_logits: bool = True):
         toks = np.ascontiguousarray(tokens, np.int32)

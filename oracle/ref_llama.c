@@ -334,18 +334,80 @@ int ref_seq_len(const ref_seq* s) { return s->len; }
 uint16_t* ref_seq_k(ref_seq* s, int layer) { return s->k[layer]; }
 uint16_t* ref_seq_v(ref_seq* s, int layer) { return s->v[layer]; }
 
-/* y[b][n] = sum_k W[n][k] * x[b][k]   (bf16 inputs, fp64 accumulation, fp32 out) */
+/* y[b][n] = sum_k W[n][k] * x[b][k]   (bf16 inputs, fp64 accumulation, fp32 out)
+ *
+ * Every output element is ONE fp64 chain acc = acc + w[k] * x[k] in ascending
+ * k, with the product and the sum rounded separately (-ffp-contract=off): the
+ * result is bit-identical to the plain triple loop.  The loops are blocked so
+ * that the chains of GB columns of b advance together (vectorised across b,
+ * never across k), which keeps the oracle fast enough for the full-size
+ * parity tests (7B/8B decode steps, the 13B 8192-token prefill). */
+#define GB 16 /* b columns per register block */
+#define GN 4  /* W rows per register block */
+#define BS 256 /* b rows per cache super-block (X^T of BS rows stays in cache) */
+#if defined(__x86_64__) && defined(__GNUC__)
+__attribute__((target_clones("avx512f", "avx2", "default")))
+#endif
+static void gemm_tile(const uint16_t* W, const double* XT /*[K][GB]*/, int64_t K, int64_t n0, int nn, int nb,
+                      int64_t N, int64_t b0, float* Y) {
+  double acc[GN][GB];
+  for (int i = 0; i < GN; ++i)
+    for (int j = 0; j < GB; ++j) acc[i][j] = 0.0;
+  if (nn == GN) {
+    const uint16_t* w0 = W + (n0 + 0) * K;
+    const uint16_t* w1 = W + (n0 + 1) * K;
+    const uint16_t* w2 = W + (n0 + 2) * K;
+    const uint16_t* w3 = W + (n0 + 3) * K;
+    for (int64_t k = 0; k < K; ++k) {
+      const double* x = XT + k * GB;
+      const double a0 = (double)bf2f(w0[k]), a1 = (double)bf2f(w1[k]);
+      const double a2 = (double)bf2f(w2[k]), a3 = (double)bf2f(w3[k]);
+      for (int j = 0; j < GB; ++j) {
+        acc[0][j] = acc[0][j] + a0 * x[j];
+        acc[1][j] = acc[1][j] + a1 * x[j];
+        acc[2][j] = acc[2][j] + a2 * x[j];
+        acc[3][j] = acc[3][j] + a3 * x[j];
+      }
+    }
+  } else {
+    for (int i = 0; i < nn; ++i) {
+      const uint16_t* wr = W + (n0 + i) * K;
+      for (int64_t k = 0; k < K; ++k) {
+        const double a = (double)bf2f(wr[k]);
+        const double* x = XT + k * GB;
+        for (int j = 0; j < GB; ++j) acc[i][j] = acc[i][j] + a * x[j];
+      }
+    }
+  }
+  for (int i = 0; i < nn; ++i)
+    for (int j = 0; j < nb; ++j) Y[(b0 + j) * N + n0 + i] = (float)acc[i][j];
+}
+
 void ref_gemm_bf16(const uint16_t* W, const uint16_t* X, int64_t B, int64_t N, int64_t K,
                    float* Y) {
+  if (B <= 0 || N <= 0) return;
+  const int64_t nbb = (B + GB - 1) / GB;
+  for (int64_t s0 = 0; s0 < nbb; s0 += BS / GB) {  /* b super-block: X^T blocks reused by every W row */
+    const int64_t s1 = s0 + BS / GB < nbb ? s0 + BS / GB : nbb;
+    double* XT = (double*)malloc((size_t)(s1 - s0) * K * GB * sizeof(double));
 #pragma omp parallel for schedule(static)
-  for (int64_t n = 0; n < N; ++n) {
-    const uint16_t* wr = W + n * K;
-    for (int64_t b = 0; b < B; ++b) {
-      const uint16_t* xr = X + b * K;
-      double acc = 0.0;
-      for (int64_t k = 0; k < K; ++k) acc += (double)bf2f(wr[k]) * (double)bf2f(xr[k]);
-      Y[b * N + n] = (float)acc;
+    for (int64_t bb = s0; bb < s1; ++bb) {
+      double* xt = XT + (bb - s0) * K * GB;
+      for (int j = 0; j < GB; ++j) {
+        const int64_t b = bb * GB + j;
+        for (int64_t k = 0; k < K; ++k) xt[k * GB + j] = b < B ? (double)bf2f(X[b * K + k]) : 0.0;
+      }
     }
+    const int64_t nnb = (N + GN - 1) / GN;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t t = 0; t < nnb * (s1 - s0); ++t) {
+      const int64_t nbk = t / (s1 - s0), bb = s0 + t % (s1 - s0);
+      const int64_t n0 = nbk * GN, b0 = bb * GB;
+      const int nn = (int)(N - n0 < GN ? N - n0 : GN);
+      const int nb = (int)(B - b0 < GB ? B - b0 : GB);
+      gemm_tile(W, XT + (bb - s0) * K * GB, K, n0, nn, nb, N, b0, Y);
+    }
+    free(XT);
   }
 }
 
@@ -498,6 +560,134 @@ int32_t ref_prefill_trace(ref_model* m, ref_seq* s, const int32_t* tokens, int n
     forward_impl(m, &s, tokens + i, 1, (i == n - 1) ? logits : NULL, &nxt, trace + (int64_t)i * m->c.d,
                  (int64_t)n * m->c.d);
   return nxt;
+}
+
+/* Batched prefill: the same math as ref_prefill (token by token through
+ * forward_impl), evaluated layer by layer over all n tokens at once.  Every
+ * per-token operation and its order is unchanged (row-wise GEMM chains in
+ * ascending k, causal attention of token i over positions [0, len + i]), so
+ * the result is bit-identical to ref_prefill / ref_prefill_trace; only the
+ * loops are reordered so that the GEMMs see n rows (fast enough for the
+ * 8192-token Llama-2-13B parity test).
+ *   rows / n_rows (optional): in the LAST layer only these token rows are
+ *   carried past the QKV projection (every row's K/V is still appended); the
+ *   trace and the logits are then defined for those rows only (the last token
+ *   must be among them when logits are requested).
+ *   trace (optional): [L+1][n][d] residual stream, as ref_prefill_trace. */
+int32_t ref_prefill_rows(ref_model* m, ref_seq* s, const int32_t* tokens, int n, const int32_t* rows, int n_rows,
+                         float* logits, float* trace) {
+  const ref_cfg* c = &m->c;
+  const int d = c->d, hd = c->hd, H = c->H, KVH = c->KVH, half = hd / 2, ffn = c->ffn;
+  const int qkv_n = (H + 2 * KVH) * hd;
+  const int pos0 = s->len;
+  int* sel = (int*)malloc((size_t)n * sizeof(int));
+  int nsel = 0;
+  if (rows) {
+    for (int i = 0; i < n_rows; ++i) sel[nsel++] = rows[i];
+  } else {
+    for (int i = 0; i < n; ++i) sel[nsel++] = i;
+  }
+  float* h = (float*)malloc((size_t)n * d * sizeof(float));
+  uint16_t* xn = (uint16_t*)malloc((size_t)n * (ffn > d ? ffn : d) * 2);
+  float* y = (float*)malloc((size_t)n * (2 * ffn > qkv_n ? 2 * ffn : qkv_n) * sizeof(float));
+  uint16_t* att = (uint16_t*)malloc((size_t)n * H * hd * 2);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) h[(int64_t)i * d + j] = bf2f(m->embed[(int64_t)tokens[i] * d + j]);
+  for (int l = 0; l < c->L; ++l) {
+    const int last = l == c->L - 1;
+    if (trace) memcpy(trace + (int64_t)l * n * d, h, (size_t)n * d * sizeof(float));
+    ref_rmsnorm(h, m->norm1[l], n, d, c->eps, xn);
+    ref_gemm_bf16(m->wqkv[l], xn, n, qkv_n, d, y);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) {
+      const int pos = pos0 + i;
+      float* row = y + (int64_t)i * qkv_n;
+      const float* cs = m->rope_cos + (int64_t)pos * half;
+      const float* sn = m->rope_sin + (int64_t)pos * half;
+      for (int hh = 0; hh < H; ++hh) rope_inplace(row + hh * hd, hd, cs, sn);
+      for (int hh = 0; hh < KVH; ++hh) rope_inplace(row + (H + hh) * hd, hd, cs, sn);
+      for (int hh = 0; hh < KVH; ++hh)
+        for (int j = 0; j < hd; ++j) {
+          s->k[l][((int64_t)pos * KVH + hh) * hd + j] = f2bf(row[(H + hh) * hd + j]);
+          s->v[l][((int64_t)pos * KVH + hh) * hd + j] = f2bf(row[(H + KVH + hh) * hd + j]);
+        }
+    }
+    const int nr = last ? nsel : n;
+    /* rows carried on: all of them, or the selected ones in the last layer
+     * (compacted to the front of h / att / xn / y) */
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < nr; ++r) {
+      const int i = last ? sel[r] : r;
+      ref_attention(y + (int64_t)i * qkv_n, s->k[l], s->v[l], pos0 + i + 1, H, KVH, hd,
+                    att + (int64_t)r * H * hd, NULL);
+    }
+    if (last && rows) {
+      for (int r = 0; r < nr; ++r)
+        memmove(h + (int64_t)r * d, h + (int64_t)sel[r] * d, (size_t)d * sizeof(float));
+    }
+    ref_gemm_bf16(m->wo[l], att, nr, d, (int64_t)H * hd, y);
+    for (int64_t i = 0; i < (int64_t)nr * d; ++i) h[i] = h[i] + y[i];
+    ref_rmsnorm(h, m->norm2[l], nr, d, c->eps, xn);
+    ref_gemm_bf16(m->wgu[l], xn, nr, 2 * ffn, d, y);
+    for (int r = 0; r < nr; ++r)
+      for (int j = 0; j < ffn; ++j) {
+        const float g = y[(int64_t)r * 2 * ffn + j];
+        const float u = y[(int64_t)r * 2 * ffn + ffn + j];
+        xn[(int64_t)r * ffn + j] = f2bf(silu(g) * u);
+      }
+    ref_gemm_bf16(m->wd[l], xn, nr, d, ffn, y);
+    for (int64_t i = 0; i < (int64_t)nr * d; ++i) h[i] = h[i] + y[i];
+    if (trace && last) {
+      float* t = trace + (int64_t)c->L * n * d;
+      for (int r = 0; r < nr; ++r)
+        memcpy(t + (int64_t)(rows ? sel[r] : r) * d, h + (int64_t)r * d, (size_t)d * sizeof(float));
+    }
+  }
+  s->len += n;
+  /* the last token's logits (row n - 1 must have been carried) */
+  int lr = -1;
+  for (int r = 0; r < nsel; ++r)
+    if (sel[r] == n - 1) lr = r;
+  int32_t best = -1;
+  if (lr >= 0) {
+    ref_rmsnorm(h + (int64_t)lr * d, m->normf, 1, d, c->eps, xn);
+    float* lg = logits ? logits : (float*)malloc((size_t)c->V * sizeof(float));
+    ref_gemm_bf16(m->lm_head, xn, 1, c->V, d, lg);
+    best = 0;
+    for (int v = 1; v < c->V; ++v)
+      if (lg[v] > lg[best]) best = v;
+    if (!logits) free(lg);
+  }
+  free(sel); free(h); free(xn); free(y); free(att);
+  return best;
+}
+
+void ref_seq_set_len(ref_seq* s, int len) { s->len = len; }
+
+/* Restatement of the device's synthetic KV fill (runtime ms_kv_fill_synthetic
+ * -> elementwise.cu fill_kv_kernel): element `off` of the pi-th listed page is
+ * bf16(u), u = (r >> 40) * 2^-24 * 2 - 1, r = splitmix64(seed + pi * per_page
+ * + off), page layout [layer][kv_head][K|V][16 tok][head_dim].  Fills this
+ * sequence's cache for positions [0, 16 * nblocks), block j being the
+ * page_index[j]-th page of the fill list. */
+void ref_seq_fill_pages(const ref_model* m, ref_seq* s, const int64_t* page_index, int nblocks, uint64_t seed) {
+  const ref_cfg* c = &m->c;
+  const int64_t hd = c->hd, KVH = c->KVH;
+  const int64_t per_page = 16 * (int64_t)c->L * KVH * 2 * hd;
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < nblocks; ++j) {
+    for (int l = 0; l < c->L; ++l)
+      for (int64_t kh = 0; kh < KVH; ++kh)
+        for (int kv = 0; kv < 2; ++kv)
+          for (int t = 0; t < 16; ++t)
+            for (int64_t i = 0; i < hd; ++i) {
+              const int64_t off = (((int64_t)l * KVH + kh) * 2 + kv) * 16 * hd + t * hd + i;
+              const uint64_t r = splitmix64(seed + (uint64_t)(page_index[j] * per_page + off));
+              const float u = (float)(r >> 40) * (1.0f / 16777216.0f) * 2.0f - 1.0f;
+              uint16_t* dst = kv ? s->v[l] : s->k[l];
+              dst[(((int64_t)j * 16 + t) * KVH + kh) * hd + i] = f2bf(u);
+            }
+  }
 }
 
 int ref_num_threads(void) {

@@ -71,6 +71,8 @@ SIGNATURES = [
     ("ms_kv_detach", C.c_int, [_P, C.POINTER(C.c_int64), C.c_int64]),
     ("ms_free_pages", C.c_int64, [_P]),
     ("ms_kv_page_of", C.c_int64, [_P, C.c_int64]),
+    ("ms_kv_export", C.c_int, [_P, C.c_int64, _P, C.c_int64]),
+    ("ms_graph_captures", C.c_int64, [_P]),
     ("ms_hist_reserve", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("ms_hist_write", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]),
     ("ms_hist_read", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]),

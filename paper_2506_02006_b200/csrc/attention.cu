@@ -684,6 +684,13 @@ static bool gqa_tensor_map(const KvGeom& kv, int64_t arena_bytes, CUtensorMap* o
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Item map: one CTA per (row, kv_head) item, or `splits` CTAs per item under
+// uniform split-KV (merged by attn_combine_kernel).
+static void attn_item_map(AttnArgs& a) {
+  a.whole_items = a.splits > 1 ? 0 : a.rows * a.KVH;
+  a.tail_splits = a.splits > 1 ? a.splits : 1;
+}
+
 template <int G>
 static cudaError_t launch_gqa(const AttnArgs& a_in, cudaStream_t stream) {
   static const int stages = [] {
@@ -708,393 +715,13 @@ static cudaError_t launch_gqa(const AttnArgs& a_in, cudaStream_t stream) {
     cudaFuncSetAttribute(attn_gqa_mma_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  attn_item_map(a, attn_gqa_mma_kernel<G>, smem);
+  attn_item_map(a);
   const int ctas = a.whole_items + (a.rows * a.KVH - a.whole_items) * a.tail_splits;
   cudaError_t e = launch_pdl(attn_gqa_mma_kernel<G>, dim3(ctas), dim3(160), smem, stream, a, tmap);
   if (e != cudaSuccess || a.whole_items == a.rows * a.KVH) return e;
   return launch_pdl(attn_combine_kernel<128>, dim3(a.rows, a.H), dim3(128), 0, stream, a);
 }
 
-// ---------------------------------------------------------------------------
-// Persistent stream-K decode attention.  The (row, kv_head) work items are laid
-// end to end as one sequence of K/V blocks (item i = row * KVH + kv_head holds
-// ceil(ctx_row / 16) blocks); CTA c of a persistent grid streams the contiguous
-// range [T c / C, T (c+1) / C) of that sequence, so every CTA moves the same
-// number of KV bytes whatever the context lengths, and the producer's ring runs
-// across item boundaries (no per-item CTA launch, prologue or tail wave).  An
-// item that straddles CTAs leaves one partial (acc, m, l) per CTA; the CTA that
-// arrives last on the item's counter merges them in CTA order (deterministic)
-// and writes the output.  The per-item q vector is bulk-copied by the producer
-// into a 2-deep q ring together with the item's first block.
-constexpr int kPersistRows = 256;  // max decode rows (scan of per-row block counts in smem)
-
-__host__ __device__ inline int64_t persist_g0(int64_t T, int C, int c) { return T * c / C; }
-__device__ inline int persist_cta_of(int64_t T, int C, int64_t g) {  // c with g0(c) <= g < g0(c+1)
-  return (int)(((g + 1) * C + T - 1) / T) - 1;
-}
-
-template <int HD, int G, int BT>
-__global__ void __launch_bounds__(160) attn_persist_kernel(AttnArgs a) {
-  constexpr int VEC = HD / 32;
-  constexpr int TPW = BT / 4;
-  constexpr uint32_t kStageBytes = (uint32_t)BT * HD * 2 * 2;
-  constexpr uint32_t kQBytes = (uint32_t)G * HD * 4;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int S = a.stages;
-  uint8_t* qring = smem + (size_t)S * kStageBytes;                             // [2][G][HD] fp32
-  float* scratch = reinterpret_cast<float*>(qring + 2 * kQBytes);              // [4][G][HD] + [4][G][2]
-  int64_t* rp = reinterpret_cast<int64_t*>(scratch + 4 * G * HD + 8 * G);      // [rows + 1] row prefix (blocks)
-  uint64_t* full = reinterpret_cast<uint64_t*>(rp + kPersistRows + 1);
-  uint64_t* empty = full + S;
-  uint64_t* qfull = empty + S;   // [2]
-  uint64_t* qempty = qfull + 2;  // [2]
-  __shared__ int s_last;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KVH = a.KVH, rows = a.rows;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 4);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&qfull[s], 1);
-      mbar_init(&qempty[s], 4);
-    }
-    fence_mbar_init();
-  }
-  pdl_wait();  // ctx_len, q and the KV append of this step come from earlier kernels
-  pdl_trigger();
-  // row prefix sums of block counts (rows <= kPersistRows): parallel loads, one scan
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) rp[r + 1] = (a.ctx_len[r] + BT - 1) / BT;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    rp[0] = 0;
-    for (int r = 1; r <= rows; ++r) rp[r] += rp[r - 1];
-  }
-  __syncthreads();
-  const int64_t T = rp[rows] * KVH;
-  // every participating CTA gets >= 1 block (the merge counts on it)
-  const int C = (int)min((int64_t)a.ctas, T), c = blockIdx.x;
-  if (c >= C) return;
-  const int64_t g0 = persist_g0(T, C, c), g1 = persist_g0(T, C, c + 1);
-  // locate (row, kv_head, block) of global block g0
-  auto locate = [&](int64_t g, int& row, int& kvh, int& blk) {
-    int lo = 0, hi = rows - 1;  // last row with rp[row] * KVH <= g
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (rp[mid] * KVH <= g) lo = mid;
-      else hi = mid - 1;
-    }
-    row = lo;
-    const int nb = (int)(rp[row + 1] - rp[row]);
-    const int64_t o = g - rp[row] * KVH;
-    kvh = (int)(o / nb);
-    blk = (int)(o - (int64_t)kvh * nb);
-  };
-  int row0, kvh0, blk0;
-  locate(g0, row0, kvh0, blk0);
-
-  if (warp == 4) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ producer
-      int row = row0, kvh = kvh0, blk = blk0, nb = (int)(rp[row + 1] - rp[row]);
-      const int32_t* ptab = a.pages + (size_t)(a.page_row ? a.page_row[row] : row) * a.page_stride;
-      int item = 0;  // items started by this CTA
-      for (int64_t g = g0, it = 0; g < g1; ++g, ++it) {
-        if (g == g0 || blk == 0) {  // new item: its q vector into the q ring
-          const int qs = item & 1;
-          if (item >= 2) mbar_wait(&qempty[qs], ((item >> 1) & 1) ^ 1);
-          mbar_expect_tx(&qfull[qs], kQBytes);
-          bulk_g2s(qring + qs * kQBytes, a.q + ((size_t)row * a.H + kvh * G) * HD, kQBytes, &qfull[qs]);
-          ++item;
-        }
-        const int s = (int)(it % S);
-        if (it >= S) mbar_wait(&empty[s], (uint32_t)((it / S) & 1) ^ 1);
-        const char* src = a.kv.arena + (int64_t)ptab[blk] * a.kv.page_bytes + a.kv.layer_off(a.layer) +
-                          (int64_t)kvh * 2 * a.kv.head_bytes();
-        mbar_expect_tx(&full[s], kStageBytes);
-        bulk_g2s(smem + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
-        if (++blk == nb) {
-          blk = 0;
-          if (++kvh == KVH) {
-            kvh = 0;
-            ++row;
-            if (row < rows) {
-              nb = (int)(rp[row + 1] - rp[row]);
-              ptab = a.pages + (size_t)(a.page_row ? a.page_row[row] : row) * a.page_stride;
-            }
-          }
-        }
-      }
-    }
-    return;
-  }
-  // ------------------------------------------------------------- consumers
-  int row = row0, kvh = kvh0, blk = blk0;
-  int64_t g = g0, it = 0;
-  int item = 0;
-  while (g < g1) {
-    const int nb = (int)(rp[row + 1] - rp[row]);
-    const int ctx = a.ctx_len[row];
-    const int seg_lo = blk;
-    const int seg_hi = (int)min((int64_t)nb, (int64_t)blk + (g1 - g));
-    const int qs = item & 1;
-    mbar_wait(&qfull[qs], (item >> 1) & 1);
-    float qv[G][VEC], m[G], l[G], acc[G][VEC];
-    const float* qsm = reinterpret_cast<const float*>(qring + qs * kQBytes);
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) qv[gg][i] = qsm[gg * HD + lane * VEC + i] * a.scale_log2;
-      m[gg] = -INFINITY;
-      l[gg] = 0.f;
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) acc[gg][i] = 0.f;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&qempty[qs]);
-    for (int b = seg_lo; b < seg_hi; ++b, ++it) {
-      const int s = (int)(it % S);
-      mbar_wait(&full[s], (uint32_t)((it / S) & 1));
-      const uint16_t* Kt = reinterpret_cast<const uint16_t*>(smem + (size_t)s * kStageBytes);
-      const uint16_t* Vt = Kt + BT * HD;
-      const int tok0 = b * BT;
-      float sc[TPW][G];
-#pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const int t = warp + 4 * i;
-        float kf[VEC];
-        if constexpr (VEC == 4) {
-          const uint2 kr = *reinterpret_cast<const uint2*>(Kt + t * HD + lane * 4);
-          kf[0] = __uint_as_float(kr.x << 16);
-          kf[1] = __uint_as_float(kr.x & 0xFFFF0000u);
-          kf[2] = __uint_as_float(kr.y << 16);
-          kf[3] = __uint_as_float(kr.y & 0xFFFF0000u);
-        } else {
-          const uint32_t kr = *reinterpret_cast<const uint32_t*>(Kt + t * HD + lane * 2);
-          kf[0] = __uint_as_float(kr << 16);
-          kf[1] = __uint_as_float(kr & 0xFFFF0000u);
-        }
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          float p = 0.f;
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) p = fmaf(qv[gg][e], kf[e], p);
-          sc[i][gg] = p;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < TPW; ++i)
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) sc[i][gg] = warp_sum(sc[i][gg]);
-      float vf[TPW][VEC];
-#pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const int t = warp + 4 * i;
-        if constexpr (VEC == 4) {
-          const uint2 vr = *reinterpret_cast<const uint2*>(Vt + t * HD + lane * 4);
-          vf[i][0] = __uint_as_float(vr.x << 16);
-          vf[i][1] = __uint_as_float(vr.x & 0xFFFF0000u);
-          vf[i][2] = __uint_as_float(vr.y << 16);
-          vf[i][3] = __uint_as_float(vr.y & 0xFFFF0000u);
-        } else {
-          const uint32_t vr = *reinterpret_cast<const uint32_t*>(Vt + t * HD + lane * 2);
-          vf[i][0] = __uint_as_float(vr << 16);
-          vf[i][1] = __uint_as_float(vr & 0xFFFF0000u);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        float mx = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < TPW; ++i)
-          if (tok0 + warp + 4 * i < ctx) mx = fmaxf(mx, sc[i][gg]);
-        const float mn = fmaxf(m[gg], mx);
-        if (mn == -INFINITY) continue;
-        const float corr = exp2f(m[gg] - mn);
-        float lsum = l[gg] * corr;
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[gg][e] *= corr;
-#pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-          const float p = (tok0 + warp + 4 * i < ctx) ? exp2f(sc[i][gg] - mn) : 0.f;
-          lsum += p;
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[gg][e] = fmaf(p, vf[i][e], acc[gg][e]);
-        }
-        l[gg] = lsum;
-        m[gg] = mn;
-      }
-    }
-    // merge the 4 consumer warps (named barrier 1: consumers only)
-    float* sacc = scratch + (size_t)warp * G * HD;
-    float* sml = scratch + (size_t)4 * G * HD + (size_t)warp * G * 2;
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) sacc[gg * HD + lane * VEC + e] = acc[gg][e];
-      if (lane == 0) {
-        sml[gg * 2 + 0] = m[gg];
-        sml[gg * 2 + 1] = l[gg];
-      }
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    const bool whole = seg_lo == 0 && seg_hi == nb;
-    const int item_id = row * KVH + kvh;
-    const int slot = item == 0 ? 0 : 1;  // first segment of this CTA -> 0, last -> 1
-    const float* smlv = scratch + (size_t)4 * G * HD;
-    for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
-      const int gg = idx / HD, dim = idx - gg * HD;
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) M = fmaxf(M, smlv[(w * G + gg) * 2]);
-      float L = 0.f, O = 0.f;
-      if (M != -INFINITY) {
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const float f = exp2f(smlv[(w * G + gg) * 2] - M);
-          L += smlv[(w * G + gg) * 2 + 1] * f;
-          O += scratch[(size_t)(w * G + gg) * HD + dim] * f;
-        }
-      }
-      if (whole) {
-        const int h = kvh * G + gg;
-        const float o = L > 0.f ? O / L : 0.f;
-        const int K = a.H * HD;
-        const size_t off = a.out_packed ? act_off(row, h * HD + dim, K, a.TM) : (size_t)row * K + h * HD + dim;
-        a.out[off] = f2bf(o);
-      } else {
-        float* pw = a.pws + (((size_t)c * 2 + slot) * G + gg) * (HD + 2);
-        pw[dim] = O;
-        if (dim == 0) {
-          pw[HD] = M;
-          pw[HD + 1] = L;
-        }
-      }
-    }
-    if (!whole) {
-      // publish the partial, count arrivals; the last CTA on the item merges
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int64_t ig0 = rp[row] * KVH + (int64_t)kvh * nb;
-      const int cf = persist_cta_of(T, C, ig0), cl = persist_cta_of(T, C, ig0 + nb - 1);
-      if (threadIdx.x == 0) s_last = atomicAdd(&a.pcnt[item_id], 1) == cl - cf;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (s_last) {
-        __threadfence();
-        for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
-          const int gg = idx / HD, dim = idx - gg * HD;
-          float M = -INFINITY;
-          for (int cc = cf; cc <= cl; ++cc) {
-            // slot of the item in CTA cc: its last segment (1) only for the first CTA
-            // when that CTA started on an earlier item
-            const int sl = (cc == cf && persist_g0(T, C, cc) < ig0) ? 1 : 0;
-            M = fmaxf(M, __ldcg(a.pws + (((size_t)cc * 2 + sl) * G + gg) * (HD + 2) + HD));
-          }
-          float L = 0.f, O = 0.f;
-          if (M != -INFINITY) {
-            for (int cc = cf; cc <= cl; ++cc) {
-              const int sl = (cc == cf && persist_g0(T, C, cc) < ig0) ? 1 : 0;
-              const float* pw = a.pws + (((size_t)cc * 2 + sl) * G + gg) * (HD + 2);
-              const float mc = __ldcg(pw + HD);
-              if (mc == -INFINITY) continue;
-              const float f = exp2f(mc - M);
-              L += __ldcg(pw + HD + 1) * f;
-              O += __ldcg(pw + dim) * f;
-            }
-          }
-          const int h = kvh * G + gg;
-          const float o = L > 0.f ? O / L : 0.f;
-          const int K = a.H * HD;
-          const size_t off = a.out_packed ? act_off(row, h * HD + dim, K, a.TM) : (size_t)row * K + h * HD + dim;
-          a.out[off] = f2bf(o);
-        }
-        if (threadIdx.x == 0) a.pcnt[item_id] = 0;  // self-reset for the next launch
-      }
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // scratch reuse
-    g += seg_hi - seg_lo;
-    ++item;
-    blk = 0;
-    if (++kvh == KVH) {
-      kvh = 0;
-      ++row;
-    }
-  }
-}
-
-int attn_persist_ctas(int num_sms) {
-  static const int per_sm = std::max(1, std::min(4, attn_env("MS_ATTN_PERSIST_PER_SM", 2)));
-  return num_sms * per_sm;
-}
-size_t attn_persist_ws_floats(int num_sms, int G, int HD) {
-  return (size_t)num_sms * 4 * 2 * G * (HD + 2);
-}
-
-template <int HD, int G>
-static cudaError_t launch_persist(const AttnArgs& a_in, cudaStream_t stream) {
-  constexpr int BT = 16;
-  static const int stages = std::max(2, std::min(kAttnMaxStages, attn_env("MS_ATTN_STAGES", 4)));
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  AttnArgs a = a_in;
-  a.stages = stages;
-  a.ctas = attn_persist_ctas(sms);
-  const size_t smem = (size_t)stages * BT * HD * 4 + 2 * (size_t)G * HD * 4 + ((size_t)4 * G * HD + 8 * G) * 4 +
-                      (kPersistRows + 1) * 8 + (2 * stages + 4) * 8;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_persist_kernel<HD, G, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  return launch_pdl(attn_persist_kernel<HD, G, BT>, dim3(a.ctas), dim3(160), smem, stream, a);
-}
-
-// Item map for a launch of `kernel`: whole items fill full waves of the
-// occupancy-limited grid; the remaining (tail) items are split so the last
-// wave is made of short CTAs.  Uniform split-KV (a.splits > 1) is kept as is.
-template <typename K>
-static void attn_item_map(AttnArgs& a, K kernel, size_t smem) {
-  const int items = a.rows * a.KVH;
-  a.whole_items = items;
-  a.tail_splits = 1;
-  if (a.splits > 1) {
-    a.whole_items = 0;
-    a.tail_splits = a.splits;
-    return;
-  }
-  static const bool on = attn_env("MS_ATTN_TAILSPLIT", 0) != 0;  // measured slower on the 7B step: off
-  if (!on || a.part_o == nullptr || a.part_ml == nullptr || a.ws_splits_max < 2) return;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 160, smem) != cudaSuccess || per_sm < 1) return;
-  const int slots = sms * per_sm;
-  const int full = items / slots * slots, tail = items - full;
-  if (full == 0 || tail == 0) return;
-  // splits t minimising the tail's length in item-times: ceil(tail * t / slots) / t
-  int best_t = 1;
-  double best = 1.0;
-  for (int t = 2; t <= a.ws_splits_max; ++t) {
-    if (a.max_blocks_hint > 0 && a.max_blocks_hint / t < 4) break;  // >= 4 blocks per piece
-    const double len = (double)((tail * t + slots - 1) / slots) / t;
-    if (len < best - 1e-9) {
-      best = len;
-      best_t = t;
-    }
-  }
-  if (best_t > 1) {
-    a.whole_items = full;
-    a.tail_splits = best_t;
-  }
-}
 
 template <int HD, int G>
 static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
@@ -1118,7 +745,7 @@ static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
     cudaFuncSetAttribute(attn_decode_kernel<HD, G, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  attn_item_map(a, attn_decode_kernel<HD, G, BT>, smem);
+  attn_item_map(a);
   const int ctas = a.whole_items + (a.rows * a.KVH - a.whole_items) * a.tail_splits;
   cudaError_t e = launch_pdl(attn_decode_kernel<HD, G, BT>, dim3(ctas), dim3(160), smem, stream, a);
   if (e != cudaSuccess || a.whole_items == a.rows * a.KVH) return e;
@@ -1133,9 +760,8 @@ static bool gqa_mma_enabled() {
 
 template <int HD>
 static cudaError_t launch_hd(const AttnArgs& a, cudaStream_t stream) {
-  const bool persist = a.pws != nullptr && a.pcnt != nullptr && a.splits <= 1 && a.rows <= kPersistRows;
   if constexpr (HD == 128) {
-    if (!persist && gqa_mma_enabled() && a.arena_bytes > 0) {
+    if (gqa_mma_enabled() && a.arena_bytes > 0) {
       switch (a.H / a.KVH) {
         case 2: return launch_gqa<2>(a, stream);
         case 4: return launch_gqa<4>(a, stream);
@@ -1145,10 +771,10 @@ static cudaError_t launch_hd(const AttnArgs& a, cudaStream_t stream) {
     }
   }
   switch (a.H / a.KVH) {
-    case 1: return persist ? launch_persist<HD, 1>(a, stream) : launch_g<HD, 1>(a, stream);
-    case 2: return persist ? launch_persist<HD, 2>(a, stream) : launch_g<HD, 2>(a, stream);
-    case 4: return persist ? launch_persist<HD, 4>(a, stream) : launch_g<HD, 4>(a, stream);
-    case 8: return persist ? launch_persist<HD, 8>(a, stream) : launch_g<HD, 8>(a, stream);
+    case 1: return launch_g<HD, 1>(a, stream);
+    case 2: return launch_g<HD, 2>(a, stream);
+    case 4: return launch_g<HD, 4>(a, stream);
+    case 8: return launch_g<HD, 8>(a, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -148,269 +148,38 @@ struct SegIter {
   }
 };
 
-// ------------------------------------------------------------- tail gang
-__device__ __forceinline__ float tail_sum_slots(const float* p, size_t stride, int n) {
-  float v[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) v[s] = s < n ? __ldcg(p + s * stride) : 0.f;
-  float acc = 0.f;
-#pragma unroll
-  for (int s = 0; s < 8; ++s)
-    if (s < n) acc += v[s];
-  for (int s = 8; s < n; ++s) acc += __ldcg(p + s * stride);
-  return acc;
-}
-
-// Runs after the CTA's MMA/epilogue work (all threads, after a CTA barrier).
-// `scratch` = the kernel's (now idle) dynamic shared memory: static shared
-// arrays would push the GEMMs over the 227 KB per-CTA limit.
-__device__ void gemm_tail_gang(const GemmEpi& e, const GemmPlanDev& plan, int M, int N, const float* __restrict__ part,
-                               uint8_t* scratch) {
-  uint32_t& s_rank = *reinterpret_cast<uint32_t*>(scratch);
-  float* s_red = reinterpret_cast<float*>(scratch + 128);
-  const int C = plan.C;
-  auto gt = [] {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-  };
-  if (threadIdx.x == 0) {
-    __threadfence();  // this CTA's partial stores before its arrival
-    s_rank = atomicAdd(&e.ctr[0], 1u);
-    if (e.tl) e.tl[blockIdx.x * 4 + 1] = gt();
-  }
-  __syncthreads();
-  const int rank = (int)s_rank;
-  const int units = e.op == kEpiResidualNorm ? M : C;  // norm: one row per helper
-  const int nh = min(C, units);
-  if (rank < C - nh) return;
-  const int hid = rank - (C - nh);
-  if (threadIdx.x == 0) {
-    while ((int)*reinterpret_cast<volatile uint32_t*>(&e.ctr[0]) < C) __nanosleep(64);
-    __threadfence();
-    // the pair resets itself for its next use once every helper is past the
-    // wait (every CTA has arrived by then); nothing host-side tracks counts, so
-    // the same launch replays correctly from a CUDA graph
-    if (atomicAdd(&e.ctr[1], 1u) == (uint32_t)nh - 1) {
-      atomicExch(&e.ctr[1], 0u);
-      atomicExch(&e.ctr[0], 0u);
-    }
-    if (e.tl) e.tl[blockIdx.x * 4 + 2] = gt();
-  }
-  __syncthreads();
-  const int nthr = blockDim.x;
-  if (e.op == kEpiResidualNorm) {
-    // rows round-robin over the helpers; per row every thread keeps up to
-    // kV float4 columns in registers, so all slot loads are issued together
-    constexpr int kV = 8;
-    const int d = N, d4 = d >> 2;
-    const size_t stride4 = (size_t)M * d / 4;
-    for (int m = hid; m < M; m += nh) {
-      float4* hr = reinterpret_cast<float4*>(e.h + (size_t)m * d);
-      const float4* pr = reinterpret_cast<const float4*>(part + (size_t)m * d);
-      float4 v[kV];
-      float ss = 0.f;
-#pragma unroll
-      for (int j = 0; j < kV; ++j) {
-        const int i4 = threadIdx.x + j * nthr;
-        if (i4 < d4) {
-          const int ns = part_slots(plan, m, i4 * 4);
-          float4 acc = __ldcg(hr + i4);
-          float4 t[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) t[q] = q < ns ? __ldcg(pr + i4 + q * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
-          float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < ns) {
-              sum.x += t[q].x;
-              sum.y += t[q].y;
-              sum.z += t[q].z;
-              sum.w += t[q].w;
-            }
-          for (int q = 4; q < ns; ++q) {
-            const float4 x = __ldcg(pr + i4 + q * stride4);
-            sum.x += x.x;
-            sum.y += x.y;
-            sum.z += x.z;
-            sum.w += x.w;
-          }
-          acc.x += sum.x;
-          acc.y += sum.y;
-          acc.z += sum.z;
-          acc.w += sum.w;
-          v[j] = acc;
-          hr[i4] = acc;
-          ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
-        }
-      }
-      for (int i4 = threadIdx.x + kV * nthr; i4 < d4; i4 += nthr) {  // (d > 4 * kV * nthr only)
-        float4 acc = hr[i4];
-        const int ns = part_slots(plan, m, i4 * 4);
-        for (int q = 0; q < ns; ++q) {
-          const float4 x = __ldcg(pr + i4 + q * stride4);
-          acc.x += x.x;
-          acc.y += x.y;
-          acc.z += x.z;
-          acc.w += x.w;
-        }
-        hr[i4] = acc;
-        ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
-      }
-      if (e.w == nullptr || m < e.row_begin) continue;  // uniform per CTA
-      ss = warp_sum(ss);
-      __syncthreads();
-      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
-      __syncthreads();
-      if (threadIdx.x < 32) {
-        float t = threadIdx.x < (unsigned)(nthr >> 5) ? s_red[threadIdx.x] : 0.f;
-        t = warp_sum(t);
-        if (threadIdx.x == 0) s_red[0] = t;
-      }
-      __syncthreads();
-      const float r = 1.0f / sqrtf(s_red[0] / (float)d + e.eps);
-      const int mo = m - e.row_begin;
-      const uint2* w4 = reinterpret_cast<const uint2*>(e.w);
-      for (int i4 = threadIdx.x; i4 < d4; i4 += nthr) {
-        const int jj = (i4 - (int)threadIdx.x) / nthr;
-        float4 vv;
-        if (jj < kV) {
-#pragma unroll
-          for (int j = 0; j < kV; ++j)
-            if (j == jj) vv = v[j];
-        } else {
-          vv = hr[i4];
-        }
-        const uint2 wv = w4[i4];
-        uint2 o;
-        o.x = pack_bf2((vv.x * r) * __uint_as_float(wv.x << 16), (vv.y * r) * __uint_as_float(wv.x & 0xFFFF0000u));
-        o.y = pack_bf2((vv.z * r) * __uint_as_float(wv.y << 16), (vv.w * r) * __uint_as_float(wv.y & 0xFFFF0000u));
-        *reinterpret_cast<uint2*>(e.x + act_off(mo, i4 * 4, d, e.tm_out)) = o;
-      }
-    }
-  } else {  // kEpiSiluMul: N = 2 * ffn, [gate | up]; float4 groups, 4 in flight per thread
-    const int ffn = N >> 1, f4 = ffn >> 2;
-    const size_t total = (size_t)M * f4;
-    const size_t stride4 = (size_t)M * N / 4;
-    const size_t per = (total + nh - 1) / nh;
-    const size_t i0 = (size_t)hid * per, i1 = min(total, i0 + per);
-    const float4* p4 = reinterpret_cast<const float4*>(part);
-    for (size_t base = i0; base < i1; base += 4 * (size_t)nthr) {
-      float4 g[4], u[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const size_t idx = base + threadIdx.x + (size_t)j * nthr;
-        g[j] = u[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (idx < i1) {
-          const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
-          const size_t o = (size_t)m * (N / 4) + j4;
-          const int ng = part_slots(plan, m, j4 * 4), nu = part_slots(plan, m, ffn + j4 * 4);
-          float4 tg[4], tu[4];  // all slot loads in flight together (predicated, unrolled)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            tg[q] = q < ng ? __ldcg(p4 + o + q * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
-            tu[q] = q < nu ? __ldcg(p4 + o + f4 + q * stride4) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q < ng) {
-              g[j].x += tg[q].x;
-              g[j].y += tg[q].y;
-              g[j].z += tg[q].z;
-              g[j].w += tg[q].w;
-            }
-            if (q < nu) {
-              u[j].x += tu[q].x;
-              u[j].y += tu[q].y;
-              u[j].z += tu[q].z;
-              u[j].w += tu[q].w;
-            }
-          }
-          for (int q = 4; q < ng; ++q) {
-            const float4 x = __ldcg(p4 + o + q * stride4);
-            g[j].x += x.x;
-            g[j].y += x.y;
-            g[j].z += x.z;
-            g[j].w += x.w;
-          }
-          for (int q = 4; q < nu; ++q) {
-            const float4 x = __ldcg(p4 + o + f4 + q * stride4);
-            u[j].x += x.x;
-            u[j].y += x.y;
-            u[j].z += x.z;
-            u[j].w += x.w;
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const size_t idx = base + threadIdx.x + (size_t)j * nthr;
-        if (idx >= i1) continue;
-        const int m = (int)(idx / f4), j4 = (int)(idx - (size_t)m * f4);
-        uint2 o;
-        auto silu = [](float v) { return __fdividef(v, 1.0f + __expf(-v)); };  // as silu_mul_kernel
-        o.x = pack_bf2(silu(g[j].x) * u[j].x, silu(g[j].y) * u[j].y);
-        o.y = pack_bf2(silu(g[j].z) * u[j].z, silu(g[j].w) * u[j].w);
-        *reinterpret_cast<uint2*>(e.x + act_off(m, j4 * 4, ffn, e.tm_out)) = o;
-      }
-    }
-  }
-  if (e.tl) {
-    __syncthreads();
-    if (threadIdx.x == 0) e.tl[blockIdx.x * 4 + 3] = gt();
-  }
-}
-
-template <bool kW4>
-__global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
+__global__ void __launch_bounds__(192, 1)
     gemm_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                float* __restrict__ out, int stages, int rstages, int dbg, GemmEpi epi) {
+                float* __restrict__ out, int stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
   const int nk = plan.nk;
-  if (epi.tl && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    epi.tl[blockIdx.x * 4 + 0] = t;
-  }
 
   const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk
-  const uint32_t a_bytes = kW4 ? 32768u : 16384u;
-  const uint32_t raw_bytes = kW4 ? (uint32_t)kW4ChunkBytes : 0u;
-  const uint32_t stage_bytes = a_bytes + (kW4 ? 2 : 1) * b_bytes;  // A + B ring stage
-  const uint32_t raw_stage = (raw_bytes + 127u) & ~127u;             // W4: separate, deeper raw ring
+  const uint32_t a_bytes = 16384u;
+  const uint32_t stage_bytes = a_bytes + b_bytes;  // A + B ring stage
   const uint32_t tm_cols = TM <= 32 ? 32u : TM <= 64 ? 64u : TM <= 128 ? 128u : 256u;
 
   uint8_t* sbase = smem;
-  uint8_t* rbase = smem + (size_t)stages * stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(rbase + (size_t)rstages * raw_stage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbase + (size_t)stages * stage_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* afull = full + 2 * stages;
-  uint64_t* tfull = full + 3 * stages;   // [2] accumulator ready
+  uint64_t* tfull = full + 2 * stages;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
-  uint64_t* rfull = tempty + 2;          // [rstages] raw W4 chunk landed
-  uint64_t* rempty = rfull + rstages;    // [rstages] raw W4 chunk consumed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + rstages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   auto sA = [&](int s) { return sbase + (size_t)s * stage_bytes; };
   auto sB = [&](int s) { return sbase + (size_t)s * stage_bytes + a_bytes; };
-  auto sRaw = [&](int r) { return rbase + (size_t)r * raw_stage; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&afull[s], 256);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
-    }
-    for (int r = 0; r < rstages; ++r) {
-      mbar_init(&rfull[r], 1);
-      mbar_init(&rempty[r], 256);
     }
     fence_mbar_init();
   }
@@ -418,22 +187,16 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
   // depend on the previous kernel, so the first ring of weight chunks is
   // issued before the TMEM allocation / CTA barrier and the grid dependency.
   uint32_t npre = 0;
-  ChunkCursor cur(W, kW4 ? kW4ChunkBytes : kBf16ChunkBytes);
+  ChunkCursor cur(W, kBf16ChunkBytes);
   if (threadIdx.x == 0) {
     SegIter pre(plan, cta);
     int t, k0, k1;
-    const uint32_t cap = kW4 ? (uint32_t)rstages : (uint32_t)stages;
-    while (npre < cap && pre.next(t, k0, k1)) {
+    while (npre < (uint32_t)stages && pre.next(t, k0, k1)) {
       const int n_tile = t % plan.n_tiles;
       cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
-      for (int k = k0; k < k1 && npre < cap; ++k, ++npre, cur.advance()) {
-        if (kW4) {
-          mbar_expect_tx(&rfull[npre], raw_bytes);
-          bulk_g2s(sRaw(npre), cur.get(), raw_bytes, &rfull[npre]);
-        } else {
-          mbar_expect_tx(&full[npre], a_bytes + ((dbg & 1) ? 0u : b_bytes));
-          bulk_g2s(sA(npre), cur.get(), a_bytes, &full[npre]);
-        }
+      for (int k = k0; k < k1 && npre < (uint32_t)stages; ++k, ++npre, cur.advance()) {
+        mbar_expect_tx(&full[npre], a_bytes + b_bytes);
+        bulk_g2s(sA(npre), cur.get(), a_bytes, &full[npre]);
       }
     }
   }
@@ -458,24 +221,14 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
         cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
         for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
           if (it < npre) {  // weight chunk already in flight: only the activations remain
-            if (!kW4) {
-              if (dbg & 1) mbar_expect_tx(&full[it], 0);  // (debug) no B: balance nothing, arrive count already 1
-              else bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
-            }
+            bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
             continue;
           }
-          if (kW4) {  // raw int4 chunks only; the dequantisers fetch B
-            const int r = it % rstages;
-            if (it >= (uint32_t)rstages) mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
-            mbar_expect_tx(&rfull[r], raw_bytes);
-            bulk_g2s(sRaw(r), cur.get(), raw_bytes, &rfull[r]);
-          } else {
-            const int s = it % stages;
-            if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
-            mbar_expect_tx(&full[s], a_bytes + ((dbg & 1) ? 0u : b_bytes));
-            bulk_g2s(sA(s), cur.get(), a_bytes, &full[s]);
-            if (!(dbg & 1)) bulk_g2s(sB(s), xb + (size_t)k * b_bytes, b_bytes, &full[s]);
-          }
+          const int s = it % stages;
+          if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], a_bytes + b_bytes);
+          bulk_g2s(sA(s), cur.get(), a_bytes, &full[s]);
+          bulk_g2s(sB(s), xb + (size_t)k * b_bytes, b_bytes, &full[s]);
         }
       }
     }
@@ -495,19 +248,12 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
       const uint32_t d = tmem_base + acc * tm_cols;
       for (int k = k0; k < k1; ++k) {
         mbar_wait(&full[s], ph);
-        if (kW4) mbar_wait(&afull[s], ph);
         tc_fence_after();
         const uint64_t da = desc_add(dA0, s * stage_bytes), db = desc_add(dB0, s * stage_bytes);
         if (elect_one()) {
 #pragma unroll
-          for (int sub = 0; sub < (kW4 ? 2 : 1); ++sub) {
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              if (!(dbg & 2))
-                umma_bf16(d, desc_add(da, sub * 16384u + kk * 256u), desc_add(db, sub * b_bytes + kk * 256u), idesc,
-                          (k != k0 || sub != 0 || kk != 0) ? 1u : 0u);
-            }
-          }
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(d, desc_add(da, kk * 256u), desc_add(db, kk * 256u), idesc, (k != k0 || kk != 0) ? 1u : 0u);
           umma_commit(&empty[s]);
         }
         __syncwarp();
@@ -520,7 +266,7 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
       __syncwarp();
       ++u;
     }
-  } else if (warp < 6) {
+  } else {
     // ------------------------------------------------------------- epilogue
     pdl_wait();
     const int quad = warp & 3;
@@ -551,66 +297,12 @@ __global__ void __launch_bounds__(kW4 ? 448 : 192, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       ++u;
     }
-  } else if (kW4) {
-    // ---------------------------------------------------------- dequantisers
-    // thread: weight row `row` of the tile, 64-wide half `half` of the group
-    const int tid = threadIdx.x - 192;
-    const int row = tid & 127, half = tid >> 7;
-    const int rg = row >> 3, r = row & 7;
-    const __nv_bfloat162 bias = __floats2bfloat162_rn(136.0f, 136.0f);
-    pdl_wait();
-    SegIter seg(plan, cta);
-    int t, k0, k1;
-    uint32_t it = 0;
-    while (seg.next(t, k0, k1)) {
-      const int m_tile = t / plan.n_tiles;
-      const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
-      for (int k = k0; k < k1; ++k, ++it) {
-        const int s = it % stages, rs = it % rstages;
-        if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);  // MMA done with stage s
-        if (tid == 0) {
-          mbar_expect_tx(&full[s], 2 * b_bytes);
-          bulk_g2s(sB(s), xb + (size_t)(2 * k) * b_bytes, 2 * b_bytes, &full[s]);
-        }
-        mbar_wait(&rfull[rs], (it / rstages) & 1);
-        const uint8_t* raw = sRaw(rs);
-        const uint16_t sraw = *reinterpret_cast<const uint16_t*>(raw + 8192 + 2 * row);
-        __nv_bfloat162 sc;
-        sc.x = __ushort_as_bfloat16(sraw);
-        sc.y = sc.x;
-        uint8_t* a = sA(s) + half * 16384;
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int j = half * 2 + jj;
-          const uint4 q = *reinterpret_cast<const uint4*>(raw + (j * 128 + row) * 16);
-          const uint32_t words[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int c = jj * 4 + w;  // 8-element k_chunk within the 64-wide half
-            uint32_t o[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint32_t x = ((words[w] >> (4 * i)) & 0x000F000Fu) | 0x43004300u;  // bf16x2 (128+nib)
-              __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
-              v = __hmul2(__hsub2(v, bias), sc);  // exact code, then one rounding of code*scale
-              o[i] = *reinterpret_cast<uint32_t*>(&v);
-            }
-            *reinterpret_cast<uint4*>(a + ((rg * 8 + c) * 8 + r) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
-          }
-        }
-        fence_proxy_async_smem();
-        mbar_arrive(&afull[s]);
-        mbar_arrive(&rempty[rs]);
-      }
-    }
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem_base, 2 * tm_cols);
-  if (epi.op != kEpiNone) gemm_tail_gang(epi, plan, M, N, out, smem);
 }
-
 
 // MS_GEMM_DEBUG (experiments only): bit0 skip activation loads, bit1 skip MMAs,
 // bit2 (W4 TMEM) skip the dequant ALU work and TMEM stores.
@@ -653,7 +345,7 @@ __device__ __forceinline__ uint32_t nib_magic(uint32_t w) {
 template <int kG, int kGPS>
 __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                        float* __restrict__ out, int bstages, int rstages, int astages, int dbg, GemmEpi epi) {
+                        float* __restrict__ out, int bstages, int rstages, int astages, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -960,7 +652,6 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   __syncthreads();
   stamp(6, threadIdx.x == 0 ? 1 : 64);
   if (warp == 1) tmem_dealloc(tmem_base, 512);
-  if (epi.op != kEpiNone) gemm_tail_gang(epi, plan, M, N, out, smem);
 }
 
 // Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 3: fastest in the 7B step with 32 W4 layers).
@@ -996,49 +687,6 @@ static int pick_w4_stages(int TM, int gps, int* rstages, int* astages, size_t* s
   return bs;
 }
 
-static size_t stage_bytes_of(bool w4, int TM) {
-  const size_t b = (size_t)TM * 128;
-  return w4 ? 32768 + 2 * b : 16384 + b;
-}
-
-// BF16: one ring of up to 8 (A,B) stages.  W4: 2 (A,B) stages plus a deep raw
-// int4 ring so that enough weight bytes are in flight per SM.
-static int pick_stages(bool w4, int TM, int* rstages, size_t* smem_out) {
-  const size_t budget = 215 * 1024;
-  const size_t stage = stage_bytes_of(w4, TM);
-  int st, rs = 0;
-  if (w4) {
-    st = 2;
-    rs = (int)((budget - st * stage) / 8576);
-    if (rs > 16) rs = 16;
-    if (rs < 2) rs = 2;
-  } else {
-    static const int max_st = w4_env("MS_GEMM_STAGES", 8);  // (experiments) ring depth cap
-    st = (int)(budget / stage);
-    if (st > max_st) st = max_st;
-    if (st < 2) st = 2;
-  }
-  *rstages = rs;
-  *smem_out = st * stage + (size_t)rs * 8576 + (3 * st + 4 + 2 * rs) * 8 + 64;
-  return st;
-}
-
-// MS_W4_SMEM=1 selects the shared-memory dequant path (A operand in smem).
-static bool w4_tmem_path() {
-  static const bool on = [] {
-    const char* e = std::getenv("MS_W4_SMEM");
-    return !(e && e[0] == '1');
-  }();
-  return on;
-}
-
-
-// MS_W4_GPS=1 (experiments): one 128-wide K group per W4 pipeline unit.
-static int w4_gps() {
-  static const int v = w4_env("MS_W4_GPS", 2) == 1 ? 1 : 2;
-  return v;
-}
-
 void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages) {
   const int64_t chunks = (int64_t)(w.N / 128) * (w.K / (w4 ? 128 : 64));
   const int64_t p0 = w.first_chunk / w.chunks_per_page;
@@ -1054,8 +702,8 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
   GemmPlanDev p{};
   p.n_tiles = N / 128;
   p.TM = TM;
-  // W4 on the TMEM path: two 128-wide K groups per unit when K allows (MS_W4_GPS=1 disables)
-  p.nk = K / (w4 ? (w4_tmem_path() && w4_gps() == 2 && K % 256 == 0 ? 256 : 128) : 64);
+  // W4: two 128-wide K groups per pipeline unit when K allows
+  p.nk = K / (w4 ? (K % 256 == 0 ? 256 : 128) : 64);
   p.tiles = p.n_tiles * ((M + TM - 1) / TM);
   p.T = (int64_t)p.tiles * p.nk;
   p.C = (int)std::min<int64_t>(num_sms, p.T);
@@ -1085,7 +733,7 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
 
 template <int kG, int kGPS>
 static cudaError_t launch_w4_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                  float* out, cudaStream_t stream, const GemmEpi& epi) {
+                                  float* out, cudaStream_t stream) {
   int rs = 0, as = 0;
   size_t sm = 0;
   const int bs = pick_w4_stages(TM, kGPS, &rs, &as, &sm);
@@ -1095,52 +743,44 @@ static cudaError_t launch_w4_tmem(const GemmWeights& w, const uint16_t* x, int M
     attr = true;
   }
   return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M, TM,
-                    plan, out, bs, rs, as, gemm_debug(), epi);
+                    plan, out, bs, rs, as, gemm_debug());
 }
 
 template <int kGPS>
 static cudaError_t launch_w4_groups(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                    float* out, cudaStream_t stream, const GemmEpi& epi) {
+                                    float* out, cudaStream_t stream) {
   // no more dequantiser groups than TMEM A stages (a group holds one stage)
   int rs = 0, as = 0;
   size_t sm = 0;
   pick_w4_stages(TM, kGPS, &rs, &as, &sm);
   switch (std::min(w4_groups(), as)) {
-    case 3: return launch_w4_tmem<3, kGPS>(w, x, M, TM, plan, out, stream, epi);
-    case 4: return launch_w4_tmem<4, kGPS>(w, x, M, TM, plan, out, stream, epi);
-    default: return launch_w4_tmem<2, kGPS>(w, x, M, TM, plan, out, stream, epi);
+    case 3: return launch_w4_tmem<3, kGPS>(w, x, M, TM, plan, out, stream);
+    case 4: return launch_w4_tmem<4, kGPS>(w, x, M, TM, plan, out, stream);
+    default: return launch_w4_tmem<2, kGPS>(w, x, M, TM, plan, out, stream);
   }
 }
 
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                        float* out, cudaStream_t stream, const GemmEpi& epi) {
-  size_t smem = 0;
-  int rstages = 0;
-  const int stages = pick_stages(w4, TM, &rstages, &smem);
-  if (w4 && w4_tmem_path()) {
-    // the plan fixed the unit: K / nk = 256 -> two K groups per pipeline unit
-    if (w.K / plan.nk == 256) return launch_w4_groups<2>(w, x, M, TM, plan, out, stream, epi);
-    return launch_w4_groups<1>(w, x, M, TM, plan, out, stream, epi);
-  }
-  if (!w4 && epi.op == kEpiNone && gemm_2sm_ok(w, TM, plan)) return gemm_2sm_launch(w, x, M, plan, out, stream);
+                        float* out, cudaStream_t stream) {
   if (w4) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
-    }
-    return launch_pdl(gemm_kernel<true>, dim3(plan.C), dim3(448), smem, stream, w, x, M, TM, plan, out, stages,
-                      rstages, gemm_debug(), epi);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
-    }
-    return launch_pdl(gemm_kernel<false>, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, stages,
-                      rstages, gemm_debug(), epi);
+    // the plan fixed the unit: K / nk = 256 -> two K groups per pipeline unit
+    if (w.K / plan.nk == 256) return launch_w4_groups<2>(w, x, M, TM, plan, out, stream);
+    return launch_w4_groups<1>(w, x, M, TM, plan, out, stream);
   }
-  return cudaGetLastError();
+  static const int max_st = [] {  // (experiments) ring depth cap
+    const char* e = std::getenv("MS_GEMM_STAGES");
+    return e ? std::atoi(e) : 8;
+  }();
+  const size_t stage = (size_t)16384 + (size_t)TM * 128;
+  int st = (int)((size_t)(215 * 1024) / stage);
+  st = std::max(2, std::min(st, max_st));
+  const size_t smem = st * stage + (2 * st + 4) * 8 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  return launch_pdl(gemm_kernel, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, st);
 }
 
 }  // namespace ms

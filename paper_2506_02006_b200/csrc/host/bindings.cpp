@@ -195,12 +195,14 @@ PYBIND11_MODULE(_core, m) {
       "run_simulation",
       [](const py::dict& engine, const py::dict& arm, const Trace& trace, uint64_t seed, uintptr_t device,
          int vocab, const std::string& clock, bool record) {
-        const ClockMode cm = clock == "device" ? ClockMode::kDevice : ClockMode::kVirtual;
-        if (clock != "device" && clock != "virtual") throw std::invalid_argument("clock must be virtual or device");
+        const ClockMode cm = clock == "device" ? ClockMode::kDevice : clock == "wall" ? ClockMode::kWall : ClockMode::kVirtual;
+        if (clock != "device" && clock != "virtual" && clock != "wall")
+          throw std::invalid_argument("clock must be virtual, device or wall");
+        if (cm == ClockMode::kWall && device == 0) throw std::invalid_argument("wall clock needs a device");
         const EngineConfig ec = engine_from(engine);
         const ArmSpec as = arm_from(arm);
         if (device == 0) return result_dict(run_simulation(ec, as, trace, seed, nullptr, cm));
-        CAbiBackend backend(reinterpret_cast<ms_ctx*>(device), vocab, cm == ClockMode::kDevice);
+        CAbiBackend backend(reinterpret_cast<ms_ctx*>(device), vocab, cm != ClockMode::kVirtual);
         backend.set_recording(record, ec.model.num_layers);
         RunResult r;
         {

@@ -632,7 +632,11 @@ std::string MetricsReport::to_json() const {
   j += ",\"device\":{\"busy_ms\":" + jnum(device_busy_ms) + ",\"decode_ms\":" + jnum(decode_ms) +
        ",\"decode_steps\":" + std::to_string(decode_steps) + ",\"decode_tokens\":" + jnum(decode_tokens) +
        ",\"exposed_swap_stall_ms\":" + jnum(exposed_swap_stall_ms) + ",\"prefill_ms\":" + jnum(prefill_ms) +
-       ",\"prefill_tokens\":" + std::to_string(prefill_tokens) + ",\"swap_upload_ms\":" + jnum(swap_upload_ms) + "}";
+       ",\"prefill_tokens\":" + std::to_string(prefill_tokens) + ",\"swap_upload_ms\":" + jnum(swap_upload_ms) +
+       ",\"decode_steps_overlap\":" + std::to_string(decode_steps_overlap) +
+       ",\"decode_ms_overlap\":" + jnum(decode_ms_overlap) +
+       ",\"exposed_stall_ms_per_token\":" + jnum(exposed_stall_ms_per_token) +
+       ",\"host_gap_ms\":" + jnum(host_gap_ms) + ",\"graph_captures\":" + std::to_string(graph_captures) + "}";
   j += "}";
   return j;
 }

@@ -105,6 +105,16 @@ bool CAbiBackend::swap_ready(int layer, double* upload_ms) {
   return done != 0;
 }
 
+double CAbiBackend::swap_wait(int layer) {
+  auto it = tickets_.find(layer);
+  if (it == tickets_.end()) throw std::logic_error("swap_wait: no swap in flight");
+  float ms = 0.f;
+  ck(ms_swap_wait(ctx_, it->second, &ms), "ms_swap_wait");
+  return ms;
+}
+
+int64_t CAbiBackend::graph_captures() { return ms_graph_captures(ctx_); }
+
 void CAbiBackend::swap_commit(int layer, double* upload_ms) {
   auto it = tickets_.find(layer);
   if (it == tickets_.end()) throw std::logic_error("swap_commit: no swap in flight");

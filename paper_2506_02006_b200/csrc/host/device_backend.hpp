@@ -28,6 +28,8 @@ class CAbiBackend final : public DeviceBackend {
   void swap_begin(int layer, int bits) override;
   void swap_commit(int layer, double* upload_ms) override;
   bool swap_ready(int layer, double* upload_ms) override;
+  double swap_wait(int layer) override;
+  int64_t graph_captures() override;
   void kv_attach(BlockId first_id, int64_t n) override;
   void kv_detach(const std::vector<BlockId>& ids) override;
   void finish() override;

@@ -288,6 +288,11 @@ struct MetricsReport {
   double device_busy_ms = 0.0, decode_ms = 0.0, prefill_ms = 0.0, decode_tokens = 0.0;
   int64_t decode_steps = 0, prefill_tokens = 0;
   double swap_upload_ms = 0.0, exposed_swap_stall_ms = 0.0;
+  // kWall: decode steps that overlapped an in-flight upload, their time above
+  // the no-upload step-time model (least squares over the other steps:
+  // ms = a + b * kv_blocks + c * batch), host time between device steps
+  int64_t decode_steps_overlap = 0, graph_captures = 0;
+  double decode_ms_overlap = 0.0, exposed_stall_ms_per_token = 0.0, host_gap_ms = 0.0;
   std::string to_json() const;
 };
 struct EventLog {
@@ -329,12 +334,25 @@ class DeviceBackend {
   // receives the measured upload time.
   virtual void swap_commit(int layer, double* upload_ms) = 0;
   virtual bool swap_ready(int layer, double* upload_ms) = 0;
+  // Blocks (no spin) until the layer's upload has landed; returns its upload ms.
+  virtual double swap_wait(int layer) = 0;
+  // CUDA-graph captures made so far (graph-safe swaps: commits must not add any).
+  virtual int64_t graph_captures() { return 0; }
   virtual void kv_attach(BlockId first_id, int64_t n) = 0;
   virtual void kv_detach(const std::vector<BlockId>& ids) = 0;
   virtual void finish() = 0;
 };
 
-enum class ClockMode { kVirtual, kDevice };
+// kVirtual: every duration from the CostModel (byte-identical reference logs).
+// kDevice:  GPU-time simulation -- the clock advances by measured step times;
+//           a swap lasts its measured upload (the host waits for it, blocking).
+// kWall:    real clock -- events run on a steady wall clock (ms since start),
+//           arrivals are released at their trace times, a step completes when
+//           the GPU says so, and a swap completes at the first event boundary
+//           after its upload has landed (polled, never waited on): decode keeps
+//           running while the LayerSwapper's copies stream (reference
+//           engine.cpp:397-402 future-dated kSwapDone).
+enum class ClockMode { kVirtual, kDevice, kWall };
 
 struct ArmSpec {
   std::string label = "static-full";

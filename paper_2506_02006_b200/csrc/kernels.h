@@ -88,34 +88,8 @@ __host__ __device__ inline int part_slots(const GemmPlanDev& p, int m, int n) {
 
 GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t part_elems);
 
-// Row work fused into the GEMM's tail ("tail gang"): every CTA counts itself
-// in on `ctr` once its partials are written; the last `helpers` CTAs to arrive
-// wait for the rest and then do the row pass over the complete partials, so the
-// separate row kernel (and its launch + grid-dependency latency) disappears.
-// Deterministic: each output element is produced by one CTA summing the slots
-// in slot order, exactly as the standalone row kernels do.  `ctr` is a
-// monotonically increasing arrival counter; `base` = its value before this
-// launch (kept by the host), so no reset is needed.
-enum { kEpiNone = 0, kEpiResidualNorm = 1, kEpiSiluMul = 2 };
-struct GemmEpi {
-  int op = kEpiNone;
-  uint32_t* ctr = nullptr;  // [arrivals, helpers past the wait]: zero at launch, reset by the last helper
-  // residual + RMSNorm (N = d): h[M][d] += sum(partials); x = pack(bf16(norm(h) * w)) for rows >= row_begin
-  float* h = nullptr;
-  const uint16_t* w = nullptr;
-  float eps = 0.f;
-  int row_begin = 0;
-  // both: packed activation image of the next GEMM (tm_out rows per m-tile)
-  uint16_t* x = nullptr;
-  int tm_out = 0;
-  unsigned long long* tl = nullptr;  // (debug) per-CTA [start, arrive, released, done] globaltimer
-};
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                        float* out, cudaStream_t stream, const GemmEpi& epi = GemmEpi());
-// CTA-pair (cta_group::2) BF16 GEMM for whole-tile long-prefill plans (gemm2sm.cu)
-bool gemm_2sm_ok(const GemmWeights& w, int TM, const GemmPlanDev& plan);
-cudaError_t gemm_2sm_launch(const GemmWeights& w, const uint16_t* x, int M, const GemmPlanDev& plan, float* out,
-                            cudaStream_t stream);
+                        float* out, cudaStream_t stream);
 
 // Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
 // every layer): [layer][kv_head][K|V][token][head_dim] bf16.
@@ -153,23 +127,13 @@ struct AttnArgs {
   int out_packed;           // 1: packed activation image (K = H*hd, TM), 0: row-major [rows][H*hd]
   int TM;
   int stages;               // K/V ring depth (set by attn_decode_launch)
-  // persistent stream-K path (used when pws != nullptr and splits <= 1):
-  float* pws;               // [ctas][2][G][HD + 2] partial (acc, m, l) of items split between CTAs
-  int* pcnt;                // [rows * KVH] arrival counters, zero between launches (self-resetting)
-  int ctas;                 // persistent grid size (set by attn_decode_launch)
   int64_t arena_bytes;      // size of kv.arena (GQA tensor-core path: TMA tensor map over the arena)
   // CTA -> work item map (set by attn_decode_launch): items (row, kv_head) are
   // numbered row * KVH + kv_head; the first `whole_items` run as one CTA each,
-  // every later item is split over `tail_splits` CTAs (merged by the combine
-  // kernel) so the last wave of equal-sized items does not leave SMs idle.
+  // every later item is split over `tail_splits` CTAs (merged by the combine kernel).
   int whole_items;
   int tail_splits;
-  int ws_splits_max;        // splits the part_o / part_ml workspace can hold (tail splitting needs >= 2)
-  int max_blocks_hint;      // blocks of the longest row (tail pieces keep >= 4 blocks)
 };
-// Persistent-grid size and workspace floats the stream-K decode attention needs.
-int attn_persist_ctas(int num_sms);
-size_t attn_persist_ws_floats(int num_sms, int G, int HD);
 cudaError_t attn_decode_launch(const AttnArgs& a, cudaStream_t stream);
 
 // Causal prefill attention of ONE sequence (positions 0..n-1) over its paged KV.

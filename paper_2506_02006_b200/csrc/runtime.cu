@@ -117,11 +117,18 @@ struct FreePage {
   cudaEvent_t fence;  // compute-stream event that must complete before reuse (may be null)
 };
 
+// Device page tables: one per precision variant of the layer, at a fixed
+// address for the context's lifetime, holding the page addresses of that
+// variant's current image.  A decode step reads the table of the layer's
+// committed precision from device memory (nothing about the pages is baked
+// into kernel parameters), so a swap commit does not invalidate captured
+// CUDA graphs: graphs are keyed by the per-layer precision vector instead.
 struct Layer {
   int bits = 16;
-  int slot = 0;
+  int slot = 0;  // table of the committed precision (slot_of(bits))
   uint64_t* d_table[2] = {nullptr, nullptr};
   uint64_t* h_table[2] = {nullptr, nullptr};  // pinned staging
+  cudaEvent_t table_ev[2] = {nullptr, nullptr};  // last H2D copy out of h_table[slot] (host may rewrite after it)
   std::vector<int32_t> pages;
   cudaEvent_t last_release = nullptr;
   // in-flight swap
@@ -159,7 +166,9 @@ struct ms_ctx {
   char* arena = nullptr;
   ms::KvGeom kv{};
   std::vector<FreePage> free_pages;
-  std::vector<cudaEvent_t> events;  // all fence events (destroyed at the end)
+  std::vector<cudaEvent_t> events;      // every event made by new_event (destroyed at the end)
+  std::vector<cudaEvent_t> fence_live;  // compute fences that pages / layers may still reference
+  std::vector<cudaEvent_t> fence_pool;  // completed fences, free for reuse
   std::vector<int32_t> id_page;     // logical KV block id -> page (-1 unmapped)
   std::vector<Layer> layers;
   uint64_t next_ticket = 1;
@@ -185,21 +194,21 @@ struct ms_ctx {
   float* q = nullptr;
   float* attn_ws = nullptr;
   size_t attn_ws_elems = 0;
-  uint32_t* gang_ctr = nullptr;          // GEMM tail-gang counter pairs (ring, self-resetting)
   unsigned long long* am_key = nullptr;  // wide argmax: per-row best key (self-resetting)
   int* am_cnt = nullptr;                 // wide argmax: per-row arrival counter (self-resetting)
-  int gang_next = 0;
   std::vector<int> submitted;  // ring slots of submitted decode steps, oldest first
   // decode-step CUDA graphs (MS_GRAPH=1): keyed by staging slot / batch shape, dropped when
   // anything baked into the kernel parameters changes (layer tables, arena mappings)
   struct StepGraph {
     const int32_t* st_d;
     int n, mb, asplits, want_logits, has_tokens;
+    std::vector<int8_t> bits;  // per-layer precision the graph's kernels were chosen for
     int64_t launches;
     cudaGraphExec_t exec;
   };
   std::vector<StepGraph> graphs;
-  std::vector<std::array<int64_t, 5>> graph_seen;  // shapes seen once (captured on the second sighting)
+  std::vector<std::array<int64_t, 6>> graph_seen;  // shapes seen once (captured on the second sighting)
+  int64_t graph_captures = 0;
   uint64_t graph_gen = 0, graph_gen_built = 0;
   uint16_t* w4_scratch = nullptr;  // long prefills: BF16 copy of the W4 matrix being multiplied (lazy)
   size_t w4_scratch_bytes = 0;
@@ -207,8 +216,6 @@ struct ms_ctx {
   size_t trace_elems = 0;
   bool tracing = false;
   int64_t tl_counter = 0;
-  float* attn_pws = nullptr;   // persistent attention partials
-  int* attn_pcnt = nullptr;    // persistent attention item counters [max_batch * KVH]
   int32_t* next = nullptr;
   float* logits = nullptr;
   int max_blocks = 0;
@@ -266,19 +273,49 @@ void give_pages(ms_ctx* c, const std::vector<int32_t>& pages, cudaEvent_t fence)
   for (auto it = pages.rbegin(); it != pages.rend(); ++it) c->free_pages.push_back({*it, fence});
 }
 
+// Fence events are recycled: once a fence has completed, every free page and
+// layer that references it drops the reference, and the event returns to the
+// pool (a long serving run records one per detach / commit / reset).
+void reclaim_fences(ms_ctx* c) {
+  if (c->fence_live.size() < 8) return;  // amortised sweep
+  std::vector<cudaEvent_t> done, live;
+  for (cudaEvent_t e : c->fence_live) (cudaEventQuery(e) == cudaSuccess ? done : live).push_back(e);
+  if (done.empty()) return;
+  std::sort(done.begin(), done.end());
+  auto is_done = [&](cudaEvent_t e) { return e && std::binary_search(done.begin(), done.end(), e); };
+  for (auto& fp : c->free_pages)
+    if (is_done(fp.fence)) fp.fence = nullptr;
+  for (auto& L : c->layers)
+    if (is_done(L.last_release)) L.last_release = nullptr;
+  c->fence_live.swap(live);
+  c->fence_pool.insert(c->fence_pool.end(), done.begin(), done.end());
+}
+
 cudaEvent_t compute_fence(ms_ctx* c) {
-  cudaEvent_t e = new_event(c);
+  reclaim_fences(c);
+  cudaEvent_t e;
+  if (!c->fence_pool.empty()) {
+    e = c->fence_pool.back();
+    c->fence_pool.pop_back();
+  } else {
+    e = new_event(c);
+  }
   CK(cudaEventRecord(e, c->compute));
+  c->fence_live.push_back(e);
   return e;
 }
 
 const ImageGeom& geom_of(ms_ctx* c, int bits) { return bits == 16 ? c->geom16 : c->geom4; }
+int slot_of(int bits) { return bits == 16 ? 0 : 1; }
 
 // Write the page-address table of `pages` into layer slot `slot` (on stream s).
 void write_table(ms_ctx* c, Layer& L, int slot, const std::vector<int32_t>& pages, cudaStream_t s) {
+  if (L.table_ev[slot]) CK(cudaEventSynchronize(L.table_ev[slot]));  // the previous copy out of h_table[slot]
+  else L.table_ev[slot] = new_event(c);
   for (size_t i = 0; i < pages.size(); ++i)
     L.h_table[slot][i] = (uint64_t)(c->arena + (int64_t)pages[i] * c->page_bytes);
   CK(cudaMemcpyAsync(L.d_table[slot], L.h_table[slot], pages.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(L.table_ev[slot], s));
 }
 
 // Upload granularity: the LayerSwapper's H2D copies share the copy engines
@@ -348,38 +385,21 @@ void make_resident_bf16(ms_ctx* c) {
     if (!L.pages.empty()) give_pages(c, L.pages, nullptr);
     L.pages = take_pages(c, c->geom16.pages, c->compute);
     L.bits = 16;
-    L.slot = 0;
+    L.slot = slot_of(16);
     upload_image(c, L.host_img[0], c->geom16, L.pages, c->compute);
-    write_table(c, L, 0, L.pages, c->compute);
+    write_table(c, L, L.slot, L.pages, c->compute);
   }
   CK(cudaStreamSynchronize(c->compute));
   c->weights_ready = true;
 }
 
+// The layer's matrix as the GEMM reads it: through the device page table of
+// its committed precision (never inlined: the table's content changes on swaps
+// while captured graphs keep their parameters).
 ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
   Layer& L = c->layers[l];
   const ImageGeom& g = geom_of(c, L.bits);
-  ms::GemmWeights w{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
-  ms::gemm_inline_pages(w, L.bits == 4, L.h_table[L.slot]);
-  return w;
-}
-
-constexpr int kGangCounters = 256;
-
-// MS_FUSE_ROWS=1 (experiment, off by default): residual-norm / SiLU in the
-// GEMM tails (tail gang) instead of standalone row kernels.  Measured slower
-// on the 7B decode step (14.43 vs 13.76 ms: the tail's row pass runs on the
-// last-arriving CTAs after the slowest one), so the standalone kernels stay
-// the default.  (A run that looked faster was a CUDA-graph replay bug: the
-// arrival counters' bases were baked into captured launches, so replayed
-// tails did not wait; the counters now reset themselves, gemm_tail_gang.)
-bool fuse_rows(int M) {
-  static const bool v = [] {
-    const char* e = std::getenv("MS_FUSE_ROWS");
-    return e && e[0] == '1';
-  }();
-  (void)M;
-  return v;
+  return ms::GemmWeights{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
 }
 
 // Rows from which a W4A16 layer's GEMM runs as a BF16 GEMM over a dequantised
@@ -416,8 +436,8 @@ ms::GemmWeights w4_as_bf16(ms_ctx* c, const ms::GemmWeights& w4w) {
   return b;
 }
 
-ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w_in, bool w4, int M, int TM, ms::GemmEpi epi = ms::GemmEpi()) {
-  bool dq = w4 && w4_dequant_rows() > 0 && M >= w4_dequant_rows() && epi.op == ms::kEpiNone;
+ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w_in, bool w4, int M, int TM) {
+  bool dq = w4 && w4_dequant_rows() > 0 && M >= w4_dequant_rows();
   if (dq) {  // never while a decode step is being captured (the scratch may need allocating)
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(c->compute, &cs));
@@ -432,61 +452,9 @@ ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w_in, bool w4, int M, int
   } no_pdl(dq);
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
   const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, w4, c->num_sms, c->part_elems);
-  if (epi.op != ms::kEpiNone) {  // next counter pair of the ring (self-resetting, see gemm_tail_gang)
-    const int i = c->gang_next;
-    c->gang_next = (c->gang_next + 1) % kGangCounters;
-    epi.ctr = c->gang_ctr + 2 * i;
-  }
-  static unsigned long long* tl = nullptr;  // (debug) MS_TAIL_TL=<layer*4+mat>: dump that GEMM's tail timeline
-  static const int tl_pick = [] {
-    const char* e = std::getenv("MS_TAIL_TL");
-    return e ? std::atoi(e) : -1;
-  }();
-  if (tl_pick >= 0 && epi.op != ms::kEpiNone && c->tl_counter++ == tl_pick) {
-    if (!tl) CK(cudaMalloc(&tl, 4096 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(tl, 0, 4096 * sizeof(unsigned long long), c->compute));
-    epi.tl = tl;
-    CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute, epi));
-    std::vector<unsigned long long> h(4 * plan.C);
-    CK(cudaMemcpyAsync(h.data(), tl, h.size() * 8, cudaMemcpyDeviceToHost, c->compute));
-    CK(cudaStreamSynchronize(c->compute));
-    unsigned long long t0 = ~0ull;
-    for (int i = 0; i < plan.C; ++i) t0 = std::min(t0, h[4 * i]);
-    double a_min = 1e30, a_max = 0, r_max = 0, d_max = 0, s_max = 0;
-    for (int i = 0; i < plan.C; ++i) {
-      s_max = std::max(s_max, (h[4 * i] - t0) / 1e3);
-      a_min = std::min(a_min, (h[4 * i + 1] - t0) / 1e3);
-      a_max = std::max(a_max, (h[4 * i + 1] - t0) / 1e3);
-      if (h[4 * i + 2]) r_max = std::max(r_max, (h[4 * i + 2] - t0) / 1e3);
-      if (h[4 * i + 3]) d_max = std::max(d_max, (h[4 * i + 3] - t0) / 1e3);
-    }
-    fprintf(stderr, "tail tl op=%d C=%d N=%d: last start %.2f us, arrivals %.2f..%.2f, released by %.2f, done %.2f\n",
-            epi.op, plan.C, w.N, s_max, a_min, a_max, r_max, d_max);
-  } else {
-    CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute, epi));
-  }
+  CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute));
   c->launches += 1;
   return plan;
-}
-
-ms::GemmEpi epi_norm(ms_ctx* c, const uint16_t* w, int tm_out, int row_begin) {
-  ms::GemmEpi e;
-  e.op = ms::kEpiResidualNorm;
-  e.h = c->h;
-  e.w = w;
-  e.eps = c->desc.rms_eps;
-  e.row_begin = row_begin;
-  e.x = c->x;
-  e.tm_out = tm_out;
-  return e;
-}
-
-ms::GemmEpi epi_silu(ms_ctx* c, int tm_out) {
-  ms::GemmEpi e;
-  e.op = ms::kEpiSiluMul;
-  e.x = c->x;
-  e.tm_out = tm_out;
-  return e;
 }
 
 // categories of ms_prof_kernels_read (include/morphserve.h MS_PK_*)
@@ -512,8 +480,8 @@ void prof_mark(ms_ctx* c) {
   CK(cudaEventRecord(c->prof_ev[c->prof_used++], c->compute));
 }
 
-// MS_ATTN_PERSIST=1 (experiments): persistent stream-K decode attention
-// instead of one CTA per (kv_head, row, split).
+constexpr int kAttnMaxSplits = 16;
+
 // Decode steps replay from captured CUDA graphs (MS_GRAPH=0 disables): a shape
 // is captured the second time it is seen, at most kMaxGraphs are kept.
 constexpr size_t kMaxGraphs = 64;
@@ -531,14 +499,6 @@ void drop_graphs(ms_ctx* c) {
   c->graph_seen.clear();
 }
 
-bool attn_persistent() {
-  static const bool v = [] {
-    const char* e = std::getenv("MS_ATTN_PERSIST");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
 int attn_splits(ms_ctx* c, int rows, int max_ctx) {
   static const int forced = [] {  // MS_ATTN_SPLITS (experiments)
     const char* e = std::getenv("MS_ATTN_SPLITS");
@@ -553,19 +513,10 @@ int attn_splits(ms_ctx* c, int rows, int max_ctx) {
   const int target = c->num_sms * (gqa ? 2 : 4);
   int s = 1;
   const int nb = (max_ctx + 15) / 16;
-  while (ctas * s < target && s < 32 && nb / (s * 2) >= 8) s *= 2;
-  while (s > 1 && (size_t)s * rows * c->desc.num_heads * (c->desc.head_dim + 2) > c->attn_ws_elems) s /= 2;
+  // at most kAttnMaxSplits: forward() lays the workspace out for that many
+  // split slots (part_o [kAttnMaxSplits][rows][H][hd], then part_ml)
+  while (ctas * s < target && s < kAttnMaxSplits && nb / (s * 2) >= 8) s *= 2;
   return s;
-}
-
-// MS_SKIP (timing experiments only, results become garbage): bit0 qkv_post,
-// bit1 residual_norm, bit2 silu_mul, bit3 attention, bit4 layer GEMMs.
-int skip_mask() {
-  static const int v = [] {
-    const char* e = std::getenv("MS_SKIP");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
 }
 
 // The decoder over M rows whose per-row metadata already sits in device memory.
@@ -585,22 +536,16 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       CK(cudaMemcpyAsync(c->trace_h + (size_t)l * M * d, c->h, (size_t)M * d * sizeof(float), cudaMemcpyDeviceToDevice,
                          c->compute));
     const bool w4 = c->layers[l].bits == 4;
-    const int skip = skip_mask();
-    ms::GemmPlanDev s = (skip & 16) ? ms::gemm_plan(1024, 1024, M, TM, false, c->num_sms, c->part_elems)
-                                    : gemm(c, mat_weights(c, l, 0), w4, M, TM);
+    ms::GemmPlanDev s = gemm(c, mat_weights(c, l, 0), w4, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_QKV_W4 : MS_PK_GEMM_QKV);
-    // decode: the attention kernel does the QKV post-processing itself
-    const bool fuse_qkv = d_page_row == nullptr && !attn_persistent();
-    if (!fuse_qkv) {
-      if (!(skip & 1))
-        CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
-                               d_page_row, page_stride, c->q, c->compute));
-      c->launches += 1;
-      pk_mark(c, MS_PK_QKV_POST);
-    }
     prof_mark(c);
     if (d_page_row != nullptr) {
-      // prefill: one sequence, tiled causal attention (page table row 0)
+      // prefill: one sequence, QKV post-processing (RoPE + K/V append) then
+      // tiled causal attention (page table row 0)
+      CK(ms::qkv_post_launch(c->part, s, M, H, KVH, hd, c->rope_cos, c->rope_sin, d_pos, c->kv, l, d_pages,
+                             d_page_row, page_stride, c->q, c->compute));
+      c->launches += 1;
+      pk_mark(c, MS_PK_QKV_POST);
       ms::PrefillAttnArgs pa{};
       pa.q = c->q;
       pa.kv = c->kv;
@@ -613,15 +558,15 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       pa.out = c->x;
       pa.TM = TM;
       pa.arena_bytes = (int64_t)c->desc.arena_pages * c->page_bytes;
-      if (!(skip & 8)) CK(ms::prefill_attn_launch(pa, c->compute));
+      CK(ms::prefill_attn_launch(pa, c->compute));
       c->launches += 1;
     } else {
+      // decode: the attention kernel does the QKV post-processing itself
       ms::AttnArgs a{};
-      a.q = c->q;
       a.kv = c->kv;
       a.layer = l;
       a.pages = d_pages;
-      a.page_row = d_page_row;
+      a.page_row = nullptr;
       a.page_stride = page_stride;
       a.ctx_len = d_ctx;
       a.rows = M;
@@ -629,62 +574,43 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
       a.KVH = KVH;
       a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
       a.splits = asplits;
+      // workspace laid out for kAttnMaxSplits split slots
       a.part_o = c->attn_ws;
-      // workspace laid out for up to 16 splits (uniform split-KV or tail splitting)
-      a.part_ml = c->attn_ws + (size_t)16 * M * H * hd;
-      a.ws_splits_max = 16;
-      a.max_blocks_hint = (max_ctx + 15) / 16;
-      if (fuse_qkv) {
-        a.qkv_part = c->part;
-        a.qkv_plan = s;
-        a.rope_cos = c->rope_cos;
-        a.rope_sin = c->rope_sin;
-        a.pos = d_pos;
-      }
-      if (attn_persistent()) {  // stream-K attention balances any context mix by itself
-        a.splits = 1;
-        a.pws = c->attn_pws;
-        a.pcnt = c->attn_pcnt;
-      }
+      a.part_ml = c->attn_ws + (size_t)kAttnMaxSplits * M * H * hd;
+      a.qkv_part = c->part;
+      a.qkv_plan = s;
+      a.rope_cos = c->rope_cos;
+      a.rope_sin = c->rope_sin;
+      a.pos = d_pos;
       a.out = c->x;
       a.out_packed = 1;
       a.TM = TM;
       a.arena_bytes = (int64_t)c->desc.arena_pages * c->page_bytes;
-      if (!(skip & 8)) CK(ms::attn_decode_launch(a, c->compute));
+      CK(ms::attn_decode_launch(a, c->compute));
       c->launches += asplits > 1 ? 2 : 1;
     }
     pk_mark(c, MS_PK_ATTN);
     prof_mark(c);
-    // residual + RMSNorm and SiLU*up run in the GEMM tails (tail gang) unless
-    // disabled or a timing experiment skips pieces of the step
-    const bool fuse = fuse_rows(M) && skip == 0;
     const uint16_t* n2 = c->norms + ((size_t)l * 2 + 1) * d;
-    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 1), w4, M, TM, fuse ? epi_norm(c, n2, TM, 0) : ms::GemmEpi());
+    s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_O_W4 : MS_PK_GEMM_O);
-    if (!fuse) {
-      if (!(skip & 2)) CK(ms::residual_norm_launch(c->part, s, M, d, c->h, n2, D.rms_eps, c->x, TM, c->compute));
-      c->launches += 1;
-      pk_mark(c, MS_PK_NORM);
-    }
-    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 2), w4, M, TM, fuse ? epi_silu(c, TM) : ms::GemmEpi());
+    CK(ms::residual_norm_launch(c->part, s, M, d, c->h, n2, D.rms_eps, c->x, TM, c->compute));
+    c->launches += 1;
+    pk_mark(c, MS_PK_NORM);
+    s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_GU_W4 : MS_PK_GEMM_GU);
-    if (!fuse) {
-      if (!(skip & 4)) CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
-      c->launches += 1;
-      pk_mark(c, MS_PK_SILU);
-    }
+    CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
+    c->launches += 1;
+    pk_mark(c, MS_PK_SILU);
     const bool last = l == D.num_layers - 1;
     const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
     const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
     const int row_begin = last ? final_row_begin : 0;
-    if (!(skip & 16)) s = gemm(c, mat_weights(c, l, 3), w4, M, TM, fuse ? epi_norm(c, nw, tm_out, row_begin) : ms::GemmEpi());
+    s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_DOWN_W4 : MS_PK_GEMM_DOWN);
-    if (!fuse) {
-      if (!(skip & 2) || last)
-        CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out, row_begin, c->compute));
-      c->launches += 1;
-      pk_mark(c, MS_PK_NORM);
-    }
+    CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out, row_begin, c->compute));
+    c->launches += 1;
+    pk_mark(c, MS_PK_NORM);
   }
   if (c->tracing)  // after the last layer (before the final norm)
     CK(cudaMemcpyAsync(c->trace_h + (size_t)D.num_layers * M * d, c->h, (size_t)M * d * sizeof(float),
@@ -828,17 +754,10 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       CK(cudaMalloc(&c->q, (size_t)c->max_rows * H * hd * sizeof(float)));
       c->attn_ws_elems = (size_t)16 * desc->max_batch * H * (hd + 2);
       CK(cudaMalloc(&c->attn_ws, c->attn_ws_elems * sizeof(float)));
-      CK(cudaMalloc(&c->attn_pws, ms::attn_persist_ws_floats(c->num_sms, H / desc->num_kv_heads, hd) * sizeof(float)));
-      CK(cudaMalloc(&c->attn_pcnt, (size_t)std::max(desc->max_batch, desc->max_prefill_tokens) * desc->num_kv_heads *
-                                       sizeof(int)));
-      CK(cudaMemset(c->attn_pcnt, 0, (size_t)std::max(desc->max_batch, desc->max_prefill_tokens) *
-                                         desc->num_kv_heads * sizeof(int)));
       CK(cudaMalloc(&c->am_key, (size_t)c->max_rows * sizeof(unsigned long long)));
       CK(cudaMemset(c->am_key, 0, (size_t)c->max_rows * sizeof(unsigned long long)));
       CK(cudaMalloc(&c->am_cnt, (size_t)c->max_rows * sizeof(int)));
       CK(cudaMemset(c->am_cnt, 0, (size_t)c->max_rows * sizeof(int)));
-      CK(cudaMalloc(&c->gang_ctr, 2 * kGangCounters * sizeof(uint32_t)));
-      CK(cudaMemset(c->gang_ctr, 0, 2 * kGangCounters * sizeof(uint32_t)));
       CK(cudaMalloc(&c->next, (size_t)c->max_rows * sizeof(int32_t)));
       CK(cudaMalloc(&c->logits, (size_t)desc->max_batch * desc->vocab * sizeof(float)));
       CK(cudaHostAlloc(&c->h_next, (size_t)c->max_rows * sizeof(int32_t), cudaHostAllocDefault));
@@ -909,7 +828,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
-                 c->h, c->x, c->part, c->q, c->attn_ws, c->attn_pws, c->attn_pcnt, c->gang_ctr, c->am_key, c->am_cnt, c->next, c->logits, c->hist};
+                 c->h, c->x, c->part, c->q, c->attn_ws, c->am_key, c->am_cnt, c->next, c->logits, c->hist};
   for (void* p : dev) cudaFree(p);
   cudaFreeHost(c->h_next);
   cudaFreeHost(c->h_logits);
@@ -1079,7 +998,7 @@ int ms_swap_begin(ms_ctx* c, int layer, int bits, uint64_t* ticket) {
     if (L.last_release) CK(cudaStreamWaitEvent(c->copy, L.last_release, 0));
     L.new_pages = take_pages(c, g.pages, c->copy);
     CK(cudaEventRecord(L.ev_start, c->copy));
-    write_table(c, L, L.slot ^ 1, L.new_pages, c->copy);
+    write_table(c, L, slot_of(bits), L.new_pages, c->copy);
     upload_image(c, L.host_img[bits == 16 ? 0 : 1], g, L.new_pages, c->copy);
     CK(cudaEventRecord(L.ev_done, c->copy));
     L.in_flight = true;
@@ -1122,7 +1041,8 @@ int ms_swap_wait(ms_ctx* c, uint64_t ticket, float* upload_ms) {
 
 int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
   return guard([&] {
-    c->graph_gen++;  // layer table changes: captured steps are stale
+    // no graph invalidation: steps read the layer's page table from device
+    // memory and graphs are keyed by the precision vector (see struct Layer)
     Layer& L = ticket_layer(c, ticket);
     CK(cudaSetDevice(c->device));
     // Token-boundary flip: steps launched from now on use the new image; the
@@ -1133,8 +1053,8 @@ int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
     give_pages(c, L.pages, fence);
     L.pages = std::move(L.new_pages);
     L.new_pages.clear();
-    L.slot ^= 1;
     L.bits = L.to_bits;
+    L.slot = slot_of(L.bits);
     L.in_flight = false;
     L.last_release = fence;
     if (pages_freed) *pages_freed = freed;
@@ -1143,7 +1063,6 @@ int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
 
 int ms_reset_state(ms_ctx* c) {
   return guard([&] {
-    c->graph_gen++;
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->compute));
     CK(cudaStreamSynchronize(c->copy));
@@ -1190,12 +1109,16 @@ int ms_kv_attach(ms_ctx* c, int64_t first_id, int64_t n) {
 
 int ms_kv_detach(ms_ctx* c, const int64_t* ids, int64_t n) {
   return guard([&] {
+    if (n < 0 || (n > 0 && !ids)) fail(MS_EVALIDATION, "kv detach: bad id list");
+    // validate every id (mapped, no duplicates) before unmapping any of them
     std::vector<int32_t> pages;
     pages.reserve(n);
-    for (int64_t i = 0; i < n; ++i) {
-      pages.push_back(page_of(c, ids[i]));
-      c->id_page[ids[i]] = -1;
-    }
+    for (int64_t i = 0; i < n; ++i) pages.push_back(page_of(c, ids[i]));
+    std::vector<int64_t> sorted(ids, ids + n);
+    std::sort(sorted.begin(), sorted.end());
+    if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+      fail(MS_EVALIDATION, "kv detach: duplicate block id");
+    for (int64_t i = 0; i < n; ++i) c->id_page[ids[i]] = -1;
     give_pages(c, pages, compute_fence(c));
   });
 }
@@ -1205,6 +1128,16 @@ int64_t ms_free_pages(ms_ctx* c) { return c ? (int64_t)c->free_pages.size() : -1
 int64_t ms_kv_page_of(ms_ctx* c, int64_t id) {
   if (!c || id < 0 || id >= (int64_t)c->id_page.size()) return -1;
   return c->id_page[id];
+}
+
+int ms_kv_export(ms_ctx* c, int64_t id, void* host_out, int64_t bytes) {
+  return guard([&] {
+    if (!host_out || bytes < c->page_bytes) fail(MS_EVALIDATION, "kv export: buffer smaller than one page");
+    const int32_t page = page_of(c, id);
+    CK(cudaMemcpyAsync(host_out, c->arena + (int64_t)page * c->page_bytes, c->page_bytes, cudaMemcpyDeviceToHost,
+                       c->compute));
+    CK(cudaStreamSynchronize(c->compute));
+  });
 }
 
 // ------------------------------------------------------------ token history
@@ -1299,14 +1232,20 @@ int decode_enqueue(ms_ctx* c, const ms_decode_batch* b, bool want_logits) {
       }
       const int asplits = attn_splits(c, n, max_ctx);
       const int wl = want_logits;
+      std::vector<int8_t> bits(c->layers.size());
+      uint64_t bits_hash = 1469598103934665603ull;
+      for (size_t l = 0; l < bits.size(); ++l) {
+        bits[l] = (int8_t)c->layers[l].bits;
+        bits_hash = (bits_hash ^ (uint64_t)(uint8_t)bits[l]) * 1099511628211ull;
+      }
       ms_ctx::StepGraph* g = nullptr;
       for (auto& x : c->graphs)
         if (x.st_d == st.d && x.n == n && x.mb == mb && x.asplits == asplits && x.want_logits == wl &&
-            x.has_tokens == 0)
+            x.has_tokens == 0 && x.bits == bits)
           g = &x;
       bool capture = false;
       if (!g) {
-        const std::array<int64_t, 5> key{(int64_t)st.d, n, mb, asplits, wl};
+        const std::array<int64_t, 6> key{(int64_t)st.d, n, mb, asplits, wl, (int64_t)bits_hash};
         auto it = std::find(c->graph_seen.begin(), c->graph_seen.end(), key);
         if (it == c->graph_seen.end()) {
           if (c->graph_seen.size() >= 4 * kMaxGraphs) c->graph_seen.clear();
@@ -1327,7 +1266,8 @@ int decode_enqueue(ms_ctx* c, const ms_decode_batch* b, bool want_logits) {
         cudaGraphExec_t exec;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         CK(cudaGraphDestroy(graph));
-        c->graphs.push_back({st.d, n, mb, asplits, wl, 0, c->launches - l0, exec});
+        c->graphs.push_back({st.d, n, mb, asplits, wl, 0, bits, c->launches - l0, exec});
+        c->graph_captures += 1;
         c->launches = l0;
         g = &c->graphs.back();
       }
@@ -1473,6 +1413,7 @@ int ms_kv_fill_synthetic(ms_ctx* c, const int64_t* ids, int64_t n, uint64_t seed
 
 // ------------------------------------------------------------ instrumentation
 int64_t ms_launch_count(ms_ctx* c) { return c ? c->launches : -1; }
+int64_t ms_graph_captures(ms_ctx* c) { return c ? c->graph_captures : -1; }
 
 int ms_timer_start(ms_ctx* c) {
   return guard([&] {
@@ -1616,7 +1557,6 @@ int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int 
     a.splits = splits < 1 ? 1 : splits;
     a.part_o = workspace;
     a.part_ml = workspace ? workspace + (size_t)a.splits * rows * H * hd : nullptr;
-    a.ws_splits_max = a.splits;
     a.out = out;
     a.out_packed = 0;
     a.TM = 16;
@@ -1628,21 +1568,6 @@ int ms_k_attn_decode(const float* q, const void* arena, int64_t page_bytes, int 
       a.arena_bytes = (int64_t)(mx + 1) * page_bytes;
     }
     if (a.splits > 1 && !workspace) fail(MS_EVALIDATION, "attn: split-KV needs a workspace");
-    if (splits == 0) {  // persistent stream-K kernel (the decode-step path)
-      static thread_local float* pws = nullptr;
-      static thread_local int* pcnt = nullptr;
-      int dev = 0, sms = 148;
-      CK(cudaGetDevice(&dev));
-      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      if (!pws) {
-        CK(cudaMalloc(&pws, ms::attn_persist_ws_floats(sms, 8, 128) * sizeof(float)));
-        CK(cudaMalloc(&pcnt, (size_t)(1 << 16) * sizeof(int)));
-        CK(cudaMemset(pcnt, 0, (size_t)(1 << 16) * sizeof(int)));
-      }
-      if ((size_t)rows * KVH > (1 << 16)) fail(MS_EVALIDATION, "attn: too many rows x kv heads");
-      a.pws = pws;
-      a.pcnt = pcnt;
-    }
     CK(ms::attn_decode_launch(a, (cudaStream_t)stream));
   });
 }

@@ -138,6 +138,13 @@ class DeviceModel:
     def page_of(self, block_id: int) -> int:
         return self.lib.ms_kv_page_of(self.h, block_id)
 
+    def kv_export(self, block_id: int) -> np.ndarray:
+        """One block's KV page (bf16 as u16): [L][KVH][2][16][hd]."""
+        s = self.shape
+        out = np.empty((s["L"], s["KVH"], 2, 16, s["hd"]), np.uint16)
+        N.check(self.lib.ms_kv_export(self.h, block_id, out.ctypes.data, out.nbytes))
+        return out
+
     # -- token history
     def hist_reserve(self, slots: int, max_len: int):
         N.check(self.lib.ms_hist_reserve(self.h, slots, max_len))

@@ -9,6 +9,13 @@ Fixtures:
   kvpool.json      reference KvBlockPool op sequences and their results
   generator.json   first values of the counter RNG weight generator (C oracle)
   engine_*.log     reference event logs for small engine scenarios (sha256 + text)
+  decoder_tiny.npz the C oracle's Llama-style decoder on BASELINE config 1 (tiny
+                   model, seed 7): prefill logits of 4 prompts, then 12 greedy
+                   decode steps with layer 1 switched to W4 g128 after step 4
+                   (logits + tokens).  Freezes the decoder contract (DESIGN.md
+                   section 4) so that a matched change to the oracle and a
+                   kernel cannot pass silently: tests/test_oracle_decoder.py
+                   recomputes it bit for bit.
 """
 import hashlib
 import json
@@ -69,7 +76,41 @@ def generator():
             "first": O.gen_weight(7, 17, 64, 0.0625).tolist()}
 
 
+TINY = dict(L=4, d=256, H=4, KVH=2, hd=64, ffn=768, V=1024, max_pos=128)
+
+
+def decoder_tiny():
+    """(prompts, prefill logits, decode tokens, decode logits) of the oracle."""
+    rng = np.random.default_rng(3)
+    B, P, steps = 4, 24, 12
+    prompts = rng.integers(0, TINY["V"], size=(B, P)).astype(np.int32)
+    m = O.RefModel(TINY, 7)
+    try:
+        seqs = [m.new_seq(P + steps + 1) for _ in range(B)]
+        pre, toks = [], []
+        for b in range(B):
+            t, lg = m.prefill(seqs[b], prompts[b])
+            pre.append(lg)
+            toks.append(t)
+        toks = np.array(toks, np.int32)
+        dtok, dlog = [], []
+        for step in range(steps):
+            if step == 4:
+                m.set_precision(1, 4)
+            nxt, lg = m.forward(seqs, toks)
+            dtok.append(nxt.copy())
+            dlog.append(lg.copy())
+            toks = nxt
+    finally:
+        m.close()
+    return dict(prompts=prompts, prefill_logits=np.array(pre, np.float32), decode_tokens=np.array(dtok, np.int32),
+                decode_logits=np.array(dlog, np.float32), first_tokens=np.array([int(np.argmax(x)) for x in pre],
+                                                                                np.int32))
+
+
 def main():
+    O.build(ref=False)
+    np.savez_compressed(os.path.join(HERE, "decoder_tiny.npz"), **decoder_tiny())
     O.build(ref=True)
     ref = O.ref_core()
     with open(os.path.join(HERE, "quantizer.json"), "w") as f:

@@ -129,13 +129,14 @@ def test_gemm_w4(Nn, K, M, TM, splits):
     (8, 8, 128, [1, 33, 250], 1),
     (32, 8, 128, [2048, 7, 300], 4),
     (8, 1, 128, [64, 129], 2),
-    # splits=0: persistent stream-K kernel (decode path); items straddle CTAs
-    (4, 2, 64, [1, 5, 16, 17, 100], 0),
-    (32, 8, 128, [2048, 7, 300, 1, 4100], 0),
-    (32, 32, 128, [2048] * 9, 0),
+    # up to 16 split-KV slices (runtime.cu kAttnMaxSplits) over long and 1-token rows
+    (4, 2, 64, [1, 5, 16, 17, 100], 2),
+    (32, 8, 128, [2048, 7, 300, 1, 4100], 16),
+    (32, 32, 128, [2048] * 9, 8),
+    (32, 32, 128, [4100], 16),
     # MHA hd 128: warp-per-block consumer, long rows (many ring wraps)
     (32, 32, 128, [2048, 1, 1500, 17, 4096], 1),
-    (8, 1, 128, [64, 129, 16, 17], 0)])
+    (8, 1, 128, [64, 129, 16, 17], 3)])
 def test_paged_attention(H, KVH, hd, ctxs, splits):
     N = _native()
     L, layer = 3, 1
