@@ -36,46 +36,10 @@ def tiny_config(trace_path, seq_path, static_blocks=40):
     }
 
 
-@pytest.fixture(scope="module")
-def setup(tmp_path_factory):
+def _replay_on_oracle(cfg, dev, calls, min_checked=300):
+    """Replays every recorded device launch on the CPU oracle with the same
+    per-layer precision; every generated token must match (near ties allowed)."""
     from paper_2506_02006_b200 import morphsim as M
-    from paper_2506_02006_b200.device import DeviceModel, layer_pages
-    assert layer_pages(TINY, 16) == 48 and layer_pages(TINY, 4) == 16
-    d = tmp_path_factory.mktemp("eng")
-    trace = d / "trace.csv"
-    trace.write_text("".join(f"{i * 3},{40 + (i % 3) * 8},{24 + (i % 4) * 4}\n" for i in range(14)) +
-                     "".join(f"{400 + i * 40},{32},{16}\n" for i in range(6)))
-    seq = str(d / "seq.json")
-    M.save_sequence(M.baseline_sequence("back_to_front", 4), seq)
-    cfg = tiny_config(str(trace), seq)
-    dev = DeviceModel(TINY, max_batch=32, max_prefill_tokens=128, max_pos=128, arena_pages=(4 * 48 + 40 + 40) + 32)
-    dev.weights_synthetic(7)
-    yield M, cfg, dev
-    dev.close()
-
-
-def test_device_backed_run_is_bit_exact_and_tokens_match_oracle(setup):
-    M, cfg, dev = setup
-    rep_cpu, log_cpu, tl_cpu = M.run_arm_full(cfg, "morph-performance")
-    rep, log, tl = M.run_arm_full(cfg, "morph-performance", device=dev, record=True)
-    assert log == log_cpu and tl == tl_cpu
-    calls = rep.pop("device_calls")
-    for r in (rep, rep_cpu):
-        r.pop("device")
-    assert rep == rep_cpu
-    assert rep["morph"]["swap_events"] >= 1 and rep["kv"]["peak_capacity_blocks"] > 40
-    assert "KV_ATTACH" in log
-    if O.have_ref_core():
-        ref = O.ref_core()
-        import tempfile
-        with tempfile.TemporaryDirectory() as td:
-            r_ref = json.loads(ref.run_arm(json.dumps(cfg), "morph-performance", td))
-            assert open(os.path.join(td, "events_morph-performance.log")).read() == log
-        rep.pop("fingerprint")
-        r_ref.pop("fingerprint")
-        assert rep == r_ref
-
-    # ---- replay every device launch on the CPU oracle
     from paper_2506_02006_b200 import _core
     from paper_2506_02006_b200.morphsim import resolve_workload
     trace = resolve_workload(M.config_from_json(cfg))
@@ -117,9 +81,53 @@ def test_device_backed_run_is_bit_exact_and_tokens_match_oracle(setup):
                 margin = float(rlog[rtok] - rlog[g])
                 assert margin <= 2e-3 * float(np.max(np.abs(rlog))), (c, r, at, margin)
                 ties.append((r, at, margin))
-    assert checked >= 300
+    assert checked >= min_checked
     assert len(ties) <= 0.02 * checked, ties
     model.close()
+
+
+
+
+@pytest.fixture(scope="module")
+def setup(tmp_path_factory):
+    from paper_2506_02006_b200 import morphsim as M
+    from paper_2506_02006_b200.device import DeviceModel, layer_pages
+    assert layer_pages(TINY, 16) == 48 and layer_pages(TINY, 4) == 16
+    d = tmp_path_factory.mktemp("eng")
+    trace = d / "trace.csv"
+    trace.write_text("".join(f"{i * 3},{40 + (i % 3) * 8},{24 + (i % 4) * 4}\n" for i in range(14)) +
+                     "".join(f"{400 + i * 40},{32},{16}\n" for i in range(6)))
+    seq = str(d / "seq.json")
+    M.save_sequence(M.baseline_sequence("back_to_front", 4), seq)
+    cfg = tiny_config(str(trace), seq)
+    dev = DeviceModel(TINY, max_batch=32, max_prefill_tokens=128, max_pos=128, arena_pages=(4 * 48 + 40 + 40) + 32)
+    dev.weights_synthetic(7)
+    yield M, cfg, dev
+    dev.close()
+
+
+def test_device_backed_run_is_bit_exact_and_tokens_match_oracle(setup):
+    M, cfg, dev = setup
+    rep_cpu, log_cpu, tl_cpu = M.run_arm_full(cfg, "morph-performance")
+    rep, log, tl = M.run_arm_full(cfg, "morph-performance", device=dev, record=True)
+    assert log == log_cpu and tl == tl_cpu
+    calls = rep.pop("device_calls")
+    for r in (rep, rep_cpu):
+        r.pop("device")
+    assert rep == rep_cpu
+    assert rep["morph"]["swap_events"] >= 1 and rep["kv"]["peak_capacity_blocks"] > 40
+    assert "KV_ATTACH" in log
+    if O.have_ref_core():
+        ref = O.ref_core()
+        import tempfile
+        with tempfile.TemporaryDirectory() as td:
+            r_ref = json.loads(ref.run_arm(json.dumps(cfg), "morph-performance", td))
+            assert open(os.path.join(td, "events_morph-performance.log")).read() == log
+        rep.pop("fingerprint")
+        r_ref.pop("fingerprint")
+        assert rep == r_ref
+
+    _replay_on_oracle(cfg, dev, calls)
 
 
 def test_device_clock_run_measures_real_time(setup):
@@ -130,3 +138,73 @@ def test_device_clock_run_measures_real_time(setup):
     assert d["decode_steps"] > 0 and d["decode_ms"] > 0 and d["prefill_ms"] > 0
     # durations in the log are the measured GPU times, not the cost model's
     assert rep["ttft_ms"]["p95"] is not None
+
+
+def test_wall_clock_run_overlaps_swaps_and_matches_oracle(setup):
+    """ClockMode::kWall: arrivals released on the wall clock, swaps polled at
+    event boundaries (never waited on), every generated token still what the
+    oracle predicts for the precision each launch ran at."""
+    M, cfg, dev = setup
+    rep, log, _ = M.run_arm_full(cfg, "morph-performance", device=dev, clock="wall", record=True)
+    calls = rep.pop("device_calls")
+    assert rep["requests"]["completed"] == rep["requests"]["total"]
+    d = rep["device"]
+    assert d["decode_steps"] > 0 and d["host_gap_ms"] >= 0.0 and d["exposed_stall_ms_per_token"] >= 0.0
+    if rep["morph"]["swap_events"]:
+        assert "done_at=poll" in log and "SWAP_DONE" in log
+    # wall-clock TTFT includes the (real) arrival spacing: the last arrival is at 600 ms
+    assert rep["sim_end_ms"] >= 600.0
+    _replay_on_oracle(cfg, dev, calls, min_checked=200)
+
+
+def test_swap_commit_keeps_captured_graphs():
+    """Page tables are read from device memory: a swap commit does not drop the
+    captured decode graphs; returning to a precision vector already captured
+    replays its graph (no new capture) and still matches the oracle."""
+    from paper_2506_02006_b200.device import DeviceModel
+    dev = DeviceModel(TINY, max_batch=4, max_prefill_tokens=64, max_pos=128, arena_pages=300)
+    ref = O.RefModel(dict(TINY, max_pos=128), 7)
+    try:
+        dev.weights_synthetic(7)
+        dev.hist_reserve(2, 128)
+        dev.kv_attach(0, 16)
+        table = np.arange(16, dtype=np.int64).reshape(2, 8)
+        prompts = (np.arange(2 * 16, dtype=np.int32).reshape(2, 16) * 53) % TINY["V"]
+        seqs = [ref.new_seq(128) for _ in range(2)]
+        toks = []
+        for b in range(2):
+            dev.hist_write(b, 0, prompts[b])
+            toks.append(dev.prefill(b, 16, table[b])[0])
+            ref.prefill(seqs[b], prompts[b])
+        toks = np.array(toks, np.int32)
+        pos = np.full(2, 16, np.int32)
+
+        def steps(k):
+            nonlocal toks, pos
+            for _ in range(k):
+                got, lg = dev.decode(np.arange(2), pos, table, tokens=toks, want_logits=True)
+                rt, rl = ref.forward(seqs, toks)
+                for b in range(2):
+                    assert np.max(np.abs(lg[b] - rl[b])) <= 2e-2 * np.max(np.abs(rl[b]))
+                toks = rt.astype(np.int32)
+                pos = pos + 1
+
+        def swap(layer, bits):
+            t = dev.swap_begin(layer, bits)
+            dev.swap_wait(t)
+            dev.swap_commit(t)
+            ref.set_precision(layer, bits)
+
+        # a step shape is captured on its second sighting per staging slot (ring of 3)
+        steps(6)
+        c0 = dev.lib.ms_graph_captures(dev.h)
+        swap(0, 4)
+        steps(6)
+        c1 = dev.lib.ms_graph_captures(dev.h)
+        swap(0, 16)
+        steps(6)
+        c2 = dev.lib.ms_graph_captures(dev.h)
+        assert c1 > c0 and c2 == c1, (c0, c1, c2)
+    finally:
+        ref.close()
+        dev.close()
