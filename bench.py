@@ -170,15 +170,24 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- GPU arm
-def build_model(local_rank: int, extra_steps: int):
-    from paper_2506_02006_b200.device import DeviceModel, layer_pages
+def dist_barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def build_model(local_rank: int, world: int, extra_steps: int):
+    from paper_2506_02006_b200.device import layer_pages
+    from paper_2506_02006_b200.replicas import replica_device
     blocks_per_seq = (CTX + extra_steps + 16) // 16 + 1
     kv_pages = BATCH * blocks_per_seq
     w_pages = SHAPE["L"] * layer_pages(SHAPE, 16)
     staging = len(W4_LAYERS) * layer_pages(SHAPE, 4) + 64
-    dev = DeviceModel(SHAPE, device=local_rank, max_batch=128, max_prefill_tokens=1024,
-                      max_pos=CTX + extra_steps + 32, arena_pages=kv_pages + w_pages + staging)
-    dev.weights_synthetic(7)
+    # N > 1: one box-wide host copy of the variant store
+    dev, store = replica_device(SHAPE, local_rank=local_rank, world=world, barrier=lambda: dist_barrier(world),
+                                key="7b", max_batch=128, max_prefill_tokens=1024, max_pos=CTX + extra_steps + 32,
+                                arena_pages=kv_pages + w_pages + staging)
+    dev.variant_store = store
     dev.hist_reserve(BATCH, CTX + extra_steps + 33)
     dev.kv_attach(0, kv_pages)
     table = np.arange(kv_pages, dtype=np.int64).reshape(BATCH, blocks_per_seq)
@@ -204,13 +213,18 @@ def dev_layer_pages(bits):
 
 
 def serve_arms(dev, wl, arms_csv, rank, world, note, budget_gib=24.0, wl_key="gamma"):
-    """Each arm of one bursty trace through the C++ engine on `dev` (GPU clock)."""
+    """Each arm of one bursty trace through the C++ engine on `dev`, on the
+    wall clock (arrivals released on time, swaps overlapping decode).  N > 1:
+    ONE trace (the per-GPU rate x N), request i served by replica i mod N."""
+    from paper_2506_02006_b200 import morphsim as M
     from paper_2506_02006_b200 import serving as S
-    from paper_2506_02006_b200.replicas import merge_reports
+    from paper_2506_02006_b200.replicas import merge_reports, shard_trace
     cfg = S.device_config(dev, wl, budget_gib=budget_gib, reserve_gib=4.0)
+    trace = shard_trace(M.resolve_workload(M.config_from_json(cfg)), rank, world) if world > 1 else None
     out = None
     for arm in [a for a in arms_csv.split(",") if a]:
-        rep, _ = S.serve(dev, cfg, arm, clock="device")
+        dist_barrier(world)
+        rep, _ = S.serve(dev, cfg, arm, clock="wall", trace=trace)
         summ = S.summary(rep)
         if world > 1:
             import torch.distributed as dist
@@ -228,20 +242,26 @@ def serve_8b(args, local_rank, rank, world):
     """BASELINE configs[2]: Llama-3-8B shape (GQA 32/8), Gamma-burst trace (CV 2),
     prompt 1024 / output 512, controller performance defaults
     (swap up to L/2 layers + KV resize under memory pressure), 24 GiB budget."""
-    from paper_2506_02006_b200.device import LLAMA3_8B, DeviceModel, layer_pages, page_bytes
+    from paper_2506_02006_b200.device import LLAMA3_8B, layer_pages, page_bytes
+    from paper_2506_02006_b200.replicas import replica_device
     shape = dict(LLAMA3_8B)
     pb = page_bytes(shape)
     budget_pages = int(24.0 * (1 << 30)) // pb
-    dev = DeviceModel(shape, device=local_rank, max_batch=128, max_prefill_tokens=2048, max_pos=1024 + 512 + 32,
-                      arena_pages=budget_pages + 2 * layer_pages(shape, 16) + 64)
+    dev, store = replica_device(shape, local_rank=local_rank, world=world, barrier=lambda: dist_barrier(world),
+                                key="8b", max_batch=128, max_prefill_tokens=2048, max_pos=1024 + 512 + 32,
+                                arena_pages=budget_pages + 2 * layer_pages(shape, 16) + 64)
     try:
-        dev.weights_synthetic(7)
-        wl = {"gamma": {"seed": 101 + rank, "rps": args.serve8b_rps, "shape": 0.25,
+        # one trace for the whole box: the per-GPU rate x N, sharded round-robin
+        wl = {"gamma": {"seed": 101, "rps": args.serve8b_rps * world, "shape": 0.25,
                         "total_ms": int(args.serve8b_seconds * 1000), "prompt_tokens": 1024, "output_tokens": 512}}
         return serve_arms(dev, wl, args.serve_arms, rank, world,
-                          "Llama-3-8B shape (BASELINE configs[2]), 24 GiB device budget, measured-GPU-clock engine run")
+                          "Llama-3-8B shape (BASELINE configs[2]), 24 GiB device budget, wall-clock engine run"
+                          + (f", one trace sharded round-robin over {world} replicas" if world > 1 else ""))
     finally:
         dev.close()
+        dist_barrier(world)
+        if store is not None and local_rank == 0:
+            store.unlink()
 
 
 def serve_13b(args, local_rank, rank, world):
@@ -332,7 +352,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     total_steps = (2 * (args.warmup + args.steps) + args.steps + 6 * max(4, args.steps // 2) + args.e2e_steps +
                    max(args.warmup, 8) + 8)
-    dev, table = build_model(local_rank, total_steps)
+    dev, table = build_model(local_rank, world, total_steps)
     slots = np.arange(BATCH, dtype=np.int32)
     pos = np.full(BATCH, CTX - 1, dtype=np.int32)
 
@@ -467,17 +487,24 @@ def run_ours(args):
         tokens = dev.decode_collect()
         inflight -= 1
     e2e_s = max_over_ranks(time.perf_counter() - t0)
+    gpus_active = world
+    if world > 1:  # ranks that completed the timed loops
+        import torch.distributed as dist
+        t = torch.tensor([1.0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        gpus_active = int(t.item())
     max_blocks = dev.max_blocks
     h2d = BATCH * (4 + max_blocks) * 4  # staged per step: slot, pos, ctx, token + block-table row per sequence
     d2h = BATCH * 4
     # ---- serving: bursty Gamma trace through the engine, measured GPU clock
     serving = None
     if args.serve_seconds > 0:
-        wl = {"gamma": {"seed": 101 + rank, "rps": args.serve_rps, "shape": 0.25,
+        wl = {"gamma": {"seed": 101, "rps": args.serve_rps * world, "shape": 0.25,
                         "total_ms": int(args.serve_seconds * 1000), "prompt_tokens": 512, "output_tokens": 256}}
         serving = serve_arms(dev, wl, args.serve_arms, rank, world,
                              "Llama-2-7B shape under a 24 GiB device budget (the paper's L4-class memory pressure), "
-                             "measured-GPU-clock engine run")
+                             "wall-clock engine run" +
+                             (f", one trace sharded round-robin over {world} replicas" if world > 1 else ""))
         # the controller and swaps change the layer table: restore the benchmark state
         dev.lib.ms_reset_state(dev.h)
     hbm, peak_kind = peaks()
@@ -488,6 +515,7 @@ def run_ours(args):
         "value": BATCH * args.steps * world / (ms * 1e-3),
         "unit": "tok/s",
         "n_gpus": world,
+        "gpus_active": gpus_active,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
@@ -524,6 +552,9 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     dev.close()
+    dist_barrier(world)
+    if dev.variant_store is not None and local_rank == 0:
+        dev.variant_store.unlink()
     if args.serve8b_seconds > 0:
         line["serving_8b"] = serve_8b(args, local_rank, rank, world)
     # the Llama-2-13B legs (BASELINE configs[3]) are single-GPU workloads; at
@@ -539,6 +570,20 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` run directly (no torchrun around it): launch N
+    ranks of this same command, one process per GPU on this node, and return
+    the launcher's exit code (rank 0 prints the JSON line)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -560,7 +605,15 @@ def main():
     ap.add_argument("--prefill-reps", type=int, default=3)
     ap.add_argument("--serve13b-rps", type=float, default=16.0,
                     help="Llama-2-13B 8k-prompt burst: Poisson arrivals at this rate for 1 s, BASELINE configs[3] (0 = skip)")
+    ap.add_argument("--ranks-probe", action="store_true",
+                    help="(launcher test) every rank prints its rank / world size and exits")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.ranks_probe:
+        rank, local_rank, world = dist_env()
+        print(json.dumps({"rank": rank, "local_rank": local_rank, "world": world}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -73,6 +73,16 @@ int ms_weights_synthetic(ms_ctx* ctx, uint64_t seed);
  * 5 down).  After all tensors: ms_weights_finalize(). */
 int ms_weights_upload(ms_ctx* ctx, int layer, int which, const uint16_t* host_bf16, int64_t count);
 int ms_weights_finalize(ms_ctx* ctx);
+/* Registers caller-owned host memory as the variant-store image of one layer at
+ * `bits` (SURVEY 8(b) ms_variant_register; the LayerSwapper uploads from it).
+ * Must precede ms_weights_synthetic / ms_weights_finalize.  The memory is
+ * page-locked here (cudaHostRegister, portable) unless already pinned and must
+ * outlive the context.  prefilled = 1: it already holds the packed image
+ * (ms_variant_bytes(bits) bytes, e.g. built by another replica process over
+ * shared memory, or by an offline packer) and finalize skips building it;
+ * prefilled = 0: finalize packs the image into it.  One host copy of every
+ * variant can thus serve all replica contexts of a box. */
+int ms_variant_register(ms_ctx* ctx, int layer, int bits, void* host, int64_t bytes, int prefilled);
 /* Copies one layer's packed variant image (from the pinned store) for inspection. */
 int64_t ms_variant_bytes(ms_ctx* ctx, int bits);
 int ms_variant_export(ms_ctx* ctx, int layer, int bits, void* host_out, int64_t bytes);
@@ -176,7 +186,7 @@ int ms_timer_stop(ms_ctx* ctx, float* ms);
 enum {
   MS_PK_EMBED = 0, MS_PK_GEMM_QKV, MS_PK_GEMM_QKV_W4, MS_PK_QKV_POST, MS_PK_ATTN, MS_PK_GEMM_O, MS_PK_GEMM_O_W4,
   MS_PK_NORM, MS_PK_GEMM_GU, MS_PK_GEMM_GU_W4, MS_PK_SILU, MS_PK_GEMM_DOWN, MS_PK_GEMM_DOWN_W4, MS_PK_LM_HEAD,
-  MS_PK_ARGMAX, MS_PK_COUNT
+  MS_PK_ARGMAX, MS_PK_LAYER, MS_PK_LAYER_W4, MS_PK_COUNT
 };
 int ms_prof_kernels(ms_ctx* ctx, int enable);
 int ms_prof_kernels_read(ms_ctx* ctx, float* ms_out, int64_t* launches_out);

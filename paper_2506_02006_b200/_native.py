@@ -61,6 +61,7 @@ SIGNATURES = [
     ("ms_weights_finalize", C.c_int, [_P]),
     ("ms_variant_bytes", C.c_int64, [_P, C.c_int]),
     ("ms_variant_export", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64]),
+    ("ms_variant_register", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64, C.c_int]),
     ("ms_swap_begin", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     ("ms_swap_poll", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int)]),
     ("ms_swap_wait", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_float)]),

@@ -94,6 +94,14 @@ class DeviceModel:
     def finalize(self):
         N.check(self.lib.ms_weights_finalize(self.h))
 
+    def variant_bytes(self, bits: int) -> int:
+        return int(self.lib.ms_variant_bytes(self.h, bits))
+
+    def variant_register(self, layer: int, bits: int, addr: int, nbytes: int, prefilled: bool):
+        """Use caller-owned host memory at `addr` as the layer's variant image
+        (ms_variant_register); before weights_synthetic / finalize."""
+        N.check(self.lib.ms_variant_register(self.h, layer, bits, C.c_void_p(addr), nbytes, int(prefilled)))
+
     def variant_image(self, layer: int, bits: int) -> np.ndarray:
         n = self.lib.ms_variant_bytes(self.h, bits)
         out = np.empty(n, np.uint8)
@@ -227,7 +235,8 @@ class DeviceModel:
         return ms.value
 
     PK_NAMES = ["embed", "gemm_qkv", "gemm_qkv_w4", "qkv_post", "attn", "gemm_o", "gemm_o_w4", "norm", "gemm_gu",
-                "gemm_gu_w4", "silu", "gemm_down", "gemm_down_w4", "lm_head", "argmax"]
+                "gemm_gu_w4", "silu", "gemm_down", "gemm_down_w4", "lm_head", "argmax", "layer_fused",
+                "layer_fused_w4"]
 
     def prof_kernels(self, enable: bool):
         N.check(self.lib.ms_prof_kernels(self.h, int(enable)))

@@ -401,9 +401,10 @@ def arm_spec(cfg: dict, arm: str) -> dict:
     raise ValueError(f"unknown arm: {arm}")
 
 
-def _run(cfg: dict, arm: str, device=None, clock: str = "virtual", record: bool = False):
+def _run(cfg: dict, arm: str, device=None, clock: str = "virtual", record: bool = False, trace=None):
     spec = arm_spec(cfg, arm)
-    trace = resolve_workload(cfg)
+    if trace is None:
+        trace = resolve_workload(cfg)
     dev_ptr, vocab = 0, 0
     if device is not None:
         dev_ptr = device.h.value if hasattr(device.h, "value") else int(device.h)
@@ -421,7 +422,9 @@ def run_arm(config, arm: str, out_dir: str = "", device=None, clock: str = "virt
 
     device: a ``paper_2506_02006_b200.device.DeviceModel`` -- every step runs on
     the GPU.  clock: "virtual" (reference cost model durations, bit-exact event
-    log) or "device" (measured GPU durations: real TTFT / TPOT).
+    log), "device" (measured GPU durations advance a simulated clock) or
+    "wall" (real clock: arrivals released on time, swaps polled at event
+    boundaries while decode continues).
     """
     cfg = _resolved(config)
     report, log, timeline = _run(cfg, arm, device, clock)
@@ -436,11 +439,14 @@ def run_arm(config, arm: str, out_dir: str = "", device=None, clock: str = "virt
     return report
 
 
-def run_arm_full(config, arm: str, device=None, clock: str = "virtual", record: bool = False):
+def run_arm_full(config, arm: str, device=None, clock: str = "virtual", record: bool = False, trace=None):
     """(report, event_log_text, timeline_csv) -- for parity checks; record=True
     adds report["device_calls"] (every prefill/decode launch with its rows and
-    the per-layer precision at launch) for replay against the CPU oracle."""
-    return _run(_resolved(config), arm, device, clock, record)
+    the per-layer precision at launch) for replay against the CPU oracle.
+    trace: serve this Trace instead of the config's workload (e.g. one
+    replica's round-robin shard, replicas.shard_trace).  clock: "virtual",
+    "device" (GPU-time simulation) or "wall" (real clock, swaps overlapped)."""
+    return _run(_resolved(config), arm, device, clock, record, trace)
 
 
 def sweep(config, rps_list, arms) -> dict:

@@ -49,9 +49,10 @@ def device_config(dev: DeviceModel, workload: dict, *, budget_gib: float = 24.0,
     return cfg
 
 
-def serve(dev: DeviceModel, cfg: dict, arm: str = "morph-performance", clock: str = "device"):
-    """Runs one arm on the GPU; returns (report, event_log)."""
-    rep, log, _ = M.run_arm_full(cfg, arm, device=dev, clock=clock)
+def serve(dev: DeviceModel, cfg: dict, arm: str = "morph-performance", clock: str = "wall", trace=None):
+    """Runs one arm on the GPU (real clock by default); returns (report, event_log).
+    trace: this replica's shard of the workload (replicas.shard_trace)."""
+    rep, log, _ = M.run_arm_full(cfg, arm, device=dev, clock=clock, trace=trace)
     return rep, log
 
 
@@ -72,4 +73,10 @@ def summary(rep: dict) -> dict:
         "prefill_ms_total": d.get("prefill_ms"),
         "device_busy_ms": d.get("busy_ms"), "decode_steps": d.get("decode_steps"),
         "swap_upload_ms_total": d.get("swap_upload_ms"),
+        "decode_steps_overlapping_uploads": d.get("decode_steps_overlap"),
+        "exposed_swap_stall_ms_per_token": d.get("exposed_stall_ms_per_token"),
+        # step time above the no-upload step model, as a fraction of all decode time
+        "exposed_swap_stall_frac_of_decode": (d["exposed_swap_stall_ms"] / d["decode_ms"]
+                                              if d.get("decode_ms") else None),
+        "host_gap_ms": d.get("host_gap_ms"), "graph_captures": d.get("graph_captures"),
     }
