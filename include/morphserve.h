@@ -186,7 +186,7 @@ int ms_timer_stop(ms_ctx* ctx, float* ms);
 enum {
   MS_PK_EMBED = 0, MS_PK_GEMM_QKV, MS_PK_GEMM_QKV_W4, MS_PK_QKV_POST, MS_PK_ATTN, MS_PK_GEMM_O, MS_PK_GEMM_O_W4,
   MS_PK_NORM, MS_PK_GEMM_GU, MS_PK_GEMM_GU_W4, MS_PK_SILU, MS_PK_GEMM_DOWN, MS_PK_GEMM_DOWN_W4, MS_PK_LM_HEAD,
-  MS_PK_ARGMAX, MS_PK_LAYER, MS_PK_LAYER_W4, MS_PK_COUNT
+  MS_PK_ARGMAX, MS_PK_COUNT
 };
 int ms_prof_kernels(ms_ctx* ctx, int enable);
 int ms_prof_kernels_read(ms_ctx* ctx, float* ms_out, int64_t* launches_out);

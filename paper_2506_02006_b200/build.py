@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
            "-I" + os.path.join(ROOT, "include")]
 NVFLAGS += os.environ.get("MS_NVCC_EXTRA", "").split()  # experiments only
-CU_SOURCES = ["gemm.cu", "layer.cu", "attention.cu", "prefill_attention.cu", "prefill_attention_tc.cu", "elementwise.cu",
+CU_SOURCES = ["gemm.cu", "attention.cu", "prefill_attention.cu", "prefill_attention_tc.cu", "elementwise.cu",
               "runtime.cu"]
 
 

@@ -1,7 +1,6 @@
-// gemm_common.cuh -- pieces shared by the tcgen05 GEMM kernels (gemm.cu) and
-// the fused decode-layer kernel (layer.cu): packed-chunk sizes, the weight
-// chunk cursor over a variant image's page table, the stream-K / whole-tile
-// segment walker, and the int4 -> bf16 magic.
+// gemm_common.cuh -- pieces of the tcgen05 GEMM kernels (gemm.cu): packed-chunk
+// sizes, the weight chunk cursor over a variant image's page table, the
+// stream-K / whole-tile segment walker, and the int4 -> bf16 magic.
 #pragma once
 #include <cstdint>
 

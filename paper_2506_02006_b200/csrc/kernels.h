@@ -91,26 +91,6 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
 cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                         float* out, cudaStream_t stream);
 
-// Fused decode layer (layer.cu): O GEMM -> residual+RMSNorm -> gate_up GEMM ->
-// SiLU*up -> down GEMM -> residual+RMSNorm as one persistent kernel with grid
-// barriers (decode steps, M <= TM <= 256, stream-K plans).
-struct DecodeLayerArgs {
-  GemmWeights w[3];           // O, gate_up, down of the layer (device page tables)
-  GemmPlanDev plan[3];
-  uint16_t* x;                // packed activations: phase inputs, rewritten by the row phases
-  float* part;                // fp32 partial slots
-  float* h;                   // residual stream [M][d]
-  const uint16_t* norm2;      // this layer's post-attention RMSNorm weight
-  const uint16_t* norm_next;  // the next layer's input RMSNorm weight (or the final norm)
-  float eps;
-  int M, TM, d, ffn;
-  int tm_out, row_begin;      // packing of the last row phase (final layer: lm_head rows)
-  uint32_t* bar;              // [grid] grid-barrier arrival counters (zero at context creation)
-  unsigned long long* tl;     // (debug, MS_LAYER_TL) [grid][8 events][3 phases] globaltimer stamps, or null
-};
-bool decode_layer_ok(const DecodeLayerArgs& a, bool w4);
-cudaError_t decode_layer_launch(const DecodeLayerArgs& a, bool w4, int grid, cudaStream_t s);
-
 // Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
 // every layer): [layer][kv_head][K|V][token][head_dim] bf16.
 struct KvGeom {

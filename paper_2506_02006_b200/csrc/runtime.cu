@@ -198,7 +198,6 @@ struct ms_ctx {
   float* q = nullptr;
   float* attn_ws = nullptr;
   size_t attn_ws_elems = 0;
-  uint32_t* layer_bar = nullptr;         // fused decode layer: per-CTA grid-barrier counters
   unsigned long long* am_key = nullptr;  // wide argmax: per-row best key (self-resetting)
   int* am_cnt = nullptr;                 // wide argmax: per-row arrival counter (self-resetting)
   std::vector<int> submitted;  // ring slots of submitted decode steps, oldest first
@@ -525,81 +524,6 @@ int attn_splits(ms_ctx* c, int rows, int max_ctx) {
   return s;
 }
 
-// Decode steps run everything of a layer after its attention as one fused
-// persistent kernel (layer.cu); MS_FUSED_LAYER=0 selects the six-launch path
-// (A/B measurements; prefills always use it).
-bool fused_layer_enabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("MS_FUSED_LAYER");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
-bool fused_layer(ms_ctx* c, int l, bool w4, int M, int TM, const uint16_t* n2, const uint16_t* nw, int tm_out,
-                 int row_begin) {
-  const ms_model_desc& D = c->desc;
-  ms::DecodeLayerArgs a{};
-  for (int p = 0; p < 3; ++p) {
-    a.w[p] = mat_weights(c, l, p + 1);
-    a.plan[p] = ms::gemm_plan(a.w[p].N, a.w[p].K, M, TM, w4, c->num_sms, c->part_elems);
-    if ((size_t)a.plan[p].slots * M * a.w[p].N > c->part_elems) return false;
-  }
-  a.x = c->x;
-  a.part = c->part;
-  a.h = c->h;
-  a.norm2 = n2;
-  a.norm_next = nw;
-  a.eps = D.rms_eps;
-  a.M = M;
-  a.TM = TM;
-  a.d = D.hidden;
-  a.ffn = D.ffn;
-  a.tm_out = tm_out;
-  a.row_begin = row_begin;
-  a.bar = c->layer_bar;
-  if (!ms::decode_layer_ok(a, w4)) return false;
-  // (debug) MS_LAYER_TL=<layer>: per-CTA timeline of that layer's fused kernel,
-  // printed after the launch (eager launches only: run with MS_GRAPH=0)
-  static const int tl_layer = [] {
-    const char* e = std::getenv("MS_LAYER_TL");
-    return e ? std::atoi(e) : -1;
-  }();
-  static unsigned long long* tl = nullptr;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  CK(cudaStreamIsCapturing(c->compute, &cs));
-  const bool want_tl = tl_layer == l && cs == cudaStreamCaptureStatusNone;
-  if (want_tl) {
-    if (!tl) CK(cudaMalloc(&tl, (size_t)c->num_sms * 24 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(tl, 0, (size_t)c->num_sms * 24 * sizeof(unsigned long long), c->compute));
-    a.tl = tl;
-  }
-  CK(ms::decode_layer_launch(a, w4, c->num_sms, c->compute));
-  c->launches += 1;
-  if (want_tl) {
-    std::vector<unsigned long long> h((size_t)c->num_sms * 24);
-    CK(cudaMemcpyAsync(h.data(), tl, h.size() * 8, cudaMemcpyDeviceToHost, c->compute));
-    CK(cudaStreamSynchronize(c->compute));
-    unsigned long long t0 = ~0ull;
-    for (int i = 0; i < c->num_sms; ++i) t0 = std::min(t0, h[(size_t)i * 24 + 6 * 3]);
-    static const char* names[8] = {"epi_last_tile", "epi_bar_pass", "rows_done", "b_go", "mma_first", "w_first",
-                                   "start", "end"};
-    for (int e = 0; e < 8; ++e)
-      for (int p = 0; p < ((e >= 6) ? 1 : 3); ++p) {
-        std::vector<double> v;
-        for (int i = 0; i < c->num_sms; ++i) {
-          const unsigned long long x = h[((size_t)i * 8 + e) * 3 + p];
-          if (x) v.push_back((double)(x - t0) / 1e3);
-        }
-        if (v.empty()) continue;
-        std::sort(v.begin(), v.end());
-        fprintf(stderr, "layer %d %s w4=%d %-14s p%d  n=%3zu  min %7.2f  med %7.2f  max %7.2f us\n", l,
-                w4 ? "W4" : "BF16", (int)w4, names[e], p, v.size(), v.front(), v[v.size() / 2], v.back());
-      }
-  }
-  return true;
-}
-
 // The decoder over M rows whose per-row metadata already sits in device memory.
 void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_pos, const int32_t* d_ctx,
              const int32_t* d_tokens, const int32_t* d_pages, const int32_t* d_page_row, int page_stride,
@@ -677,10 +601,6 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
     const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
     const int row_begin = last ? final_row_begin : 0;
-    if (d_page_row == nullptr && fused_layer_enabled() && fused_layer(c, l, w4, M, TM, n2, nw, tm_out, row_begin)) {
-      pk_mark(c, w4 ? MS_PK_LAYER_W4 : MS_PK_LAYER);
-      continue;
-    }
     s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_O_W4 : MS_PK_GEMM_O);
     CK(ms::residual_norm_launch(c->part, s, M, d, c->h, n2, D.rms_eps, c->x, TM, c->compute));
@@ -839,8 +759,6 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       CK(cudaMalloc(&c->q, (size_t)c->max_rows * H * hd * sizeof(float)));
       c->attn_ws_elems = (size_t)16 * desc->max_batch * H * (hd + 2);
       CK(cudaMalloc(&c->attn_ws, c->attn_ws_elems * sizeof(float)));
-      CK(cudaMalloc(&c->layer_bar, (size_t)c->num_sms * 32 * sizeof(uint32_t)));  // one 128-B line per CTA
-      CK(cudaMemset(c->layer_bar, 0, (size_t)c->num_sms * 32 * sizeof(uint32_t)));
       CK(cudaMalloc(&c->am_key, (size_t)c->max_rows * sizeof(unsigned long long)));
       CK(cudaMemset(c->am_key, 0, (size_t)c->max_rows * sizeof(unsigned long long)));
       CK(cudaMalloc(&c->am_cnt, (size_t)c->max_rows * sizeof(int)));
@@ -916,7 +834,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
-                 c->h, c->x, c->part, c->q, c->attn_ws, c->layer_bar, c->am_key, c->am_cnt, c->next, c->logits, c->hist};
+                 c->h, c->x, c->part, c->q, c->attn_ws, c->am_key, c->am_cnt, c->next, c->logits, c->hist};
   for (void* p : dev) cudaFree(p);
   cudaFreeHost(c->h_next);
   cudaFreeHost(c->h_logits);

@@ -235,8 +235,7 @@ class DeviceModel:
         return ms.value
 
     PK_NAMES = ["embed", "gemm_qkv", "gemm_qkv_w4", "qkv_post", "attn", "gemm_o", "gemm_o_w4", "norm", "gemm_gu",
-                "gemm_gu_w4", "silu", "gemm_down", "gemm_down_w4", "lm_head", "argmax", "layer_fused",
-                "layer_fused_w4"]
+                "gemm_gu_w4", "silu", "gemm_down", "gemm_down_w4", "lm_head", "argmax"]
 
     def prof_kernels(self, enable: bool):
         N.check(self.lib.ms_prof_kernels(self.h, int(enable)))
