@@ -1536,15 +1536,15 @@ int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_pa
   return guard([&] {
     if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "gemm: bits must be 16 or 4");
     if (N % 128 || K % 128 || M < 1 || TM % 16 || TM < 16 || TM > 256) fail(MS_EVALIDATION, "gemm: bad shape");
-    // one-entry page table per contiguous packed matrix (up to 64 distinct
+    // one-entry page table per contiguous packed matrix (up to 1024 distinct
     // matrices; written once, so later calls may be graph-captured)
     static thread_local uint64_t* tables = nullptr;
     static thread_local std::vector<uint64_t> known;
-    if (!tables) CK(cudaMalloc(&tables, 64 * sizeof(uint64_t)));
+    if (!tables) CK(cudaMalloc(&tables, 1024 * sizeof(uint64_t)));
     const uint64_t addr = (uint64_t)w_packed;
     size_t idx = std::find(known.begin(), known.end(), addr) - known.begin();
     if (idx == known.size()) {
-      if (known.size() == 64) fail(MS_EVALIDATION, "gemm: more than 64 distinct weight matrices");
+      if (known.size() == 1024) fail(MS_EVALIDATION, "gemm: more than 1024 distinct weight matrices");
       CK(cudaMemcpyAsync(tables + idx, &addr, sizeof(addr), cudaMemcpyHostToDevice, (cudaStream_t)stream));
       CK(cudaStreamSynchronize((cudaStream_t)stream));
       known.push_back(addr);

@@ -14,7 +14,6 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2506_02006_b200 import _native as N  # noqa: E402
@@ -77,21 +76,6 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
     ms = time_it(run, iters=4 * len(copies) if len(copies) > 12 else 48, warm=len(copies) + 2)
     total = wbytes + M * K * 2 + M * Nn * 4
     tflops = 2.0 * M * Nn * K / (ms * 1e-3) / 1e12
-    if int(os.environ.get("MS_GEMM_DEBUG", "0")) & 8:
-        torch.cuda.synchronize()
-        tl = out[150 * M * Nn:150 * M * Nn + 2 * 8 * 64].view(torch.int64).view(8, 64).cpu().numpy()
-        t0 = tl[6, 0]
-        names = ["raw_issue", "grp_rfull", "grp_aempty", "grp_afull", "mma_go", "b_issue", "start/end", "mma_issued"]
-        for e in range(8):
-            v = [(x - t0) / 1000 if x > 0 and x - t0 < 10**7 else None for x in tl[e]]
-            print(f"{names[e]:10s}", " ".join(f"{x:5.2f}" if x is not None else "  -  " for x in v[:24]))
-        iss, rf = tl[0].astype(float), tl[1].astype(float)
-        n = int(np.sum(rf > 0))
-        lat = [(rf[i] - iss[i]) / 1000 for i in range(n) if iss[i] > 0]
-        gaps = [(rf[i + 1] - rf[i]) / 1000 for i in range(n - 1)]
-        print("chunks", n, "issue->full latency us: first", [round(x, 2) for x in lat[:4]], "mean(after 16)",
-              round(float(np.mean(lat[16:])), 2) if len(lat) > 16 else None,
-              "full->full gap mean(after 16)", round(float(np.mean(gaps[16:])), 3) if len(gaps) > 16 else None)
     return {"bits": bits, "N": Nn, "K": K, "M": M, "us": ms * 1e3, "GBps": total / ms / 1e6, "TFLOPs": tflops,
             "slots": used.value, "copies": len(copies)}
 
