@@ -500,53 +500,6 @@ cudaError_t quant_w4_launch(const uint16_t* w, int N, int K, uint8_t* out, int8_
   return cudaGetLastError();
 }
 
-// --------------------------------------- W4 image -> BF16 image (long prefills)
-// CTA = one W4 chunk (128 rows x one 128-wide group: 8 KB nibbles + 128 bf16
-// scales) -> the two BF16 chunks (128 rows x 64 k, canonical layout) it covers.
-// Thread = (row, 64-column half); nibble e of word q of slice j is k = 32 j +
-// 8 q + e (quant_w4_kernel's packing).
-__global__ void __launch_bounds__(256) w4_dequant_kernel(GemmWeights w, uint16_t* __restrict__ out) {
-  const int G = w.K / 128, KB = w.K / 64;
-  const int64_t ci = blockIdx.x;
-  const int64_t gc = w.first_chunk + ci;
-  const int64_t p = gc / w.chunks_per_page;
-  const int64_t i = p - w.inl_p0;
-  const uint8_t* page = reinterpret_cast<const uint8_t*>(i >= 0 && i < w.n_inl ? w.inl[i] : w.pages[p]);
-  const uint8_t* chunk = page + (gc - p * w.chunks_per_page) * 8448;
-  const int nt = (int)(ci / G), g = (int)(ci - (int64_t)nt * G);
-  const int row = threadIdx.x & 127, hk = threadIdx.x >> 7;  // hk: k in [64 hk, 64 hk + 64)
-  const float sc = bf2f(*reinterpret_cast<const uint16_t*>(chunk + 8192 + row * 2));
-  uint16_t* dst = out + ((int64_t)nt * KB + 2 * g + hk) * 8192 + ((row >> 3) * 64 + (row & 7)) * 8;
-#pragma unroll
-  for (int jj = 0; jj < 2; ++jj) {
-    const int j = 2 * hk + jj;
-    const uint4 wv = *reinterpret_cast<const uint4*>(chunk + (j * 128 + row) * 16);
-    const uint32_t words[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t o[4];
-#pragma unroll
-      for (int e2 = 0; e2 < 4; ++e2) {
-        float f[2];
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int e = 2 * e2 + b;
-          const int code = (int)((words[q] >> ((e & 1) * 16 + (e >> 1) * 4)) & 0xFu) - 8;
-          f[b] = (float)code * sc;  // exact in fp32; one bf16 rounding below
-        }
-        o[e2] = pack_bf2(f[0], f[1]);
-      }
-      const int c = jj * 4 + q;  // 8-column group within the 64-wide chunk
-      *reinterpret_cast<uint4*>(dst + c * 64) = make_uint4(o[0], o[1], o[2], o[3]);
-    }
-  }
-}
-cudaError_t w4_dequant_launch(const GemmWeights& w, uint16_t* out, cudaStream_t s) {
-  if (w.N % 128 || w.K % 128) return cudaErrorInvalidValue;
-  const int64_t chunks = (int64_t)(w.N / 128) * (w.K / 128);
-  w4_dequant_kernel<<<(unsigned)chunks, 256, 0, s>>>(w, out);
-  return cudaGetLastError();
-}
 
 // ------------------------------------------------ activation packer (tests / e2e)
 __global__ void pack_act_kernel(const uint16_t* __restrict__ x, int M, int K, int TM, uint16_t* __restrict__ out) {

@@ -598,7 +598,9 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
   p.n_tiles = N / 128;
   p.TM = TM;
   // W4: two 128-wide K groups per pipeline unit when K allows
-  p.nk = K / (w4 ? (K % 256 == 0 ? 256 : 128) : 64);
+  // (one group per unit for token tiles > 128: the activation stage of a
+  // two-group unit would leave a single B stage, serialising loads and MMAs)
+  p.nk = K / (w4 ? (K % 256 == 0 && TM <= 128 ? 256 : 128) : 64);
   p.tiles = p.n_tiles * ((M + TM - 1) / TM);
   p.T = (int64_t)p.tiles * p.nk;
   p.C = (int)std::min<int64_t>(num_sms, p.T);

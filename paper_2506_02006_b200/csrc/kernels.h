@@ -19,10 +19,6 @@ inline bool pdl_enabled() {
   }();
   return on;
 }
-// Set around a launch whose prologue must not run ahead of the previous kernel
-// (the GEMM over a just-dequantised weight copy: its producer pre-issues weight
-// loads before griddepcontrol.wait).
-inline thread_local bool pdl_suppress = false;
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -35,7 +31,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl_enabled() && !pdl_suppress) ? 1 : 0;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -54,10 +50,6 @@ struct GemmWeights {
   int inl_p0 = 0;
   uint64_t inl[kGemmInlinePages] = {};
 };
-// W4A16 image of a matrix -> its BF16 chunk image (dense, chunk order), each
-// weight bf16(code * scale) exactly as the W4 GEMM dequantises it.  Plain
-// launch (no PDL): it waits for the kernel before it, which may still read `out`.
-cudaError_t w4_dequant_launch(const GemmWeights& w4, uint16_t* out, cudaStream_t s);
 // Fill the inline page table from a host copy of `pages` (host_pages[p] ==
 // pages[p]); leaves n_inl = 0 when the matrix spans too many pages.
 void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages);

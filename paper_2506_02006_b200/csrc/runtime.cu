@@ -214,8 +214,6 @@ struct ms_ctx {
   std::vector<std::array<int64_t, 6>> graph_seen;  // shapes seen once (captured on the second sighting)
   int64_t graph_captures = 0;
   uint64_t graph_gen = 0, graph_gen_built = 0;
-  uint16_t* w4_scratch = nullptr;  // long prefills: BF16 copy of the W4 matrix being multiplied (lazy)
-  size_t w4_scratch_bytes = 0;
   float* trace_h = nullptr;  // ms_prefill_trace: device [L+1][n][d] residual stream snapshots (lazy)
   size_t trace_elems = 0;
   bool tracing = false;
@@ -407,54 +405,9 @@ ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
   return ms::GemmWeights{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
 }
 
-// Rows from which a W4A16 layer's GEMM runs as a BF16 GEMM over a dequantised
-// copy of the matrix (MS_W4_DEQUANT_M, default 512; 0 = never).  The W4 kernel
-// dequantises every weight chunk once per 256-token tile, so for a long
-// prefill one dequant pass (~N*K*2.5 bytes of traffic) plus the BF16 GEMM is
-// cheaper; decode (M <= 256) keeps the fused W4 kernel.  Same weights either
-// way: bf16(code * scale).
-int w4_dequant_rows() {
-  static const int v = [] {
-    const char* e = std::getenv("MS_W4_DEQUANT_M");
-    return e ? std::atoi(e) : 512;
-  }();
-  return v;
-}
-
-ms::GemmWeights w4_as_bf16(ms_ctx* c, const ms::GemmWeights& w4w) {
-  const size_t bytes = (size_t)w4w.N * w4w.K * 2;
-  if (bytes > c->w4_scratch_bytes) {
-    const ms_model_desc& D = c->desc;
-    const size_t qkv_n = (size_t)(D.num_heads + 2 * D.num_kv_heads) * D.head_dim;
-    const size_t mx = std::max(std::max(qkv_n * D.hidden, (size_t)D.hidden * D.num_heads * D.head_dim),
-                               (size_t)2 * D.ffn * D.hidden) * 2;
-    if (c->w4_scratch) CK(cudaFree(c->w4_scratch));
-    c->w4_scratch_bytes = std::max(bytes, mx);
-    CK(cudaMalloc(&c->w4_scratch, c->w4_scratch_bytes));
-  }
-  CK(ms::w4_dequant_launch(w4w, c->w4_scratch, c->compute));
-  c->launches += 1;
-  ms::GemmWeights b{nullptr, 0, (int64_t)(w4w.N / 128) * (w4w.K / 64), w4w.N, w4w.K};
-  b.n_inl = 1;  // one "page": the dense scratch copy, passed inline
-  b.inl_p0 = 0;
-  b.inl[0] = reinterpret_cast<uint64_t>(c->w4_scratch);
-  return b;
-}
-
-ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w_in, bool w4, int M, int TM) {
-  bool dq = w4 && w4_dequant_rows() > 0 && M >= w4_dequant_rows();
-  if (dq) {  // never while a decode step is being captured (the scratch may need allocating)
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    CK(cudaStreamIsCapturing(c->compute, &cs));
-    dq = cs == cudaStreamCaptureStatusNone;
-  }
-  const ms::GemmWeights w = dq ? w4_as_bf16(c, w_in) : w_in;
-  if (dq) w4 = false;
-  struct NoPdl {  // the GEMM's producer must not pre-issue weight loads before the dequant finished
-    bool on;
-    explicit NoPdl(bool o) : on(o) { if (on) ms::pdl_suppress = true; }
-    ~NoPdl() { if (on) ms::pdl_suppress = false; }
-  } no_pdl(dq);
+// W4A16 layers at every M run the fused kernel (int4 -> bf16 dequantised into
+// TMEM in the GEMM's staging path); no dequantised copy of a matrix exists.
+ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
   const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, w4, c->num_sms, c->part_elems);
   CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute));
@@ -828,7 +781,6 @@ int ms_ctx_destroy(ms_ctx* c) {
   drop_graphs(c);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   if (c->trace_h) cudaFree(c->trace_h);
-  if (c->w4_scratch) cudaFree(c->w4_scratch);
   if (c->tm0) cudaEventDestroy(c->tm0);
   if (c->tm1) cudaEventDestroy(c->tm1);
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);

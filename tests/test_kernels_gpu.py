@@ -112,7 +112,7 @@ def test_gemm_bf16(Nn, K, M, TM, splits):
 
 @pytest.mark.parametrize("Nn,K,M,TM,splits", [
     (128, 128, 1, 16, 1), (256, 768, 4, 16, 0), (512, 1024, 64, 64, 0), (256, 256, 200, 208, 1),
-    (512, 256, 2500, 256, 3), (768, 512, 100, 112, 5),
+    (512, 256, 2500, 256, 3), (768, 512, 100, 112, 5), (1024, 1024, 600, 256, 0),
     # Llama-2-7B decode shapes (o / down): two 128-row tiles per activation chunk
     (4096, 4096, 64, 64, 0), (4096, 11008, 64, 64, 0)])
 def test_gemm_w4(Nn, K, M, TM, splits):

@@ -27,8 +27,10 @@ def child(steps, w4s, shape, prof, order_kind, reps):
     slots = np.arange(bench.BATCH, dtype=np.int32)
     if order_kind == "lis":
         order = bench.W4_LAYERS + [l for l in range(32) if l not in bench.W4_LAYERS]
-    else:
+    elif order_kind == "seq":
         order = list(range(32))
+    else:
+        order = [int(x) for x in order_kind.split(",")]
     cur = set()
     res = {w4: [] for w4 in w4s}
     # configurations interleaved over `reps` rounds (the SM clock drifts down
@@ -75,7 +77,7 @@ def main():
     ap.add_argument("--shape", default="7b", choices=["7b", "8b"])
     ap.add_argument("--prof", action="store_true")
     ap.add_argument("--child", action="store_true")
-    ap.add_argument("--order", default="lis", choices=["lis", "seq"])
+    ap.add_argument("--order", default="lis", help="lis | seq | comma-separated layer list")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("configs", nargs="*", default=["base:"])
     a = ap.parse_args()
