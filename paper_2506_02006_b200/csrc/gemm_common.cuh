@@ -34,7 +34,7 @@ struct ChunkCursor {
     return reinterpret_cast<const uint8_t*>(i >= 0 && i < w->n_inl ? w->inl[i] : w->pages[p]);
   }
   __device__ void seek(int64_t c) {
-    const int64_t p = c / cpp;
+    const int64_t p = (c >> 31) == 0 && (cpp >> 31) == 0 ? (int64_t)((uint32_t)c / (uint32_t)cpp) : c / cpp;
     in_page = c - p * cpp;
     if (p != page) {
       page = p;
@@ -79,8 +79,9 @@ struct SegIter {
       m_tiles = p.tiles / p.n_tiles;
       g = g1 = 0;
     } else {
-      g = p.T * c / p.C;
-      g1 = p.T * (c + 1) / p.C;
+      // stream-K plans satisfy (T + 1) * C < 2^31 (gemm_plan): 32-bit division
+      g = (int64_t)((uint32_t)p.T * (uint32_t)c / (uint32_t)p.C);
+      g1 = (int64_t)((uint32_t)p.T * (uint32_t)(c + 1) / (uint32_t)p.C);
     }
   }
   __device__ int raster(int v) const {
@@ -101,7 +102,7 @@ struct SegIter {
       return true;
     }
     if (g >= g1) return false;
-    t = (int)(g / nk);
+    t = (int)((uint32_t)g / (uint32_t)nk);
     k0 = (int)(g - (int64_t)t * nk);
     const int64_t end = min(g1, (int64_t)(t + 1) * nk);
     k1 = (int)(end - (int64_t)t * nk);

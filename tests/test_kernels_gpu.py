@@ -114,7 +114,9 @@ def test_gemm_bf16(Nn, K, M, TM, splits):
     (128, 128, 1, 16, 1), (256, 768, 4, 16, 0), (512, 1024, 64, 64, 0), (256, 256, 200, 208, 1),
     (512, 256, 2500, 256, 3), (768, 512, 100, 112, 5), (1024, 1024, 600, 256, 0),
     # Llama-2-7B decode shapes (o / down): two 128-row tiles per activation chunk
-    (4096, 4096, 64, 64, 0), (4096, 11008, 64, 64, 0)])
+    (4096, 4096, 64, 64, 0), (4096, 11008, 64, 64, 0),
+    # odd K-group counts with stream-K ranges crossing tiles, TM 128
+    (1280, 1152, 48, 48, 7), (512, 512, 128, 128, 3), (1280, 640, 33, 48, 0), (640, 512, 64, 64, 3)])
 def test_gemm_w4(Nn, K, M, TM, splits):
     W = O.gen_weight(22, 1, Nn * K, 1 / np.sqrt(K)).reshape(Nn, K)
     X = O.gen_weight(22, 2, M * K, 1.0).reshape(M, K)

@@ -21,7 +21,9 @@ from paper_2506_02006_b200 import _native as N  # noqa: E402
 SHAPES = {"qkv": (12288, 4096), "o": (4096, 4096), "gate_up": (22016, 4096), "down": (4096, 11008),
           "lm_head": (32000, 4096),
           # Llama-2-13B (BASELINE configs[3] prefill): d 5120, ffn 13824
-          "qkv13": (15360, 5120), "o13": (5120, 5120), "gate_up13": (27648, 5120), "down13": (5120, 13824)}
+          "qkv13": (15360, 5120),
+          # fixed per-launch cost probes
+          "t256": (256, 128), "t4k": (4096, 128), "t4k1k": (4096, 1024), "o13": (5120, 5120), "gate_up13": (27648, 5120), "down13": (5120, 13824)}
 
 
 def stream():
@@ -62,7 +64,7 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
         N.check(L.ms_k_quant_w4(C.c_void_p(w.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), None, stream()))
         wbytes = Nn * K // 2 + Nn * K // 128 * 2
     del w
-    copies = [wp] + [wp.clone() for _ in range(max(0, -(-300_000_000 // wp.numel() // wp.element_size()) - 1))]
+    copies = [wp] + [wp.clone() for _ in range(min(63, max(0, -(-300_000_000 // wp.numel() // wp.element_size()) - 1)))]
     xp = torch.randint(-2000, 2000, (((M + TM - 1) // TM) * TM * K,), dtype=torch.int16, device="cuda")
     out = torch.zeros((160 if M <= 256 else 4) * M * Nn, dtype=torch.float32, device="cuda")
     used = C.c_int()
