@@ -51,7 +51,10 @@ const char* ms_last_error(void);
 
 /* Bytes of one arena page = one KV block (all layers, K and V). */
 int64_t ms_page_bytes(const ms_model_desc* desc);
-/* Pages one layer's packed image occupies at `bits` (16 = BF16, 4 = W4A16 g128).
+/* Pages one layer's packed image occupies at `bits`: 16 = BF16, 8 / 4 / 3 =
+ * the reference's kQ8 / kQ4 / kQ3 levels (proj/include/morphsim/toy_model.hpp:26)
+ * as g128 codes + bf16 scales (Q8: one byte per code; Q4 and Q3: 4-bit
+ * containers, so a Q3 image occupies the same pages as Q4).
  * page_count * ms_page_bytes() is the value a morphsim config must use for
  * model.layer_bytes[...] so that floor(freed / block_bytes) matches
  * (reference proj/src/engine.cpp:273, SimModelConfig sim_config.hpp:17-28). */
@@ -66,13 +69,20 @@ int ms_num_sms(ms_ctx* ctx);
 /* Generates every tensor on the device with the counter RNG that
  * oracle/ref_llama.c restates bit for bit, packs the BF16 image of every layer
  * into arena pages (all layers start BF16), and builds the pinned-host variant
- * store (BF16 and W4 g128 images of every layer) the LayerSwapper uploads from. */
+ * store the LayerSwapper uploads from: BF16 and Q4 images of every layer, plus
+ * Q8 / Q3 when enabled with ms_variant_enable. */
 int ms_weights_synthetic(ms_ctx* ctx, uint64_t seed);
 /* Row-major bf16 upload of one tensor (layer -1 = global: which 0 embed,
  * 1 final norm, 2 lm_head; layer >= 0: 0 norm1, 1 qkv, 2 o, 3 norm2, 4 gate_up,
  * 5 down).  After all tensors: ms_weights_finalize(). */
 int ms_weights_upload(ms_ctx* ctx, int layer, int which, const uint16_t* host_bf16, int64_t count);
 int ms_weights_finalize(ms_ctx* ctx);
+/* Adds the `bits` level (16, 8, 4, 3) to the variant store built at weight
+ * finalisation (BF16 and Q4 are always built; Q8 and Q3 on request, each
+ * costs one more pinned image per layer).  Must precede ms_weights_*.
+ * Replaces the reference's eager build of every level
+ * (proj/src/toy_model.cpp:64-75 materialize_variants). */
+int ms_variant_enable(ms_ctx* ctx, int bits);
 /* Registers caller-owned host memory as the variant-store image of one layer at
  * `bits` (SURVEY 8(b) ms_variant_register; the LayerSwapper uploads from it).
  * Must precede ms_weights_synthetic / ms_weights_finalize.  The memory is
@@ -198,6 +208,10 @@ int ms_prof_attention_read(ms_ctx* ctx, float* total_ms, int64_t* launches);
 int ms_k_gen_weight(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset, uint16_t* out,
                     void* stream);
 int ms_k_pack_bf16(const uint16_t* w, int N, int K, uint16_t* out, void* stream);
+/* g128 quantiser (reference quantize_weights, proj/src/toy_model.cpp:47-60, per
+ * 128-wide group) + packer: bits 8 -> W8 chunks (16640 B), 4 / 3 -> 4-bit
+ * container chunks (8448 B); codes_out (optional) = int8 codes [N][K]. */
+int ms_k_quant(int bits, const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, void* stream);
 int ms_k_quant_w4(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, void* stream);
 int ms_k_pack_act(const uint16_t* x, int M, int K, int TM, uint16_t* out, void* stream);
 /* out[s][m][n] fp32 partials of W(packed, bits) x X(packed, TM) from the

@@ -59,6 +59,7 @@ def lib():
         L.ref_dequant_w4.argtypes = [i8p, u16p, C.c_int64, C.c_int64, C.c_int, u16p]
         L.ref_pack_bf16.argtypes = [u16p, C.c_int64, C.c_int64, u16p]
         L.ref_pack_w4.argtypes = [i8p, u16p, C.c_int64, C.c_int64, u8p]
+        L.ref_pack_w8.argtypes = [i8p, u16p, C.c_int64, C.c_int64, u8p]
         L.ref_gemm_bf16.argtypes = [u16p, u16p, C.c_int64, C.c_int64, C.c_int64, f32p]
         L.ref_rmsnorm.argtypes = [f32p, u16p, C.c_int64, C.c_int64, C.c_float, u16p]
         L.ref_attention.argtypes = [f32p, u16p, u16p, C.c_int, C.c_int, C.c_int, C.c_int, u16p, f32p]
@@ -138,6 +139,7 @@ def quantize_groups(w_bf16: np.ndarray, group: int = 128, bits: int = 4):
 
 
 def dequant_w4(codes: np.ndarray, scales_bf16: np.ndarray) -> np.ndarray:
+    """bf16(code * float(scale_bf16)) per g128 group (every quantised level: 8, 4, 3 bits)."""
     N, K = codes.shape
     out = np.empty((N, K), np.uint16)
     lib().ref_dequant_w4(np.ascontiguousarray(codes), np.ascontiguousarray(scales_bf16), N, K, 128, out)
@@ -156,6 +158,18 @@ def pack_w4(codes: np.ndarray, scales_bf16: np.ndarray) -> np.ndarray:
     out = np.empty((N // 128) * (K // 128) * 8448, np.uint8)
     lib().ref_pack_w4(np.ascontiguousarray(codes), np.ascontiguousarray(scales_bf16), N, K, out)
     return out
+
+
+def pack_w8(codes: np.ndarray, scales_bf16: np.ndarray) -> np.ndarray:
+    N, K = codes.shape
+    out = np.empty((N // 128) * (K // 128) * 16640, np.uint8)
+    lib().ref_pack_w8(np.ascontiguousarray(codes), np.ascontiguousarray(scales_bf16), N, K, out)
+    return out
+
+
+def pack_quant(codes: np.ndarray, scales_bf16: np.ndarray, bits: int) -> np.ndarray:
+    """Device image of a quantised matrix: W8 chunks for 8 bits, 4-bit containers for 4 and 3 bits."""
+    return pack_w8(codes, scales_bf16) if bits == 8 else pack_w4(codes, scales_bf16)
 
 
 def gemm_bf16(W: np.ndarray, X: np.ndarray) -> np.ndarray:

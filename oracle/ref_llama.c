@@ -176,6 +176,29 @@ void ref_pack_w4(const int8_t* codes, const uint16_t* scales_bf16, int64_t N, in
   }
 }
 
+/* W8 chunk layout: chunk (n_tile, group g of 128 K) = 16640 bytes:
+ *   bytes [0, 16384): codes as [j 8][row 128][16 B]; the 16 B of (j,row) hold
+ *   K-elements [16j, 16j+16) of the group in order, one byte each, stored as
+ *   (code + 128) (codes are in [-127, 127], so 1..255);
+ *   bytes [16384, 16640): 128 bf16 scales, one per row.
+ * Q3 (codes in [-3, 3]) uses the W4 layout above (4-bit containers). */
+void ref_pack_w8(const int8_t* codes, const uint16_t* scales_bf16, int64_t N, int64_t K,
+                 uint8_t* out) {
+  const int64_t G = K / 128;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n) {
+    const int64_t nt = n / 128, row = n % 128;
+    for (int64_t g = 0; g < G; ++g) {
+      uint8_t* chunk = out + (nt * G + g) * 16640;
+      for (int j = 0; j < 8; ++j)
+        for (int e = 0; e < 16; ++e)
+          chunk[(j * 128 + row) * 16 + e] = (uint8_t)(codes[n * K + g * 128 + j * 16 + e] + 128);
+      uint16_t s = scales_bf16[n * G + g];
+      memcpy(chunk + 16384 + row * 2, &s, 2);
+    }
+  }
+}
+
 /* --------------------------------------------------------------- model */
 typedef struct {
   int L, d, H, KVH, hd, ffn, V, max_pos;
@@ -190,7 +213,7 @@ typedef struct {
   uint16_t **norm1, **norm2;
   uint16_t **wqkv, **wo, **wgu, **wd;       /* effective bf16 weights */
   uint16_t **bqkv, **bo, **bgu, **bd;       /* pristine BF16 copies (for restore) */
-  int* tag;                                  /* 0 = BF16, 4 = W4 */
+  int* tag;                                  /* 0 = BF16, else the quantised bits (8, 4, 3) */
   float *rope_cos, *rope_sin;                /* [max_pos][hd/2] */
 } ref_model;
 
@@ -251,10 +274,10 @@ ref_model* ref_model_create(const ref_cfg* cfg, uint64_t seed) {
   return m;
 }
 
-static uint16_t* dequant_copy(const uint16_t* w, int64_t N, int64_t K) {
+static uint16_t* dequant_copy(const uint16_t* w, int64_t N, int64_t K, int bits) {
   int8_t* codes = (int8_t*)malloc((size_t)N * K);
   uint16_t* sc = (uint16_t*)malloc((size_t)N * (K / 128) * 2);
-  ref_quantize_groups(w, N, K, 128, 4, codes, NULL, sc);
+  ref_quantize_groups(w, N, K, 128, bits, codes, NULL, sc);
   uint16_t* out = (uint16_t*)malloc((size_t)N * K * 2);
   ref_dequant_w4(codes, sc, N, K, 128, out);
   free(codes);
@@ -262,19 +285,21 @@ static uint16_t* dequant_copy(const uint16_t* w, int64_t N, int64_t K) {
   return out;
 }
 
-/* Per-layer precision dispatch (toy_model.cpp:153): bits 16 or 4. */
+/* Per-layer precision dispatch (toy_model.cpp:153; precision levels
+ * toy_model.hpp:26 kFull/kQ8/kQ4/kQ3): bits 16, 8, 4 or 3, every quantised
+ * level through the same g128 quantiser and bf16(code * scale) contract. */
 void ref_model_set_precision(ref_model* m, int layer, int bits) {
   const ref_cfg* c = &m->c;
   const int64_t qkv_n = (int64_t)(c->H + 2 * c->KVH) * c->hd;
-  if (m->tag[layer] == 4) {
+  if (m->tag[layer] != 0) {
     free(m->wqkv[layer]); free(m->wo[layer]); free(m->wgu[layer]); free(m->wd[layer]);
   }
-  if (bits == 4) {
-    m->wqkv[layer] = dequant_copy(m->bqkv[layer], qkv_n, c->d);
-    m->wo[layer] = dequant_copy(m->bo[layer], c->d, (int64_t)c->H * c->hd);
-    m->wgu[layer] = dequant_copy(m->bgu[layer], (int64_t)2 * c->ffn, c->d);
-    m->wd[layer] = dequant_copy(m->bd[layer], c->d, c->ffn);
-    m->tag[layer] = 4;
+  if (bits == 8 || bits == 4 || bits == 3) {
+    m->wqkv[layer] = dequant_copy(m->bqkv[layer], qkv_n, c->d, bits);
+    m->wo[layer] = dequant_copy(m->bo[layer], c->d, (int64_t)c->H * c->hd, bits);
+    m->wgu[layer] = dequant_copy(m->bgu[layer], (int64_t)2 * c->ffn, c->d, bits);
+    m->wd[layer] = dequant_copy(m->bd[layer], c->d, c->ffn, bits);
+    m->tag[layer] = bits;
   } else {
     m->wqkv[layer] = m->bqkv[layer]; m->wo[layer] = m->bo[layer];
     m->wgu[layer] = m->bgu[layer]; m->wd[layer] = m->bd[layer];
@@ -302,7 +327,7 @@ uint16_t* ref_model_tensor(ref_model* m, int layer, int which) {
 void ref_model_destroy(ref_model* m) {
   if (!m) return;
   for (int l = 0; l < m->c.L; ++l) {
-    if (m->tag[l] == 4) ref_model_set_precision(m, l, 16);
+    if (m->tag[l] != 0) ref_model_set_precision(m, l, 16);
     free(m->norm1[l]); free(m->norm2[l]);
     free(m->bqkv[l]); free(m->bo[l]); free(m->bgu[l]); free(m->bd[l]);
   }
@@ -721,10 +746,10 @@ double ref_bench_decode_sample(const ref_cfg* c, int B, int ctx, int w4, uint64_
   uint16_t* wd = gen_alloc(seed, t_layer(0, W_DOWN), (int64_t)d * ffn, 1.0 / sqrt((double)ffn), 0.0);
   if (w4) {
     uint16_t* t;
-    t = dequant_copy(wqkv, qkv_n, d); free(wqkv); wqkv = t;
-    t = dequant_copy(wo, d, (int64_t)H * hd); free(wo); wo = t;
-    t = dequant_copy(wgu, (int64_t)2 * ffn, d); free(wgu); wgu = t;
-    t = dequant_copy(wd, d, ffn); free(wd); wd = t;
+    t = dequant_copy(wqkv, qkv_n, d, 4); free(wqkv); wqkv = t;
+    t = dequant_copy(wo, d, (int64_t)H * hd, 4); free(wo); wo = t;
+    t = dequant_copy(wgu, (int64_t)2 * ffn, d, 4); free(wgu); wgu = t;
+    t = dequant_copy(wd, d, ffn, 4); free(wd); wd = t;
   }
   const size_t per_seq = (size_t)ctx * KVH * hd;
   uint16_t* kc = gen_alloc(seed ^ 0x55, 1000, (int64_t)(per_seq * B), 1.0, 0.0);

@@ -59,6 +59,7 @@ SIGNATURES = [
     ("ms_weights_synthetic", C.c_int, [_P, C.c_uint64]),
     ("ms_weights_upload", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64]),
     ("ms_weights_finalize", C.c_int, [_P]),
+    ("ms_variant_enable", C.c_int, [_P, C.c_int]),
     ("ms_variant_bytes", C.c_int64, [_P, C.c_int]),
     ("ms_variant_export", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64]),
     ("ms_variant_register", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64, C.c_int]),
@@ -95,6 +96,7 @@ SIGNATURES = [
     ("ms_prof_attention_read", C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_int64)]),
     ("ms_k_gen_weight", C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_double, C.c_double, _P, _P]),
     ("ms_k_pack_bf16", C.c_int, [_P, C.c_int, C.c_int, _P, _P]),
+    ("ms_k_quant", C.c_int, [C.c_int, _P, C.c_int, C.c_int, _P, _P, _P]),
     ("ms_k_quant_w4", C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P]),
     ("ms_k_pack_act", C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _P]),
     ("ms_k_gemm", C.c_int, [C.c_int, _P, C.c_int, C.c_int, _P, C.c_int, C.c_int, C.c_int, _P,

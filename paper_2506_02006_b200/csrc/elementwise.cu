@@ -458,45 +458,65 @@ cudaError_t pack_bf16_launch(const uint16_t* w, int N, int K, uint16_t* out, cud
   return cudaGetLastError();
 }
 
-// ----------------------------------------- g128 W4 quantiser + chunk packer
-// One thread per (row, group).  Reference semantics (toy_model.cpp:40-60):
-// scale = max|w| / 7 in fp64, code = round(w / scale) (half away from zero),
-// all-zero group -> scale 1, codes 0.  Stored: nibble (code + 8), bf16 scale.
-__global__ void quant_w4_kernel(const uint16_t* __restrict__ w, int N, int K, uint8_t* __restrict__ out,
-                                int8_t* __restrict__ codes_out) {
+// --------------------------------- g128 quantiser (8 / 4 / 3 bits) + chunk packer
+// One thread per (row, group).  Reference semantics (toy_model.cpp:40-60, for
+// every bit width of toy_model.hpp:26): scale = max|w| / (2^(bits-1) - 1) in
+// fp64, code = round(w / scale) (half away from zero), all-zero group ->
+// scale 1, codes 0.  Stored: 4-bit containers (code + 8) for 4 and 3 bits
+// (W4 chunk, 8448 B), bytes (code + 128) for 8 bits (W8 chunk, 16640 B); the
+// bf16 scales follow the codes.
+__global__ void quant_kernel(const uint16_t* __restrict__ w, int N, int K, int bits, uint8_t* __restrict__ out,
+                             int8_t* __restrict__ codes_out) {
   const int G = K / 128;
   const int64_t total = (int64_t)N * G;
+  const double qmax = (double)((1 << (bits - 1)) - 1);
+  const int chunk_bytes = bits == 8 ? kW8ChunkBytes : kW4ChunkBytes;
+  const int code_bytes = bits == 8 ? 16384 : 8192;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int n = (int)(idx / G), g = (int)(idx - (int64_t)n * G);
     const uint16_t* src = w + (size_t)n * K + (size_t)g * 128;
     double mx = 0.0;
     for (int i = 0; i < 128; ++i) mx = fmax(mx, fabs((double)bf2f(src[i])));
-    const double scale = mx == 0.0 ? 1.0 : __ddiv_rn(mx, 7.0);
-    uint8_t* chunk = out + ((int64_t)(n >> 7) * G + g) * 8448;
+    const double scale = mx == 0.0 ? 1.0 : __ddiv_rn(mx, qmax);
+    uint8_t* chunk = out + ((int64_t)(n >> 7) * G + g) * chunk_bytes;
     const int row = n & 127;
-    for (int j = 0; j < 4; ++j) {
-      uint32_t words[4];
-      for (int q = 0; q < 4; ++q) {
-        uint32_t v = 0;
-        for (int e = 0; e < 8; ++e) {
-          const int kk = j * 32 + q * 8 + e;
-          const int code = mx == 0.0 ? 0 : (int)round(__ddiv_rn((double)bf2f(src[kk]), scale));
-          if (codes_out) codes_out[(size_t)n * K + (size_t)g * 128 + kk] = (int8_t)code;
-          v |= ((uint32_t)(code + 8) & 0xFu) << ((e & 1) * 16 + (e >> 1) * 4);
+    auto code_of = [&](int kk) {
+      const int code = mx == 0.0 ? 0 : (int)round(__ddiv_rn((double)bf2f(src[kk]), scale));
+      if (codes_out) codes_out[(size_t)n * K + (size_t)g * 128 + kk] = (int8_t)code;
+      return code;
+    };
+    if (bits == 8) {
+      for (int j = 0; j < 8; ++j) {
+        uint32_t words[4];
+        for (int q = 0; q < 4; ++q) {
+          uint32_t v = 0;
+          for (int e = 0; e < 4; ++e) v |= ((uint32_t)(code_of(j * 16 + q * 4 + e) + 128) & 0xFFu) << (8 * e);
+          words[q] = v;
         }
-        words[q] = v;
+        *reinterpret_cast<uint4*>(chunk + (j * 128 + row) * 16) = make_uint4(words[0], words[1], words[2], words[3]);
       }
-      *reinterpret_cast<uint4*>(chunk + (j * 128 + row) * 16) = make_uint4(words[0], words[1], words[2], words[3]);
+    } else {
+      for (int j = 0; j < 4; ++j) {
+        uint32_t words[4];
+        for (int q = 0; q < 4; ++q) {
+          uint32_t v = 0;
+          for (int e = 0; e < 8; ++e)
+            v |= ((uint32_t)(code_of(j * 32 + q * 8 + e) + 8) & 0xFu) << ((e & 1) * 16 + (e >> 1) * 4);
+          words[q] = v;
+        }
+        *reinterpret_cast<uint4*>(chunk + (j * 128 + row) * 16) = make_uint4(words[0], words[1], words[2], words[3]);
+      }
     }
-    *reinterpret_cast<uint16_t*>(chunk + 8192 + row * 2) = f2bf(__double2float_rn(scale));
+    *reinterpret_cast<uint16_t*>(chunk + code_bytes + row * 2) = f2bf(__double2float_rn(scale));
   }
 }
-cudaError_t quant_w4_launch(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, cudaStream_t s) {
+cudaError_t quant_launch(const uint16_t* w, int N, int K, int bits, uint8_t* out, int8_t* codes_out, cudaStream_t s) {
+  if (bits != 8 && bits != 4 && bits != 3) return cudaErrorInvalidValue;
   const int64_t total = (int64_t)N * (K / 128);
   int64_t blocks = (total + 127) / 128;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  quant_w4_kernel<<<(int)blocks, 128, 0, s>>>(w, N, K, out, codes_out);
+  quant_kernel<<<(int)blocks, 128, 0, s>>>(w, N, K, bits, out, codes_out);
   return cudaGetLastError();
 }
 

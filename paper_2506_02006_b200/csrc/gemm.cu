@@ -1,7 +1,8 @@
 // gemm.cu -- the decoder linear layers on 5th-gen tensor cores (tcgen05).
 //
 // P[slot][m][n] = sum_{k in segment} W[n][k] * X[m][k] for one weight matrix W
-// [N x K] (BF16, or W4A16 g128 dequantised in the staging path) and a token
+// [N x K] (BF16, or g128-quantised Q8 / Q4 / Q3 codes dequantised in the
+// staging path) and a token
 // block X [M x K] (BF16), fp32 partials.  "Swap-AB": the weight rows are the
 // UMMA M=128 side and the tokens the UMMA N side (16..256, runtime), so a
 // decode batch of 64 is one N=64 instruction and a prefill is N=256 tiles --
@@ -9,7 +10,7 @@
 //
 // Replaces the priced stand-ins `decode_ms_per_layer[tag]` (reference
 // proj/src/sim_config.cpp:23-27) and `tokens * prefill_ms_per_token`
-// (proj/src/engine.cpp:477-478); the BF16-vs-W4 choice comes from the layer
+// (proj/src/engine.cpp:477-478); the per-layer precision comes from the layer
 // table snapshot taken at step launch (engine.cpp:523-525).
 //
 // Persistent, stream-K balanced: one CTA per SM walks a contiguous range of
@@ -24,6 +25,8 @@
 // the UMMA canonical K-major no-swizzle image:
 //   weight chunk (n_tile, kb64)  = 16 KB  [row_group 16][k_chunk 8][row 8][8 bf16]
 //   W4 chunk (n_tile, g128)      = 8448 B [j 4][row 128][16 B codes] + 128 bf16 scales
+//                                  (Q4 and Q3 codes, 4-bit containers)
+//   W8 chunk (n_tile, g128)      = 16640 B [j 8][row 128][16 B codes] + 128 bf16 scales
 //   activation chunk (m_tile,kb) = TM*128 B, same core-matrix order.
 // Weight chunks are found through the variant image's page table, so a layer
 // image may live in any free pages of the KV/weight arena.
@@ -236,8 +239,22 @@ constexpr int kMaxAStages = 8;
 
 // kGPS = 128-wide K groups per pipeline unit (1 or 2): two groups per unit
 // halve the per-unit handshakes (mbarrier round trips, MMA commits, B copies)
-// per weight byte.
-template <int kG, int kGPS>
+// per weight byte.  kBits = code width of the chunk format: 4 (the 4- and
+// 3-bit levels, nibble containers) or 8 (Q8, one byte per code; kGPS = 1).
+//
+// Q8 conversion, per pair of codes: byte_perm puts code + 128 into the
+// mantissa of 2^23 (fp32 0x4B0000xx), one FADD removes 2^23 + 128 (exact),
+// one FMUL by the fp32 scale (exact: 7 x 8 significant bits), and one
+// cvt.rn.bf16x2.f32 rounds both products once: bf16(code * scale), the same
+// contract as the 4-bit levels.
+__device__ __forceinline__ uint32_t w8_pair(uint32_t word, int e, float s) {
+  const float a = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7440u | (uint32_t)e)) - 8388736.0f;
+  const float b = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7440u | (uint32_t)(e + 1))) - 8388736.0f;
+  __nv_bfloat162 v = __floats2bfloat162_rn(a * s, b * s);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int kG, int kGPS, int kBits>
 __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
                         float* __restrict__ out, int bstages, int rstages, int astages, int dbg) {
@@ -247,8 +264,11 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   const int cta = blockIdx.x;
   const int nk = plan.nk;
   const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk; a B stage holds 2 * kGPS
-  constexpr uint32_t raw_stage = kGPS == 1 ? 8576u : 16896u;
-  constexpr uint32_t raw_bytes = kGPS * (uint32_t)kW4ChunkBytes;
+  static_assert(kBits == 4 || (kBits == 8 && kGPS == 1), "Q8 units hold one K group");
+  constexpr uint32_t chunkB = kBits == 8 ? (uint32_t)kW8ChunkBytes : (uint32_t)kW4ChunkBytes;
+  constexpr uint32_t code_bytes = kBits == 8 ? 16384u : 8192u;
+  constexpr uint32_t raw_stage = kBits == 8 ? 16640u : (kGPS == 1 ? 8576u : 16896u);
+  constexpr uint32_t raw_bytes = kGPS * chunkB;
   constexpr uint32_t a_cols = 64u * kGPS;  // packed bf16x2 TMEM columns of one A stage
   const int64_t gpr = W.K / 128;           // W4 chunks (K groups) per weight row tile
   const uint32_t tm_cols = TM <= 32 ? 32u : TM <= 64 ? 64u : TM <= 128 ? 128u : 256u;
@@ -301,7 +321,7 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   // Producer (thread 0, which initialised the barriers): the first ring of raw
   // int4 chunks is issued before the TMEM allocation and the CTA barrier.
   uint32_t npre = 0;
-  ChunkCursor cur(W, kW4ChunkBytes);
+  ChunkCursor cur(W, (int)chunkB);
   // one unit's kGPS consecutive chunks into raw stage r (one copy when they
   // are contiguous in the same page); leaves the cursor at the next unit
   auto issue_unit = [&](int r) {
@@ -309,16 +329,16 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     const uint8_t* c0 = cur.get();
     cur.advance();
     if (kGPS == 1) {
-      bulk_g2s(sRaw(r), c0, kW4ChunkBytes, &rfull[r]);
+      bulk_g2s(sRaw(r), c0, chunkB, &rfull[r]);
       return;
     }
     const uint8_t* c1 = cur.get();
     cur.advance();
-    if (c1 == c0 + kW4ChunkBytes) {
-      bulk_g2s(sRaw(r), c0, 2 * kW4ChunkBytes, &rfull[r]);
+    if (c1 == c0 + chunkB) {
+      bulk_g2s(sRaw(r), c0, 2 * chunkB, &rfull[r]);
     } else {
-      bulk_g2s(sRaw(r), c0, kW4ChunkBytes, &rfull[r]);
-      bulk_g2s(sRaw(r) + kW4ChunkBytes, c1, kW4ChunkBytes, &rfull[r]);
+      bulk_g2s(sRaw(r), c0, chunkB, &rfull[r]);
+      bulk_g2s(sRaw(r) + chunkB, c1, chunkB, &rfull[r]);
     }
   };
   if (threadIdx.x == 0) {
@@ -492,18 +512,22 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
         mbar_wait(&rfull[rs], (it / rstages) & 1);
         if (lane == 0 && quad == 0) stamp(1, it);
         const uint8_t* raw = sRaw(rs);
+        constexpr int kQ = kBits == 8 ? 8 : 4;  // uint4 of codes per row per K group
         __nv_bfloat162 sc[kGPS];
-        uint4 q[kGPS][4];
+        uint4 q[kGPS][kQ];
 #pragma unroll
         for (int h = 0; h < kGPS; ++h) {
-          const uint8_t* rh = raw + h * kW4ChunkBytes;
-          sc[h].x = __ushort_as_bfloat16(*reinterpret_cast<const uint16_t*>(rh + 8192 + 2 * row));
+          const uint8_t* rh = raw + h * chunkB;
+          sc[h].x = __ushort_as_bfloat16(*reinterpret_cast<const uint16_t*>(rh + code_bytes + 2 * row));
           sc[h].y = sc[h].x;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) q[h][j] = *reinterpret_cast<const uint4*>(rh + (j * 128 + row) * 16);
+          for (int j = 0; j < kQ; ++j) q[h][j] = *reinterpret_cast<const uint4*>(rh + (j * 128 + row) * 16);
         }
+        // raw chunk consumed (values are in registers): order these generic-proxy
+        // reads before the producer's next async-proxy (bulk copy) write
+        fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&rempty[rs]);  // raw chunk consumed (values are in registers)
+        if (lane == 0) mbar_arrive(&rempty[rs]);
         if (it >= (uint32_t)astages) mbar_wait(&aempty[a], ((it / astages) & 1) ^ 1);
         if (lane == 0 && quad == 0) stamp(2, it);
         tc_fence_after();
@@ -517,19 +541,33 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t o[32];
+            if (kBits == 8) {
+              const float s32 = __bfloat162float(sc[h].x);
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-              const uint4 qq = q[h][hh * 2 + jj];
-              const uint32_t words[4] = {qq.x, qq.y, qq.z, qq.w};
+              for (int jj = 0; jj < 4; ++jj) {
+                const uint4 qq = q[h][hh * 4 + jj];
+                const uint32_t words[4] = {qq.x, qq.y, qq.z, qq.w};
 #pragma unroll
-              for (int w = 0; w < 4; ++w)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const uint32_t x = nib_magic(words[w] >> (4 * i));
-                  __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
-                  v = __hmul2(__hsub2(v, bias), sc[h]);  // exact code, then one rounding of code*scale
-                  o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
+                for (int w = 0; w < 4; ++w) {
+                  o[jj * 8 + w * 2 + 0] = w8_pair(words[w], 0, s32);
+                  o[jj * 8 + w * 2 + 1] = w8_pair(words[w], 2, s32);
                 }
+              }
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 2; ++jj) {
+                const uint4 qq = q[h][hh * 2 + jj];
+                const uint32_t words[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    const uint32_t x = nib_magic(words[w] >> (4 * i));
+                    __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&x);
+                    v = __hmul2(__hsub2(v, bias), sc[h]);  // exact code, then one rounding of code*scale
+                    o[jj * 16 + w * 4 + i] = *reinterpret_cast<uint32_t*>(&v);
+                  }
+              }
             }
             tmem_st32(lane_base + (uint32_t)a * a_cols + (uint32_t)h * 64u + (uint32_t)hh * 32u, o);
           }
@@ -549,30 +587,15 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   if (warp == 1) tmem_dealloc(tmem_base, 512);
 }
 
-// Dequantiser groups (MS_W4_GROUPS=2|3|4, experiments; default 3: fastest in the 7B step with 32 W4 layers).
-static int w4_groups() {
-  static const int v = [] {
-    const char* e = std::getenv("MS_W4_GROUPS");
-    const int g = e ? std::atoi(e) : 3;
-    return g == 2 || g == 4 ? g : 3;
-  }();
-  return v;
-}
-
-static int w4_env(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
-
-static int pick_w4_stages(int TM, int gps, int* rstages, int* astages, size_t* smem_out) {
+// Ring sizes of the quantised kernel: activation (B) stages, raw chunk
+// stages (the rest of the shared-memory budget), TMEM A stages.
+static int pick_q_stages(int TM, int gps, int bits, int* rstages, int* astages, size_t* smem_out) {
   const size_t budget = 215 * 1024;
   const size_t bst = (size_t)TM * 128 * 2 * gps;
-  const size_t raw_stage = gps == 1 ? 8576 : 16896;
-  static const int bs_env = w4_env("MS_W4_BSTAGES", 0), rs_env = w4_env("MS_W4_RSTAGES", 16);
-  int bs = gps == 1 ? (TM <= 64 ? 6 : (TM <= 128 ? 4 : 2)) : (TM <= 64 ? 3 : (TM <= 128 ? 2 : 1));
-  if (bs_env > 0 && (size_t)bs_env * bst <= budget / 2) bs = bs_env;
+  const size_t raw_stage = bits == 8 ? 16640 : (gps == 1 ? 8576 : 16896);
+  const int bs = gps == 1 ? (TM <= 64 ? 6 : (TM <= 128 ? 4 : 2)) : (TM <= 64 ? 3 : (TM <= 128 ? 2 : 1));
   int rs = (int)((budget - bs * bst) / raw_stage);
-  if (rs > rs_env) rs = rs_env;
+  if (rs > 16) rs = 16;
   if (rs < 2) rs = 2;
   *rstages = rs;
   const int tm_cols = TM <= 32 ? 32 : TM <= 64 ? 64 : TM <= 128 ? 128 : 256;
@@ -582,8 +605,8 @@ static int pick_w4_stages(int TM, int gps, int* rstages, int* astages, size_t* s
   return bs;
 }
 
-void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages) {
-  const int64_t chunks = (int64_t)(w.N / 128) * (w.K / (w4 ? 128 : 64));
+void gemm_inline_pages(GemmWeights& w, int wkind, const uint64_t* host_pages) {
+  const int64_t chunks = (int64_t)(w.N / 128) * (w.K / chunk_k(wkind));
   const int64_t p0 = w.first_chunk / w.chunks_per_page;
   const int64_t p1 = (w.first_chunk + chunks - 1) / w.chunks_per_page;
   w.n_inl = 0;
@@ -593,14 +616,15 @@ void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages) {
   w.n_inl = (int)(p1 - p0 + 1);
 }
 
-GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t part_elems) {
+GemmPlanDev gemm_plan(int N, int K, int M, int TM, int wkind, int num_sms, size_t part_elems) {
   GemmPlanDev p{};
   p.n_tiles = N / 128;
   p.TM = TM;
-  // W4: two 128-wide K groups per pipeline unit when K allows
+  // int4: two 128-wide K groups per pipeline unit when K allows
   // (one group per unit for token tiles > 128: the activation stage of a
-  // two-group unit would leave a single B stage, serialising loads and MMAs)
-  p.nk = K / (w4 ? (K % 256 == 0 && TM <= 128 ? 256 : 128) : 64);
+  // two-group unit would leave a single B stage, serialising loads and MMAs);
+  // int8: one K group per unit (a group's raw chunk is already 16.6 KB)
+  p.nk = wkind == 16 ? K / 64 : wkind == 8 ? K / 128 : K / (K % 256 == 0 && TM <= 128 ? 256 : 128);
   p.tiles = p.n_tiles * ((M + TM - 1) / TM);
   p.T = (int64_t)p.tiles * p.nk;
   p.C = (int)std::min<int64_t>(num_sms, p.T);
@@ -628,42 +652,43 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t 
   return p;
 }
 
-template <int kG, int kGPS>
-static cudaError_t launch_w4_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                  float* out, cudaStream_t stream) {
+template <int kG, int kGPS, int kBits>
+static cudaError_t launch_q_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+                                 float* out, cudaStream_t stream) {
   int rs = 0, as = 0;
   size_t sm = 0;
-  const int bs = pick_w4_stages(TM, kGPS, &rs, &as, &sm);
+  const int bs = pick_q_stages(TM, kGPS, kBits, &rs, &as, &sm);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG, kGPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG, kGPS, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
     attr = true;
   }
-  return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M, TM,
-                    plan, out, bs, rs, as, gemm_debug());
+  return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS, kBits>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M,
+                    TM, plan, out, bs, rs, as, gemm_debug());
 }
 
-template <int kGPS>
-static cudaError_t launch_w4_groups(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                    float* out, cudaStream_t stream) {
-  // no more dequantiser groups than TMEM A stages (a group holds one stage)
+// Three dequantiser groups (fastest in the 7B step), two when TMEM holds only
+// two A stages (a group holds one stage).
+template <int kGPS, int kBits>
+static cudaError_t launch_q_groups(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+                                   float* out, cudaStream_t stream) {
   int rs = 0, as = 0;
   size_t sm = 0;
-  pick_w4_stages(TM, kGPS, &rs, &as, &sm);
-  switch (std::min(w4_groups(), as)) {
-    case 3: return launch_w4_tmem<3, kGPS>(w, x, M, TM, plan, out, stream);
-    case 4: return launch_w4_tmem<4, kGPS>(w, x, M, TM, plan, out, stream);
-    default: return launch_w4_tmem<2, kGPS>(w, x, M, TM, plan, out, stream);
-  }
+  pick_q_stages(TM, kGPS, kBits, &rs, &as, &sm);
+  if (as >= 3) return launch_q_tmem<3, kGPS, kBits>(w, x, M, TM, plan, out, stream);
+  return launch_q_tmem<2, kGPS, kBits>(w, x, M, TM, plan, out, stream);
 }
 
-cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+cudaError_t gemm_launch(const GemmWeights& w, int wkind, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                         float* out, cudaStream_t stream) {
-  if (w4) {
+  if (wkind == 8) return launch_q_groups<1, 8>(w, x, M, TM, plan, out, stream);
+  if (wkind == 4) {
     // the plan fixed the unit: K / nk = 256 -> two K groups per pipeline unit
-    if (w.K / plan.nk == 256) return launch_w4_groups<2>(w, x, M, TM, plan, out, stream);
-    return launch_w4_groups<1>(w, x, M, TM, plan, out, stream);
+    if (w.K / plan.nk == 256) return launch_q_groups<2, 4>(w, x, M, TM, plan, out, stream);
+    return launch_q_groups<1, 4>(w, x, M, TM, plan, out, stream);
   }
+  if (wkind != 16) return cudaErrorInvalidValue;
   static const int max_st = [] {  // (experiments) ring depth cap
     const char* e = std::getenv("MS_GEMM_STAGES");
     return e ? std::atoi(e) : 8;

@@ -9,8 +9,6 @@
 
 namespace ms {
 
-constexpr int kBf16ChunkBytes = 16384;
-constexpr int kW4ChunkBytes = 8448;
 
 __device__ __forceinline__ const uint8_t* chunk_ptr(const GemmWeights& w, int64_t ci, int chunk_bytes) {
   const int64_t c = w.first_chunk + ci;

@@ -35,6 +35,19 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Packed weight chunk sizes: one chunk = 128 weight
+// rows x one K block (64 for BF16, a 128-wide quantisation group otherwise).
+constexpr int kBf16ChunkBytes = 16384;  // [row_group 16][k_chunk 8][row 8][8 bf16]
+constexpr int kW4ChunkBytes = 8448;     // [j 4][row 128][16 B of nibbles] + 128 bf16 scales (4- and 3-bit codes)
+constexpr int kW8ChunkBytes = 16640;    // [j 8][row 128][16 B of bytes] + 128 bf16 scales
+// Weight kinds of the GEMM: 16 = BF16, 8 = int8 codes, 4 = int4 containers
+// (the 4- and 3-bit levels share the container format and kernel).
+inline int wkind_of_bits(int bits) { return bits == 3 ? 4 : bits; }
+inline int chunk_k(int wkind) { return wkind == 16 ? 64 : 128; }
+inline int chunk_bytes_of(int wkind) {
+  return wkind == 16 ? kBf16ChunkBytes : wkind == 8 ? kW8ChunkBytes : kW4ChunkBytes;
+}
+
 // A weight matrix as the GEMM sees it: chunk c of the matrix lives in page
 // (first_chunk + c) / chunks_per_page of its variant image.
 // The pages a matrix spans are also passed inline in the kernel parameters
@@ -52,7 +65,7 @@ struct GemmWeights {
 };
 // Fill the inline page table from a host copy of `pages` (host_pages[p] ==
 // pages[p]); leaves n_inl = 0 when the matrix spans too many pages.
-void gemm_inline_pages(GemmWeights& w, bool w4, const uint64_t* host_pages);
+void gemm_inline_pages(GemmWeights& w, int wkind, const uint64_t* host_pages);
 
 // Stream-K partition of one GEMM: T = tiles * nk k-steps split into C
 // contiguous ranges (one persistent CTA each).  CTA c covers global k-steps
@@ -78,9 +91,9 @@ __host__ __device__ inline int part_slots(const GemmPlanDev& p, int m, int n) {
   return plan_count(p, (m / p.TM) * p.n_tiles + (n >> 7));
 }
 
-GemmPlanDev gemm_plan(int N, int K, int M, int TM, bool w4, int num_sms, size_t part_elems);
+GemmPlanDev gemm_plan(int N, int K, int M, int TM, int wkind, int num_sms, size_t part_elems);
 
-cudaError_t gemm_launch(const GemmWeights& w, bool w4, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
+cudaError_t gemm_launch(const GemmWeights& w, int wkind, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                         float* out, cudaStream_t stream);
 
 // Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
@@ -168,7 +181,8 @@ cudaError_t argmax_launch(const float* part, const GemmPlanDev& plan, int M, int
 cudaError_t gen_weight_launch(uint64_t seed, uint64_t tensor, int64_t n, double scale, double offset,
                               uint16_t* out, cudaStream_t s);
 cudaError_t pack_bf16_launch(const uint16_t* w, int N, int K, uint16_t* out, cudaStream_t s);
-cudaError_t quant_w4_launch(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, cudaStream_t s);
+// g128 quantiser + packer for 8, 4 or 3 bits (W8 chunks / 4-bit containers)
+cudaError_t quant_launch(const uint16_t* w, int N, int K, int bits, uint8_t* out, int8_t* codes_out, cudaStream_t s);
 cudaError_t pack_act_launch(const uint16_t* x, int M, int K, int TM, uint16_t* out, cudaStream_t s);
 cudaError_t fill_kv_launch(const KvGeom& kv, const int32_t* page_list, int n_pages, uint64_t seed,
                            cudaStream_t s);

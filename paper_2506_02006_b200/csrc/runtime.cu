@@ -59,6 +59,12 @@ int guard(F&& f) {
 }
 
 constexpr int kMats = 4;  // qkv, o, gate_up, down
+// Precision variants of a layer, in the reference's Precision order
+// (proj/include/morphsim/toy_model.hpp:26 kFull, kQ8, kQ4, kQ3).
+constexpr int kVariants = 4;
+constexpr int kVariantBits[kVariants] = {16, 8, 4, 3};
+int variant_of(int bits) { return bits == 16 ? 0 : bits == 8 ? 1 : bits == 4 ? 2 : bits == 3 ? 3 : -1; }
+bool valid_bits(int bits) { return variant_of(bits) >= 0; }
 constexpr int kRing = 3;  // staging ring depth (host may run this many steps ahead)
 
 struct MatShape {
@@ -98,14 +104,18 @@ ImageGeom image_geom(const ms_model_desc& d, int bits) {
   g.mat[1] = {d.hidden, d.num_heads * d.head_dim};
   g.mat[2] = {2 * d.ffn, d.hidden};
   g.mat[3] = {d.hidden, d.ffn};
-  g.chunk_bytes = bits == 16 ? 16384 : 8448;
+  const int wk = ms::wkind_of_bits(bits);
+  g.chunk_bytes = ms::chunk_bytes_of(wk);
   const int64_t pb = page_bytes_of(d);
   g.cpp = pb / g.chunk_bytes;
-  if (g.cpp < 1) fail(MS_EVALIDATION, "page smaller than one weight chunk");
+  if (g.cpp < 1) {  // this level cannot be paged at this page size (e.g. Q8 with 16 KiB pages)
+    g.pages = -1;
+    return g;
+  }
   int64_t c = 0;
   for (int i = 0; i < kMats; ++i) {
     g.first_chunk[i] = c;
-    c += (int64_t)(g.mat[i].N / 128) * (g.mat[i].K / (bits == 16 ? 64 : 128));
+    c += (int64_t)(g.mat[i].N / 128) * (g.mat[i].K / ms::chunk_k(wk));
   }
   g.total_chunks = c;
   g.pages = (c + g.cpp - 1) / g.cpp;
@@ -125,10 +135,10 @@ struct FreePage {
 // CUDA graphs: graphs are keyed by the per-layer precision vector instead.
 struct Layer {
   int bits = 16;
-  int slot = 0;  // table of the committed precision (slot_of(bits))
-  uint64_t* d_table[2] = {nullptr, nullptr};
-  uint64_t* h_table[2] = {nullptr, nullptr};  // pinned staging
-  cudaEvent_t table_ev[2] = {nullptr, nullptr};  // last H2D copy out of h_table[slot] (host may rewrite after it)
+  int slot = 0;  // table of the committed precision (variant_of(bits))
+  uint64_t* d_table[kVariants] = {};
+  uint64_t* h_table[kVariants] = {};  // pinned staging
+  cudaEvent_t table_ev[kVariants] = {};  // last H2D copy out of h_table[slot] (host may rewrite after it)
   std::vector<int32_t> pages;
   cudaEvent_t last_release = nullptr;
   // in-flight swap
@@ -138,11 +148,11 @@ struct Layer {
   std::vector<int32_t> new_pages;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
   // pinned host variant store
-  uint8_t* host_img[2] = {nullptr, nullptr};  // [0] bf16, [1] w4
+  uint8_t* host_img[kVariants] = {};  // by variant_of(bits)
   // caller-registered images (ms_variant_register): not freed here; `ready`
   // = the memory already holds the packed image (another process built it)
-  bool host_registered[2] = {false, false};
-  bool host_ready[2] = {false, false};
+  bool host_registered[kVariants] = {};
+  bool host_ready[kVariants] = {};
 };
 
 struct Staging {  // one slot of the per-step H2D ring
@@ -165,7 +175,8 @@ struct ms_ctx {
   int device = 0;
   int num_sms = 148;
   int64_t page_bytes = 0;
-  ImageGeom geom16, geom4;
+  ImageGeom geom[kVariants];                  // by variant_of(bits)
+  bool variant_on[kVariants] = {true, false, true, false};  // stores built at weight finalisation (ms_variant_enable)
   cudaStream_t compute = nullptr, copy = nullptr;
   char* arena = nullptr;
   ms::KvGeom kv{};
@@ -307,8 +318,7 @@ cudaEvent_t compute_fence(ms_ctx* c) {
   return e;
 }
 
-const ImageGeom& geom_of(ms_ctx* c, int bits) { return bits == 16 ? c->geom16 : c->geom4; }
-int slot_of(int bits) { return bits == 16 ? 0 : 1; }
+const ImageGeom& geom_of(ms_ctx* c, int bits) { return c->geom[variant_of(bits)]; }
 
 // Write the page-address table of `pages` into layer slot `slot` (on stream s).
 void write_table(ms_ctx* c, Layer& L, int slot, const std::vector<int32_t>& pages, cudaStream_t s) {
@@ -348,7 +358,7 @@ void upload_image(ms_ctx* c, const uint8_t* img, const ImageGeom& g, const std::
 
 // Scatter a contiguous packed matrix (device) into a pinned host image.
 void scatter_to_image(ms_ctx* c, const ImageGeom& g, int mat, const uint8_t* packed_dev, uint8_t* img) {
-  const int64_t n = (int64_t)(g.mat[mat].N / 128) * (g.mat[mat].K / (g.bits == 16 ? 64 : 128));
+  const int64_t n = (int64_t)(g.mat[mat].N / 128) * (g.mat[mat].K / ms::chunk_k(ms::wkind_of_bits(g.bits)));
   int64_t ci = 0;
   while (ci < n) {
     const int64_t c_abs = g.first_chunk[mat] + ci;
@@ -364,8 +374,9 @@ int round16(int m) { return (m + 15) / 16 * 16; }
 
 void build_images(ms_ctx* c, int l, uint16_t* w_dev[kMats], uint8_t* tmp) {
   Layer& L = c->layers[l];
-  for (int bi = 0; bi < 2; ++bi) {
-    const ImageGeom& g = bi == 0 ? c->geom16 : c->geom4;
+  for (int bi = 0; bi < kVariants; ++bi) {
+    if (!c->variant_on[bi]) continue;
+    const ImageGeom& g = c->geom[bi];
     if (L.host_ready[bi]) continue;  // pre-packed image registered by the caller
     if (!L.host_img[bi]) {
       CK(cudaHostAlloc(&L.host_img[bi], g.pages * c->page_bytes, cudaHostAllocPortable));
@@ -375,7 +386,7 @@ void build_images(ms_ctx* c, int l, uint16_t* w_dev[kMats], uint8_t* tmp) {
       if (bi == 0)
         CK(ms::pack_bf16_launch(w_dev[m], g.mat[m].N, g.mat[m].K, reinterpret_cast<uint16_t*>(tmp), c->compute));
       else
-        CK(ms::quant_w4_launch(w_dev[m], g.mat[m].N, g.mat[m].K, tmp, nullptr, c->compute));
+        CK(ms::quant_launch(w_dev[m], g.mat[m].N, g.mat[m].K, g.bits, tmp, nullptr, c->compute));
       scatter_to_image(c, g, m, tmp, L.host_img[bi]);
       CK(cudaStreamSynchronize(c->compute));  // tmp reused
     }
@@ -386,10 +397,10 @@ void make_resident_bf16(ms_ctx* c) {
   for (int l = 0; l < c->desc.num_layers; ++l) {
     Layer& L = c->layers[l];
     if (!L.pages.empty()) give_pages(c, L.pages, nullptr);
-    L.pages = take_pages(c, c->geom16.pages, c->compute);
+    L.pages = take_pages(c, c->geom[0].pages, c->compute);
     L.bits = 16;
-    L.slot = slot_of(16);
-    upload_image(c, L.host_img[0], c->geom16, L.pages, c->compute);
+    L.slot = 0;
+    upload_image(c, L.host_img[0], c->geom[0], L.pages, c->compute);
     write_table(c, L, L.slot, L.pages, c->compute);
   }
   CK(cudaStreamSynchronize(c->compute));
@@ -405,12 +416,13 @@ ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
   return ms::GemmWeights{L.d_table[L.slot], g.first_chunk[mat], g.cpp, g.mat[mat].N, g.mat[mat].K};
 }
 
-// W4A16 layers at every M run the fused kernel (int4 -> bf16 dequantised into
-// TMEM in the GEMM's staging path); no dequantised copy of a matrix exists.
-ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, bool w4, int M, int TM) {
+// Quantised layers (Q8 / Q4 / Q3) at every M run the fused kernel (codes ->
+// bf16 dequantised into TMEM in the GEMM's staging path); no dequantised copy
+// of a matrix exists.  wkind: 16 BF16, 8 int8 codes, 4 int4 containers.
+ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, int wkind, int M, int TM) {
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
-  const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, w4, c->num_sms, c->part_elems);
-  CK(ms::gemm_launch(w, w4, c->x, M, TM, plan, c->part, c->compute));
+  const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, wkind, c->num_sms, c->part_elems);
+  CK(ms::gemm_launch(w, wkind, c->x, M, TM, plan, c->part, c->compute));
   c->launches += 1;
   return plan;
 }
@@ -493,8 +505,9 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     if (c->tracing)  // residual stream entering layer l
       CK(cudaMemcpyAsync(c->trace_h + (size_t)l * M * d, c->h, (size_t)M * d * sizeof(float), cudaMemcpyDeviceToDevice,
                          c->compute));
-    const bool w4 = c->layers[l].bits == 4;
-    ms::GemmPlanDev s = gemm(c, mat_weights(c, l, 0), w4, M, TM);
+    const int wk = ms::wkind_of_bits(c->layers[l].bits);
+    const bool w4 = wk != 16;  // profile category: quantised layer
+    ms::GemmPlanDev s = gemm(c, mat_weights(c, l, 0), wk, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_QKV_W4 : MS_PK_GEMM_QKV);
     prof_mark(c);
     if (d_page_row != nullptr) {
@@ -554,17 +567,17 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     const uint16_t* nw = last ? c->normf : c->norms + ((size_t)(l + 1) * 2) * d;
     const int tm_out = last ? round16(M - final_row_begin) > 256 ? 256 : round16(M - final_row_begin) : TM;
     const int row_begin = last ? final_row_begin : 0;
-    s = gemm(c, mat_weights(c, l, 1), w4, M, TM);
+    s = gemm(c, mat_weights(c, l, 1), wk, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_O_W4 : MS_PK_GEMM_O);
     CK(ms::residual_norm_launch(c->part, s, M, d, c->h, n2, D.rms_eps, c->x, TM, c->compute));
     c->launches += 1;
     pk_mark(c, MS_PK_NORM);
-    s = gemm(c, mat_weights(c, l, 2), w4, M, TM);
+    s = gemm(c, mat_weights(c, l, 2), wk, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_GU_W4 : MS_PK_GEMM_GU);
     CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
     c->launches += 1;
     pk_mark(c, MS_PK_SILU);
-    s = gemm(c, mat_weights(c, l, 3), w4, M, TM);
+    s = gemm(c, mat_weights(c, l, 3), wk, M, TM);
     pk_mark(c, w4 ? MS_PK_GEMM_DOWN_W4 : MS_PK_GEMM_DOWN);
     CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out, row_begin, c->compute));
     c->launches += 1;
@@ -577,8 +590,8 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
   const int TMo = round16(Mo) > 256 ? 256 : round16(Mo);
   ms::GemmWeights lw{c->lm_table, 0, (int64_t)1 << 40, D.vocab, d};
   const uint64_t lm_addr = (uint64_t)c->lm_packed;
-  ms::gemm_inline_pages(lw, false, &lm_addr);
-  const ms::GemmPlanDev s = gemm(c, lw, false, Mo, TMo);
+  ms::gemm_inline_pages(lw, 16, &lm_addr);
+  const ms::GemmPlanDev s = gemm(c, lw, 16, Mo, TMo);
   pk_mark(c, MS_PK_LM_HEAD);
   CK(ms::argmax_launch(c->part, s, Mo, D.vocab, want_logits ? c->logits : nullptr, c->next, c->hist,
                        d_slot + final_row_begin, d_pos + final_row_begin, c->hist_len, c->compute, c->am_key,
@@ -654,8 +667,9 @@ int64_t ms_page_bytes(const ms_model_desc* desc) { return desc ? page_bytes_of(*
 int64_t ms_layer_pages(const ms_model_desc* desc, int bits) {
   int64_t out = -1;
   guard([&] {
-    if (!desc || (bits != 16 && bits != 4)) fail(MS_EVALIDATION, "bits must be 16 or 4");
+    if (!desc || !valid_bits(bits)) fail(MS_EVALIDATION, "bits must be 16, 8, 4 or 3");
     out = image_geom(*desc, bits).pages;
+    if (out < 0) fail(MS_EVALIDATION, "page smaller than one weight chunk at this precision");
   });
   return out;
 }
@@ -677,8 +691,9 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       c->num_sms = prop.multiProcessorCount;
       if (prop.major != 10) fail(MS_ERUNTIME, "libmorphserve is built for sm_100a (B200) only");
       c->page_bytes = page_bytes_of(*desc);
-      c->geom16 = image_geom(*desc, 16);
-      c->geom4 = image_geom(*desc, 4);
+      for (int v = 0; v < kVariants; ++v) c->geom[v] = image_geom(*desc, kVariantBits[v]);
+      for (int v : {0, 2})  // BF16 and Q4 are always built
+        if (c->geom[v].pages < 0) fail(MS_EVALIDATION, "page smaller than one weight chunk");
       CK(cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
       CK(cudaMalloc(&c->arena, (size_t)desc->arena_pages * c->page_bytes));
@@ -687,9 +702,10 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       c->free_pages.reserve(desc->arena_pages);
       for (int64_t p = desc->arena_pages - 1; p >= 0; --p) c->free_pages.push_back({(int32_t)p, nullptr});
       c->layers.resize(desc->num_layers);
-      const int64_t max_img_pages = std::max(c->geom16.pages, c->geom4.pages);
+      int64_t max_img_pages = 0;
+      for (int v = 0; v < kVariants; ++v) max_img_pages = std::max(max_img_pages, c->geom[v].pages);
       for (auto& L : c->layers) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kVariants; ++s) {
           CK(cudaMalloc(&L.d_table[s], max_img_pages * sizeof(uint64_t)));
           CK(cudaHostAlloc(&L.h_table[s], max_img_pages * sizeof(uint64_t), cudaHostAllocDefault));
         }
@@ -760,7 +776,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->compute) cudaStreamSynchronize(c->compute);
   if (c->copy) cudaStreamSynchronize(c->copy);
   for (auto& L : c->layers) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kVariants; ++s) {
       cudaFree(L.d_table[s]);
       cudaFreeHost(L.h_table[s]);
       if (L.host_registered[s]) cudaHostUnregister(L.host_img[s]);
@@ -925,15 +941,26 @@ int ms_weights_finalize(ms_ctx* c) {
 }
 
 int64_t ms_variant_bytes(ms_ctx* c, int bits) {
-  return (bits == 16 ? c->geom16.pages : c->geom4.pages) * c->page_bytes;
+  if (!c || !valid_bits(bits) || c->geom[variant_of(bits)].pages < 0) return -1;
+  return c->geom[variant_of(bits)].pages * c->page_bytes;
+}
+
+int ms_variant_enable(ms_ctx* c, int bits) {
+  return guard([&] {
+    if (!valid_bits(bits)) fail(MS_EVALIDATION, "variant enable: bits must be 16, 8, 4 or 3");
+    if (c->weights_ready) fail(MS_EVALIDATION, "variant enable: weights already finalized");
+    if (c->geom[variant_of(bits)].pages < 0)
+      fail(MS_EVALIDATION, "variant enable: page smaller than one " + std::to_string(bits) + "-bit weight chunk");
+    c->variant_on[variant_of(bits)] = true;
+  });
 }
 
 int ms_variant_export(ms_ctx* c, int layer, int bits, void* host_out, int64_t bytes) {
   return guard([&] {
     if (layer < 0 || layer >= c->desc.num_layers) fail(MS_EVALIDATION, "layer out of range");
-    if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "bits must be 16 or 4");
+    if (!valid_bits(bits)) fail(MS_EVALIDATION, "bits must be 16, 8, 4 or 3");
     const Layer& L = c->layers[layer];
-    const uint8_t* img = L.host_img[bits == 16 ? 0 : 1];
+    const uint8_t* img = L.host_img[variant_of(bits)];
     if (!img) fail(MS_EVALIDATION, "variant store not built");
     const int64_t n = std::min<int64_t>(bytes, ms_variant_bytes(c, bits));
     std::memcpy(host_out, img, (size_t)n);
@@ -943,12 +970,14 @@ int ms_variant_export(ms_ctx* c, int layer, int bits, void* host_out, int64_t by
 int ms_variant_register(ms_ctx* c, int layer, int bits, void* host, int64_t bytes, int prefilled) {
   return guard([&] {
     if (layer < 0 || layer >= c->desc.num_layers) fail(MS_EVALIDATION, "variant register: layer out of range");
-    if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "variant register: bits must be 16 or 4");
+    if (!valid_bits(bits)) fail(MS_EVALIDATION, "variant register: bits must be 16, 8, 4 or 3");
     if (!host || bytes < ms_variant_bytes(c, bits)) fail(MS_EVALIDATION, "variant register: buffer too small");
     if (c->weights_ready) fail(MS_EVALIDATION, "variant register: weights already finalized");
     Layer& L = c->layers[layer];
-    const int bi = bits == 16 ? 0 : 1;
+    const int bi = variant_of(bits);
+    if (c->geom[bi].pages < 0) fail(MS_EVALIDATION, "variant register: page smaller than one weight chunk");
     if (L.host_img[bi]) fail(MS_EVALIDATION, "variant register: image already present");
+    c->variant_on[bi] = true;
     CK(cudaSetDevice(c->device));
     const cudaError_t e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterPortable);
     if (e == cudaErrorHostMemoryAlreadyRegistered) {
@@ -968,9 +997,11 @@ int ms_swap_begin(ms_ctx* c, int layer, int bits, uint64_t* ticket) {
     if (layer < 0 || layer >= c->desc.num_layers) fail(MS_EVALIDATION, "begin_swap: layer out of range");
     Layer& L = c->layers[layer];
     if (L.in_flight) fail(MS_EVALIDATION, "begin_swap: swap already in flight on layer");
-    if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "begin_swap: bits must be 16 or 4");
+    if (!valid_bits(bits)) fail(MS_EVALIDATION, "begin_swap: bits must be 16, 8, 4 or 3");
     if (L.bits == bits) fail(MS_EVALIDATION, "begin_swap: layer already at target precision");
     if (!c->weights_ready) fail(MS_EVALIDATION, "weights not initialised");
+    if (!L.host_img[variant_of(bits)])
+      fail(MS_EVALIDATION, "begin_swap: no " + std::to_string(bits) + "-bit variant store (ms_variant_enable)");
     const ImageGeom& g = geom_of(c, bits);
     CK(cudaSetDevice(c->device));
     // the inactive table slot may still be read by steps launched before the
@@ -978,8 +1009,8 @@ int ms_swap_begin(ms_ctx* c, int layer, int bits, uint64_t* ticket) {
     if (L.last_release) CK(cudaStreamWaitEvent(c->copy, L.last_release, 0));
     L.new_pages = take_pages(c, g.pages, c->copy);
     CK(cudaEventRecord(L.ev_start, c->copy));
-    write_table(c, L, slot_of(bits), L.new_pages, c->copy);
-    upload_image(c, L.host_img[bits == 16 ? 0 : 1], g, L.new_pages, c->copy);
+    write_table(c, L, variant_of(bits), L.new_pages, c->copy);
+    upload_image(c, L.host_img[variant_of(bits)], g, L.new_pages, c->copy);
     CK(cudaEventRecord(L.ev_done, c->copy));
     L.in_flight = true;
     L.to_bits = bits;
@@ -1034,7 +1065,7 @@ int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
     L.pages = std::move(L.new_pages);
     L.new_pages.clear();
     L.bits = L.to_bits;
-    L.slot = slot_of(L.bits);
+    L.slot = variant_of(L.bits);
     L.in_flight = false;
     L.last_release = fence;
     if (pages_freed) *pages_freed = freed;
@@ -1471,10 +1502,18 @@ int ms_k_pack_bf16(const uint16_t* w, int N, int K, uint16_t* out, void* stream)
     CK(ms::pack_bf16_launch(w, N, K, out, (cudaStream_t)stream));
   });
 }
+int ms_k_quant(int bits, const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, void* stream) {
+  return guard([&] {
+    if (bits != 8 && bits != 4 && bits != 3) fail(MS_EVALIDATION, "quant: bits must be 8, 4 or 3");
+    if (N % 128 || K % 128) fail(MS_EVALIDATION, "quant: N%128, K%128");
+    CK(ms::quant_launch(w, N, K, bits, out, codes_out, (cudaStream_t)stream));
+  });
+}
+
 int ms_k_quant_w4(const uint16_t* w, int N, int K, uint8_t* out, int8_t* codes_out, void* stream) {
   return guard([&] {
     if (N % 128 || K % 128) fail(MS_EVALIDATION, "quant_w4: N%128, K%128");
-    CK(ms::quant_w4_launch(w, N, K, out, codes_out, (cudaStream_t)stream));
+    CK(ms::quant_launch(w, N, K, 4, out, codes_out, (cudaStream_t)stream));
   });
 }
 int ms_k_pack_act(const uint16_t* x, int M, int K, int TM, uint16_t* out, void* stream) {
@@ -1486,7 +1525,7 @@ int ms_k_pack_act(const uint16_t* x, int M, int K, int TM, uint16_t* out, void* 
 int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_packed, int M, int TM, int splits,
               float* out, int* splits_used, void* stream) {
   return guard([&] {
-    if (bits != 16 && bits != 4) fail(MS_EVALIDATION, "gemm: bits must be 16 or 4");
+    if (!valid_bits(bits)) fail(MS_EVALIDATION, "gemm: bits must be 16, 8, 4 or 3");
     if (N % 128 || K % 128 || M < 1 || TM % 16 || TM < 16 || TM > 256) fail(MS_EVALIDATION, "gemm: bad shape");
     // one-entry page table per contiguous packed matrix (up to 1024 distinct
     // matrices; written once, so later calls may be graph-captured)
@@ -1503,15 +1542,15 @@ int ms_k_gemm(int bits, const void* w_packed, int N, int K, const uint16_t* x_pa
     }
     uint64_t* table = tables + idx;
     ms::GemmWeights w{table, 0, (int64_t)1 << 40, N, K};
-    const bool w4 = bits == 4;
-    ms::gemm_inline_pages(w, w4, &addr);
+    const int wk = ms::wkind_of_bits(bits);
+    ms::gemm_inline_pages(w, wk, &addr);
     int dev = 0, sms = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     // `splits` > 0 caps the persistent CTA count (exercises other partitions)
     const int ctas = splits > 0 ? std::min(splits, sms) : sms;
-    ms::GemmPlanDev plan = ms::gemm_plan(N, K, M, TM, w4, ctas, (size_t)16 * M * N);
-    CK(ms::gemm_launch(w, w4, x_packed, M, TM, plan, out, (cudaStream_t)stream));
+    ms::GemmPlanDev plan = ms::gemm_plan(N, K, M, TM, wk, ctas, (size_t)16 * M * N);
+    CK(ms::gemm_launch(w, wk, x_packed, M, TM, plan, out, (cudaStream_t)stream));
     // slots actually written per tile are part_slots() <= plan.slots; slots a
     // tile does not use are left untouched (callers pass a zeroed buffer)
     if (splits_used) *splits_used = plan.aligned ? 1 : plan.slots;

@@ -51,7 +51,7 @@ class DeviceModel:
     """One device context: arena, layer table, variant store, streams, steps."""
 
     def __init__(self, shape: dict, *, device: int = 0, max_batch: int = 64, max_prefill_tokens: int = 2048,
-                 max_pos: int = 4096, arena_pages: int, eps: float = 1e-5):
+                 max_pos: int = 4096, arena_pages: int, eps: float = 1e-5, variants=(16, 4)):
         self.shape = dict(shape)
         self.desc = model_desc(shape, max_batch=max_batch, max_prefill_tokens=max_prefill_tokens,
                                max_pos=max_pos, arena_pages=arena_pages, eps=eps)
@@ -61,6 +61,9 @@ class DeviceModel:
         self.h = h
         self.max_blocks = (max_pos + 15) // 16
         self.page_bytes = self.lib.ms_page_bytes(C.byref(self.desc))
+        # precision levels of the variant store (BF16 and Q4 always; Q8 / Q3 on request)
+        for bits in variants:
+            self.variant_enable(bits)
 
     # -- lifecycle
     def close(self):
@@ -93,6 +96,10 @@ class DeviceModel:
 
     def finalize(self):
         N.check(self.lib.ms_weights_finalize(self.h))
+
+    def variant_enable(self, bits: int):
+        """Add the `bits` level (16, 8, 4, 3) to the pinned variant store (ms_variant_enable)."""
+        N.check(self.lib.ms_variant_enable(self.h, bits))
 
     def variant_bytes(self, bits: int) -> int:
         return int(self.lib.ms_variant_bytes(self.h, bits))

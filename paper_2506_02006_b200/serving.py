@@ -29,7 +29,7 @@ def device_config(dev: DeviceModel, workload: dict, *, budget_gib: float = 24.0,
                   slo_ms: float = 2000.0, seed: int = 7, controller: dict | None = None) -> dict:
     shape = dev.shape
     pb = dev.page_bytes
-    p16, p4 = layer_pages(shape, 16), layer_pages(shape, 4)
+    p16, p8, p4, p3 = (layer_pages(shape, b) for b in (16, 8, 4, 3))
     budget = int(budget_gib * GIB)
     if budget // pb > dev.desc.arena_pages:
         raise ValueError(f"budget {budget_gib} GiB exceeds the device arena ({dev.desc.arena_pages} pages)")
@@ -37,7 +37,7 @@ def device_config(dev: DeviceModel, workload: dict, *, budget_gib: float = 24.0,
         "seed": seed,
         "slo_ms": slo_ms,
         "model": {"num_layers": shape["L"],
-                  "layer_bytes": {"full": p16 * pb, "q8": p4 * pb, "q4": p4 * pb, "q3": p4 * pb}},
+                  "layer_bytes": {"full": p16 * pb, "q8": p8 * pb, "q4": p4 * pb, "q3": p3 * pb}},
         "kv": {"block_tokens": 16, "block_bytes": pb, "static_capacity_blocks": 0},
         "budget": {"device_bytes": budget, "reserve_bytes": int(reserve_gib * GIB)},
         "toy": {"num_layers": shape["L"]},

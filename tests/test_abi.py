@@ -38,8 +38,12 @@ def test_no_device_fails_loudly():
     if torch.cuda.is_available():
         pytest.skip("a GPU is present")
     from paper_2506_02006_b200 import _native as N
-    from paper_2506_02006_b200.device import DeviceModel, TINY, layer_pages
+    from paper_2506_02006_b200.device import DeviceModel, LLAMA2_7B, TINY, layer_pages
     assert layer_pages(TINY, 16) == 48 and layer_pages(TINY, 4) == 16
+    # Q8 images: 16640-B chunks; Q3 shares the 4-bit container image
+    # (32 KiB tiny pages hold one 16640-B chunk each, so tiny Q8 saves nothing)
+    assert layer_pages(TINY, 8) == 48 and layer_pages(TINY, 3) == layer_pages(TINY, 4)
+    assert layer_pages(LLAMA2_7B, 8) == 25 and layer_pages(LLAMA2_7B, 3) == 13
     with pytest.raises(N.MsError):
         DeviceModel(TINY, arena_pages=64)
 

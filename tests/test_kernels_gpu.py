@@ -52,21 +52,25 @@ def test_pack_bf16_bit_exact(N_, K):
     assert np.array_equal(to_np_u16(out), O.pack_bf16(w))
 
 
+@pytest.mark.parametrize("bits", [4, 8, 3])
 @pytest.mark.parametrize("N_,K", [(128, 128), (256, 768), (512, 256)])
-def test_quant_w4_codes_and_image_bit_exact(N_, K):
+def test_quant_codes_and_image_bit_exact(N_, K, bits):
+    """g128 quantiser + packer at every precision level (Q4 / Q8 / Q3) against
+    the oracle restatement of quantize_weights (toy_model.cpp:47-60)."""
     N = _native()
     w = O.gen_weight(11, 6, N_ * K, 0.02).reshape(N_, K).copy()
     w[3, :128] = 0          # all-zero group -> scale 1, codes 0 (toy_model.cpp:43,53)
     w[5, 128 - 1] = w[5, 0]  # ties are fine, exercise equal maxima
     dw = dev_u16(w)
-    img = torch.empty((N_ // 128) * (K // 128) * 8448, dtype=torch.uint8, device="cuda")
+    chunk = 16640 if bits == 8 else 8448
+    img = torch.empty((N_ // 128) * (K // 128) * chunk, dtype=torch.uint8, device="cuda")
     codes = torch.empty(N_ * K, dtype=torch.int8, device="cuda")
-    N.check(N.lib().ms_k_quant_w4(C.c_void_p(dw.data_ptr()), N_, K, C.c_void_p(img.data_ptr()),
-                                  C.c_void_p(codes.data_ptr()), stream()))
+    N.check(N.lib().ms_k_quant(bits, C.c_void_p(dw.data_ptr()), N_, K, C.c_void_p(img.data_ptr()),
+                               C.c_void_p(codes.data_ptr()), stream()))
     torch.cuda.synchronize()
-    rc, _, rs = O.quantize_groups(w)
+    rc, _, rs = O.quantize_groups(w, bits=bits)
     assert np.array_equal(codes.cpu().numpy().reshape(N_, K), rc)
-    assert np.array_equal(img.cpu().numpy(), O.pack_w4(rc, rs))
+    assert np.array_equal(img.cpu().numpy(), O.pack_quant(rc, rs, bits))
 
 
 def _run_gemm(bits, W, X, TM, splits=0):
@@ -79,8 +83,10 @@ def _run_gemm(bits, W, X, TM, splits=0):
         wp = torch.empty(Nn * K, dtype=torch.int16, device="cuda")
         N.check(N.lib().ms_k_pack_bf16(C.c_void_p(dw.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), stream()))
     else:
-        wp = torch.empty((Nn // 128) * (K // 128) * 8448, dtype=torch.uint8, device="cuda")
-        N.check(N.lib().ms_k_quant_w4(C.c_void_p(dw.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), None, stream()))
+        chunk = 16640 if bits == 8 else 8448
+        wp = torch.empty((Nn // 128) * (K // 128) * chunk, dtype=torch.uint8, device="cuda")
+        N.check(N.lib().ms_k_quant(bits, C.c_void_p(dw.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), None,
+                                   stream()))
     m_tiles = (M + TM - 1) // TM
     xp = torch.zeros(m_tiles * TM * K, dtype=torch.int16, device="cuda")
     dx = dev_u16(X)
@@ -118,14 +124,30 @@ def test_gemm_bf16(Nn, K, M, TM, splits):
     # odd K-group counts with stream-K ranges crossing tiles, TM 128
     (1280, 1152, 48, 48, 7), (512, 512, 128, 128, 3), (1280, 640, 33, 48, 0), (640, 512, 64, 64, 3)])
 def test_gemm_w4(Nn, K, M, TM, splits):
+    _check_quant_gemm(4, Nn, K, M, TM, splits)
+
+
+def _check_quant_gemm(bits, Nn, K, M, TM, splits):
     W = O.gen_weight(22, 1, Nn * K, 1 / np.sqrt(K)).reshape(Nn, K)
     X = O.gen_weight(22, 2, M * K, 1.0).reshape(M, K)
-    got, _ = _run_gemm(4, W, X, TM, splits)
-    codes, _, s16 = O.quantize_groups(W)
-    Wq = O.dequant_w4(codes, s16)
+    got, _ = _run_gemm(bits, W, X, TM, splits)
+    codes, _, s16 = O.quantize_groups(W, bits=bits)
+    Wq = O.dequant_w4(codes, s16)  # bf16(code * scale), every level
     ref = O.gemm_bf16(Wq, X)
     bound = 1e-5 * (np.abs(O.bf16_to_f32(X)) @ np.abs(O.bf16_to_f32(Wq)).T) + 1e-6
     assert np.all(np.abs(got - ref) <= bound), np.max(np.abs(got - ref) / bound)
+
+
+@pytest.mark.parametrize("bits", [8, 3])
+@pytest.mark.parametrize("Nn,K,M,TM,splits", [
+    (128, 128, 1, 16, 1), (512, 1024, 64, 64, 0), (768, 512, 100, 112, 5), (1280, 1152, 48, 48, 7),
+    (512, 256, 2500, 256, 3), (1024, 1024, 600, 256, 0),
+    # Llama-2-7B decode shapes (o / down)
+    (4096, 4096, 64, 64, 0), (4096, 11008, 64, 64, 0)])
+def test_gemm_q8_q3(bits, Nn, K, M, TM, splits):
+    """Q8 (byte codes, fp32 magic conversion) and Q3 (4-bit containers) through
+    the same tcgen05 kernel family, same bf16(code * scale) contract."""
+    _check_quant_gemm(bits, Nn, K, M, TM, splits)
 
 
 @pytest.mark.parametrize("H,KVH,hd,ctxs,splits", [

@@ -180,3 +180,71 @@ def test_long_prefill_w4_layers_dequant_path():
         ref.close()
     finally:
         m.close()
+
+
+def test_multilevel_variants_decode_matches_oracle():
+    """Every precision level of the reference (toy_model.hpp:26 kFull / kQ8 /
+    kQ4 / kQ3) as a real device variant: Q8 and Q3 stores built next to BF16
+    and Q4, the Q8 image bit-identical to the oracle packing, and decode parity
+    while layers move between levels (including quantised -> quantised swaps)
+    at token boundaries."""
+    from paper_2506_02006_b200.device import DeviceModel, layer_pages, page_bytes
+    m = DeviceModel(TINY, max_batch=4, max_prefill_tokens=64, max_pos=256, arena_pages=512,
+                    variants=(16, 8, 4, 3))
+    ref = O.RefModel(dict(TINY, max_pos=256), 7)
+    try:
+        m.weights_synthetic(7)
+        # Q8 image of layer 1's qkv: one 16640-B chunk per 32 KiB tiny page
+        pb = page_bytes(TINY)
+        qkv = ref.tensor(1, O.W_QKV, (512, 256))
+        codes, _, s16 = O.quantize_groups(qkv, bits=8)
+        chunks = O.pack_w8(codes, s16).reshape(-1, 16640)
+        img8 = m.variant_image(1, 8)
+        for ci in range(chunks.shape[0]):
+            assert np.array_equal(img8[ci * pb: ci * pb + 16640], chunks[ci])
+        c3, _, s3 = O.quantize_groups(qkv, bits=3)
+        img3 = m.variant_image(1, 3)
+        ch3 = O.pack_w4(c3, s3).reshape(-1, 8448)
+        for ci in range(ch3.shape[0]):
+            p, slot = divmod(ci, 3)
+            assert np.array_equal(img3[p * pb + slot * 8448: p * pb + (slot + 1) * 8448], ch3[ci])
+
+        B, P = 2, 16
+        rng = np.random.default_rng(5)
+        prompts = rng.integers(0, TINY["V"], size=(B, P)).astype(np.int32)
+        m.hist_reserve(B, 256)
+        m.kv_attach(0, B * 16)
+        table = np.arange(B * 16, dtype=np.int64).reshape(B, 16)
+        seqs = [ref.new_seq(256) for _ in range(B)]
+        toks = []
+        for b in range(B):
+            m.hist_write(b, 0, prompts[b])
+            t, lg = m.prefill(b, P, table[b], want_logits=True)
+            rt, rl = ref.prefill(seqs[b], prompts[b])
+            _check_logits(lg, rl)
+            toks.append(t)
+        toks = np.array(toks, np.int32)
+        pos = np.full(B, P, np.int32)
+        plan = {2: [(0, 8), (1, 3)], 6: [(2, 4), (0, 3)], 10: [(1, 8), (3, 8)], 14: [(0, 16), (1, 4)]}
+        for step in range(18):
+            for layer, bits in plan.get(step, []):
+                before = m.free_pages()
+                old = m.layer_bits(layer)
+                t = m.swap_begin(layer, bits)
+                m.swap_wait(t)
+                freed = m.swap_commit(t)
+                assert freed == layer_pages(TINY, old)
+                assert m.free_pages() == before - layer_pages(TINY, bits) + freed
+                assert m.layer_bits(layer) == bits
+                ref.set_precision(layer, bits)
+            got, lg = m.decode(np.arange(B), pos, table, want_logits=True)
+            rt, rl = ref.forward(seqs, toks)
+            for b in range(B):
+                _check_logits(lg[b], rl[b])
+                if got[b] != rt[b]:
+                    assert rl[b][rt[b]] - rl[b][got[b]] <= 2e-3 * np.max(np.abs(rl[b])), (step, b)
+            toks = got  # the oracle follows the device's tokens (held in the device history)
+            pos += 1
+    finally:
+        ref.close()
+        m.close()

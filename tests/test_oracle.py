@@ -38,14 +38,22 @@ def test_quantizer_kats_and_bounds():
 
 
 @pytest.mark.skipif(not O.have_ref_core(), reason="oracle/_ref not built")
-def test_quantizer_matches_live_reference():
+@pytest.mark.parametrize("bits", [8, 4, 3])
+def test_quantizer_matches_live_reference(bits):
+    """Every precision level of the reference (toy_model.hpp:26 kQ8/kQ4/kQ3):
+    the g128 restatement reproduces quantize_weights(rows, bits) exactly
+    (codes recovered from the reference's dequantised rows, and the products)."""
     ref = O.ref_core()
-    rng = np.random.default_rng(99)
+    rng = np.random.default_rng(99 + bits)
     w = O.f32_to_bf16((rng.standard_normal((16, 256)) * 0.02).astype(np.float32))
-    codes, s64, _ = O.quantize_groups(w)
+    w[3, :128] = 0  # zero group: scale 1, codes 0
+    codes, s64, _ = O.quantize_groups(w, bits=bits)
     rows = O.bf16_to_f32(w).astype(np.float64).reshape(32, 128)
-    q = np.array(ref.quantize_weights(rows.tolist(), 4))
+    q = np.array(ref.quantize_weights(rows.tolist(), bits))
     assert np.array_equal(np.round(q / s64.reshape(32, 1)).astype(np.int8).reshape(16, 256), codes)
+    assert np.array_equal(q, codes.reshape(32, 128).astype(np.float64) * s64.reshape(32, 1))
+    qmax = (1 << (bits - 1)) - 1
+    assert codes.min() >= -qmax and codes.max() <= qmax
 
 
 def test_generator_golden():
@@ -71,6 +79,23 @@ def test_pack_layouts_roundtrip():
             dec = nib.transpose(1, 0, 2, 3).reshape(128, 128)  # [row][j*32 + w*8 + e]
             assert np.array_equal(dec, codes[nt * 128:(nt + 1) * 128, g * 128:(g + 1) * 128])
             assert np.array_equal(chunk[8192:].view(np.uint16), s16[nt * 128:(nt + 1) * 128, g])
+
+
+def test_pack_w8_layout():
+    rng = np.random.default_rng(1)
+    N, K = 256, 384
+    codes, _, s16 = O.quantize_groups(O.f32_to_bf16(rng.uniform(-1, 1, (N, K)).astype(np.float32)), bits=8)
+    img = O.pack_w8(codes, s16).reshape(N // 128, K // 128, 16640)
+    for nt in range(N // 128):
+        for g in range(K // 128):
+            chunk = img[nt, g]
+            b = chunk[:16384].reshape(8, 128, 16).astype(np.int16) - 128  # [j][row][e]
+            dec = b.transpose(1, 0, 2).reshape(128, 128)
+            assert np.array_equal(dec, codes[nt * 128:(nt + 1) * 128, g * 128:(g + 1) * 128])
+            assert np.array_equal(chunk[16384:].view(np.uint16), s16[nt * 128:(nt + 1) * 128, g])
+    # Q3 codes use the 4-bit container layout
+    c3, _, s3 = O.quantize_groups(O.f32_to_bf16(rng.uniform(-1, 1, (N, K)).astype(np.float32)), bits=3)
+    assert np.array_equal(O.pack_quant(c3, s3, 3), O.pack_w4(c3, s3))
 
 
 def test_oracle_forward_deterministic_and_prefill_equals_decode():

@@ -60,9 +60,10 @@ def gemm(bits, Nn, K, M, TM, ctas=0):
         N.check(L.ms_k_pack_bf16(C.c_void_p(w.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), stream()))
         wbytes = Nn * K * 2
     else:
-        wp = torch.empty((Nn // 128) * (K // 128) * 8448, dtype=torch.uint8, device="cuda")
-        N.check(L.ms_k_quant_w4(C.c_void_p(w.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), None, stream()))
-        wbytes = Nn * K // 2 + Nn * K // 128 * 2
+        chunk = 16640 if bits == 8 else 8448
+        wp = torch.empty((Nn // 128) * (K // 128) * chunk, dtype=torch.uint8, device="cuda")
+        N.check(L.ms_k_quant(bits, C.c_void_p(w.data_ptr()), Nn, K, C.c_void_p(wp.data_ptr()), None, stream()))
+        wbytes = (Nn // 128) * (K // 128) * (chunk - 256) + Nn * K // 128 * 2
     del w
     copies = [wp] + [wp.clone() for _ in range(min(63, max(0, -(-300_000_000 // wp.numel() // wp.element_size()) - 1)))]
     xp = torch.randint(-2000, 2000, (((M + TM - 1) // TM) * TM * K,), dtype=torch.int16, device="cuda")
@@ -94,7 +95,7 @@ def main():
         for name in args.names.split(","):
             Nn, K = SHAPES[name]
             for bits in [int(b) for b in args.bits.split(",")]:
-                if name == "lm_head" and bits == 4:
+                if name == "lm_head" and bits != 16:
                     continue
                 r = gemm(bits, Nn, K, args.M, min(256, (args.M + 15) // 16 * 16))
                 r["name"] = name
