@@ -421,7 +421,7 @@ def run_ours(args):
     # stream from pinned host (committed at the next token boundary once landed,
     # then the freed pages are carved into KV ids and detached back) vs without.
     swap_layer = W4_LAYERS[0]
-    nsw = max(4, args.steps // 2)
+    nsw = max(10, args.steps)
     extra_id = 10_000_000
 
     def swap_window(n):
@@ -454,9 +454,13 @@ def run_ours(args):
             dev.swap_commit(t2)
         return t, done
 
-    # alternate A (no swap) / B (swap traffic) three times; medians
+    # one untimed swap window first: the decode graphs of the precision vectors
+    # the window alternates between are captured once, as in a long serving run;
+    # then A (no swap) / B (swap traffic) windows interleaved 5 times (the SM
+    # clock drifts under the power cap), medians
+    swap_window(nsw)
     t_a, t_b, swaps = [], [], 0
-    for _ in range(3):
+    for _ in range(5):
         t_a.append(timed(nsw)[0])
         tb, dn = swap_window(nsw)
         t_b.append(tb)
@@ -539,7 +543,7 @@ def run_ours(args):
         "serving": serving,
         "swap_upload_ms": {"w4_layer_mean": float(np.mean(swap_ms))},
         "swap_exposed_stall_ms_per_token": stall_ms_per_token,
-        "swap_stall_test": {"steps_per_window": nsw, "windows": 3, "swaps_committed": swaps,
+        "swap_stall_test": {"steps_per_window": nsw, "windows": 5, "swaps_committed": swaps,
                             "ms_without_median": t_noswap, "ms_with_median": t_swap,
                             "ms_without": t_a, "ms_with": t_b,
                             "frac_of_tpot": (max(0.0, t_swap - t_noswap) / t_noswap) if t_noswap else None},

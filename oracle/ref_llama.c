@@ -469,7 +469,8 @@ void ref_attention(const float* q /*[H][hd]*/, const uint16_t* kc, const uint16_
     for (int t = 0; t < ctx; ++t) {
       double acc = 0.0;
       const uint16_t* kr = kc + ((int64_t)t * KVH + kh) * hd;
-      for (int i = 0; i < hd; ++i) acc += (double)q[h * hd + i] * (double)bf2f(kr[i]);
+      /* q enters q.k rounded to bf16 (every device attention path), fp32 scale after */
+      for (int i = 0; i < hd; ++i) acc += (double)bf2f(f2bf(q[h * hd + i])) * (double)bf2f(kr[i]);
       s[t] = (float)acc * scale;
       if (s[t] > mx) mx = s[t];
     }

@@ -27,6 +27,9 @@
 
 namespace ms {
 
+// q enters every attention path rounded to bf16
+__device__ __forceinline__ float bf16r(float x) { return bf2f(f2bf(x)); }
+
 // K/V ring depth and CTAs per SM (MS_ATTN_STAGES / MS_ATTN_CTAS override,
 // experiments): bytes in flight per SM = CTAs x stages x 8 KB.
 constexpr int kAttnMaxStages = 12;
@@ -187,14 +190,14 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
         const int c = (2 * i + rot) & 15;
         const float4 x0 = *reinterpret_cast<const float4*>(qp + c * 8);
         const float4 x1 = *reinterpret_cast<const float4*>(qp + c * 8 + 4);
-        qr[i][0] = x0.x * a.scale_log2;
-        qr[i][1] = x0.y * a.scale_log2;
-        qr[i][2] = x0.z * a.scale_log2;
-        qr[i][3] = x0.w * a.scale_log2;
-        qr[i][4] = x1.x * a.scale_log2;
-        qr[i][5] = x1.y * a.scale_log2;
-        qr[i][6] = x1.z * a.scale_log2;
-        qr[i][7] = x1.w * a.scale_log2;
+        qr[i][0] = bf16r(x0.x) * a.scale_log2;
+        qr[i][1] = bf16r(x0.y) * a.scale_log2;
+        qr[i][2] = bf16r(x0.z) * a.scale_log2;
+        qr[i][3] = bf16r(x0.w) * a.scale_log2;
+        qr[i][4] = bf16r(x1.x) * a.scale_log2;
+        qr[i][5] = bf16r(x1.y) * a.scale_log2;
+        qr[i][6] = bf16r(x1.z) * a.scale_log2;
+        qr[i][7] = bf16r(x1.w) * a.scale_log2;
       }
     }
     float* pb = pbuf + warp * 16;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
     for (int g = 0; g < G; ++g) {
       const float* qp = qsrc + (size_t)g * HD + lane * VEC;
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) qv[g][i] = qp[i] * a.scale_log2;
+      for (int i = 0; i < VEC; ++i) qv[g][i] = bf16r(qp[i]) * a.scale_log2;
       m[g] = -INFINITY;
       l[g] = 0.f;
 #pragma unroll
@@ -430,8 +433,8 @@ __global__ void attn_combine_kernel(AttnArgs a) {
 // ---------------------------------------------------------------------------
 // GQA decode attention (G = H / KVH >= 2 query heads per KV head, hd 128) on the
 // tensor cores: per 16-token block one consumer warp computes S = Q K^T with
-// mma.sync m16n8k16 (the G query heads are the M rows; q = hi + lo bf16 split
-// keeps fp32-level score accuracy, as in prefill_attention.cu), the online
+// mma.sync m16n8k16 (the G query heads are the M rows, bf16(q) as on every
+// attention path; rows G..15 are padding), the online
 // softmax on the accumulator fragments, and O += P V (P bf16).  The producer
 // warp stages each block's K and V rows with 16-byte cp.async into an
 // XOR-swizzled layout (chunk c of row r at c ^ (r & 7)) so the ldmatrix
@@ -534,8 +537,9 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
   }
   const float* qsrc = fused ? qsm : a.q + ((size_t)row * a.H + kvh * G) * HD;
   const int g = lane >> 2, t4 = lane & 3;  // fragment row (query head) / column pair
-  // Q A-fragments (rows g < G valid), scaled to the log2 domain, hi/lo split
-  uint32_t qh[8][2], ql[8][2];
+  // Q A-fragments: rows g < G hold bf16(q) of query head g (unscaled, the
+  // attention contract of every path); rows >= G (and g + 8) are zero
+  uint32_t qh[8][2];
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
@@ -543,12 +547,10 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
       float x0 = 0.f, x1 = 0.f;
       if (g < G) {
         const float* qp = qsrc + (size_t)g * HD + ks * 16 + hf * 8 + 2 * t4;
-        x0 = qp[0] * a.scale_log2;
-        x1 = qp[1] * a.scale_log2;
+        x0 = qp[0];
+        x1 = qp[1];
       }
-      const uint16_t h0 = f2bf(x0), h1 = f2bf(x1);
-      qh[ks][hf] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-      ql[ks][hf] = pack_bf2(x0 - bf2f(h0), x1 - bf2f(h1));
+      qh[ks][hf] = pack_bf2(x0, x1);
     }
   float o[16][4];
 #pragma unroll
@@ -560,21 +562,21 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
     const int s = it % S;
     mbar_wait(&full[s], (it / S) & 1);
     const uint32_t kt = smem_u32(smem + (size_t)s * kStageBytes), vt = kt + 16 * 128;  // V rows = lines 16..31
-    // ---- S = Q K^T: n-tile 0 = tokens 0-7, n-tile 1 = tokens 8-15.  A rows g
-    // carry q_hi of head g and rows g + 8 its q_lo, so one MMA per k-step and
-    // n-tile yields both halves (summed below).
+    // ---- S = Q K^T: n-tile 0 = tokens 0-7, n-tile 1 = tokens 8-15 (A rows
+    // g + 8 are zero padding of the m16 shape)
     float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       uint32_t k0, k1, k2, k3;  // (tok 0-7, dims 16ks..+7), (tok 0-7, +8..), (tok 8-15, ..), (tok 8-15, +8..)
       gqa_ldsm_x4(kt + gqa_tsw(lr, ks >> 2, 2 * (ks & 3) + lc), k0, k1, k2, k3);
-      gqa_mma(sc[0], qh[ks][0], ql[ks][0], qh[ks][1], ql[ks][1], k0, k1);
-      gqa_mma(sc[1], qh[ks][0], ql[ks][0], qh[ks][1], ql[ks][1], k2, k3);
+      gqa_mma(sc[0], qh[ks][0], 0u, qh[ks][1], 0u, k0, k1);
+      gqa_mma(sc[1], qh[ks][0], 0u, qh[ks][1], 0u, k2, k3);
     }
     // ---- online softmax for head g over this block's 16 tokens
     const int tok0 = (b0 + it) * BT;
-    // tokens 2t4, 2t4+1, 8+2t4, 9+2t4: hi row + lo row
-    float v4[4] = {sc[0][0] + sc[0][2], sc[0][1] + sc[0][3], sc[1][0] + sc[1][2], sc[1][1] + sc[1][3]};
+    // tokens 2t4, 2t4+1, 8+2t4, 9+2t4 of head g, scaled to the log2 domain
+    const float sl = a.scale_log2;
+    float v4[4] = {sc[0][0] * sl, sc[0][1] * sl, sc[1][0] * sl, sc[1][1] * sl};
     const int tk[4] = {2 * t4, 2 * t4 + 1, 8 + 2 * t4, 9 + 2 * t4};
     float mx = -INFINITY;
 #pragma unroll

@@ -11,8 +11,9 @@
 // tile: cp.async 16-B chunks of K and V (4 paged blocks) into XOR-swizzled
 // shared memory (double buffered), S = Q K^T and O += P V on the tensor cores
 // with mma.sync m16n8k16 bf16 (fp32 accumulate), online softmax in registers
-// (log2 domain).  Q is split q = hi + lo (two bf16 MMAs) so the scores keep
-// fp32-level accuracy (the oracle computes q.k in fp32).
+// (log2 domain).  Q enters the MMA rounded to bf16 (unscaled), the score is
+// scaled in fp32 afterwards: the attention contract of every path (DESIGN.md
+// section 4, oracle ref_attention).
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_bf16.h>
@@ -67,8 +68,7 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sQh = smem;
-  uint8_t* sQl = sQh + kQTile * HD * 2;
-  uint8_t* sKV = sQl + kQTile * HD * 2;  // [2 buffers][K tile | V tile]
+  uint8_t* sKV = sQh + kQTile * HD * 2;  // [2 buffers][K tile | V tile]
   int32_t* sPage = reinterpret_cast<int32_t*>(sKV + 2 * 2 * kKTile * HD * 2);
 
   pdl_wait();
@@ -83,25 +83,20 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
   const int n_blocks = q_last / 16 + 1;
   for (int b = threadIdx.x; b < n_blocks; b += 128) sPage[b] = a.pages[b];
 
-  // ---- Q tile: fp32 -> (hi, lo) bf16 split into swizzled smem
+  // ---- Q tile: fp32 -> bf16 into swizzled smem
   for (int idx = threadIdx.x; idx < kQTile * CH; idx += 128) {
     const int r = idx / CH, c = idx - r * CH;
     const int q = q0 + r;
-    uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    uint32_t hi[4] = {0, 0, 0, 0};
     if (q < n) {
       const float4* src = reinterpret_cast<const float4*>(a.q + ((size_t)q * a.H + h) * HD + c * 8);
       const float4 x0 = src[0], x1 = src[1];
-      const float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float a0 = v[2 * e], a1 = v[2 * e + 1];
-        const uint16_t h0 = f2bf(a0), h1 = f2bf(a1);
-        hi[e] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-        lo[e] = pack_bf2(a0 - bf2f(h0), a1 - bf2f(h1));
-      }
+      hi[0] = pack_bf2(x0.x, x0.y);
+      hi[1] = pack_bf2(x0.z, x0.w);
+      hi[2] = pack_bf2(x1.x, x1.y);
+      hi[3] = pack_bf2(x1.z, x1.w);
     }
     *reinterpret_cast<uint4*>(sQh + swz(r, c, CH)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4*>(sQl + swz(r, c, CH)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
   __syncthreads();
 
@@ -127,7 +122,7 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   const int g = lane >> 2, t4 = lane & 3;
   const int qrow0 = q0 + warp * 16 + g;  // this thread's two query rows: qrow0, qrow0 + 8
-  const uint32_t sQh_u = smem_u32(sQh), sQl_u = smem_u32(sQl);
+  const uint32_t sQh_u = smem_u32(sQh);
 
   load_tile(0, 0);
   for (int kt = 0; kt < n_ktiles; ++kt) {
@@ -148,11 +143,10 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
     for (int j = 0; j < kKTile / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-      uint32_t ah[4], al[4];
+      uint32_t ah[4];
       {
         const int r = warp * 16 + (lane & 15), c = kk * 2 + (lane >> 4);
         ldsm_x4(sQh_u + swz(r, c, CH), ah[0], ah[1], ah[2], ah[3]);
-        ldsm_x4(sQl_u + swz(r, c, CH), al[0], al[1], al[2], al[3]);
       }
 #pragma unroll
       for (int jp = 0; jp < kKTile / 16; ++jp) {  // pairs of 8-token n-tiles
@@ -160,9 +154,7 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
         const int r = jp * 16 + (lane & 7) + ((lane >> 4) << 3), c = kk * 2 + ((lane >> 3) & 1);
         ldsm_x4(sK_u + swz(r, c, CH), b0, b1, b2, b3);
         mma16816(s[2 * jp], ah[0], ah[1], ah[2], ah[3], b0, b1);
-        mma16816(s[2 * jp], al[0], al[1], al[2], al[3], b0, b1);
         mma16816(s[2 * jp + 1], ah[0], ah[1], ah[2], ah[3], b2, b3);
-        mma16816(s[2 * jp + 1], al[0], al[1], al[2], al[3], b2, b3);
       }
     }
     // ---- online softmax (log2 domain), causal mask on the diagonal tiles
@@ -262,7 +254,7 @@ cudaError_t prefill_attn_launch(const PrefillAttnArgs& a, cudaStream_t stream) {
   }
   const int qtiles = (a.n + kQTile - 1) / kQTile;
   const int max_blocks = (a.n + 15) / 16;
-  auto smem_for = [&](int hd) { return (size_t)kQTile * hd * 2 * 2 + (size_t)2 * 2 * kKTile * hd * 2 + max_blocks * 4 + 16; };
+  auto smem_for = [&](int hd) { return (size_t)kQTile * hd * 2 + (size_t)2 * 2 * kKTile * hd * 2 + max_blocks * 4 + 16; };
   if (a.kv.head_dim == 128) {
     const size_t sm = smem_for(128);
     static bool attr = false;

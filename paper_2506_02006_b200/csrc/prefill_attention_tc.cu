@@ -17,16 +17,16 @@
 //            V 2 (freed when PV(kt) completes); separate warps so neither
 //            queue waits behind the other.
 //   warp 9   MMA issuer (one elected lane of a converged warp):
-//            S(kt) = Q_hi K^T + Q_lo K^T (16 MMAs M128 N128 K16 into one of
-//            three TMEM S buffers; q = hi + lo bf16 keeps fp32-level score
-//            accuracy as the mma.sync kernel and the decode paths do), then
-//            O += P(kt) V (8 MMAs, A = P read from TMEM, B = V MN-major).
+//            S(kt) = Q K^T (8 MMAs M128 N128 K16 into one of three TMEM S
+//            buffers; Q = bf16(q) unscaled, the attention contract of every
+//            path), then O += P(kt) V (8 MMAs, A = P
+//            read from TMEM, B = V MN-major).
 //            Order S(0), S(1), [S(kt+2), PV(kt)]...: the tensor cores run up to
 //            two S tiles ahead of the softmax.
 //   warps 0-7 softmax: thread = (query row = TMEM lane, half of the 128 keys);
 //            the halves of a row exchange maxima through shared memory under a
-//            pairwise named barrier.  Online softmax in the log2 domain (scale
-//            folded into q) with lazy rescaling: the running max moves only
+//            pairwise named barrier.  Online softmax in the log2 domain (the
+//            fp32 scores scaled by log2(e)/sqrt(hd) inside the exp2 FMA) with lazy rescaling: the running max moves only
 //            when a tile's max exceeds it by more than 2^8, so O (in TMEM) is
 //            rescaled a handful of times per row instead of every tile; the
 //            result is the same softmax (exact up to fp32 rounding).  P (bf16)
@@ -130,8 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // operands: 1024-B aligned (SW128 atoms)
   uint8_t* ops = smem_raw + (((smem_u32(smem_raw) + kCtrlBytes + 1023u) & ~1023u) - smem_u32(smem_raw));
   uint8_t* sQh = ops;                         // canonical no-swizzle, written by the softmax warps
-  uint8_t* sQl = sQh + kOpBytes;
-  uint8_t* sK = sQl + kOpBytes;               // [kKStages] SW128 images [dim half][key][128 B]
+  uint8_t* sK = sQh + kOpBytes;               // [kKStages] SW128 images [dim half][key][128 B]
   uint8_t* sV = sK + kKStages * kOpBytes;     // [kVStages] same
 
   // head-major, longest query tiles of a head first: the CTAs in flight share
@@ -189,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 10 && n_ktiles > kVStages) row_v = tile_row(kVStages);
   if (warp == 9) tmem_alloc<512>(tmem_slot);
 
-  // ---- Q tile (softmax warps): fp32 * scale_log2 -> (hi, lo) bf16, canonical layout;
+  // ---- Q tile (softmax warps): fp32 -> bf16, canonical layout;
   // all 16 loads of a thread in flight at once (the CTA's first S waits on this)
   if (warp < 8) {
     float4 x[8][2];
@@ -204,20 +203,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int idx = threadIdx.x + it * 256, r = idx >> 4, c = idx & 15;
-      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+      uint32_t hi[4] = {0, 0, 0, 0};
       if (q0 + r < n) {
-        const float sl = a.scale_log2;  // scores come out of the MMA already in the log2 domain
         const float4 x0 = x[it][0], x1 = x[it][1];
-        const float v[8] = {x0.x * sl, x0.y * sl, x0.z * sl, x0.w * sl, x1.x * sl, x1.y * sl, x1.z * sl, x1.w * sl};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint16_t h0 = f2bf(v[2 * e]), h1 = f2bf(v[2 * e + 1]);
-          hi[e] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-          lo[e] = pack_bf2(v[2 * e] - bf2f(h0), v[2 * e + 1] - bf2f(h1));
-        }
+        hi[0] = pack_bf2(x0.x, x0.y);
+        hi[1] = pack_bf2(x0.z, x0.w);
+        hi[2] = pack_bf2(x1.x, x1.y);
+        hi[3] = pack_bf2(x1.z, x1.w);
       }
       *reinterpret_cast<uint4*>(sQh + canon(r, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(sQl + canon(r, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
     fence_proxy_async_smem();
   }
@@ -250,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------- MMA issuer
     const uint32_t idesc = umma_idesc_bf16(128, 128);
     const uint32_t idesc_pv = idesc | (1u << 16);  // B (= V) MN-major
-    const uint64_t dQh = umma_desc(smem_u32(sQh), 128u, 2048u), dQl = umma_desc(smem_u32(sQl), 128u, 2048u);
-    auto issue_s = [&](int kt) {  // S(kt) = Q_hi K^T + Q_lo K^T into S buffer kt % kSBufs
+    const uint64_t dQh = umma_desc(smem_u32(sQh), 128u, 2048u);
+    auto issue_s = [&](int kt) {  // S(kt) = Q K^T into S buffer kt % kSBufs
       const int s = kt % kKStages;
       mbar_wait(&kfull[s], (kt / kKStages) & 1);
       tc_fence_after();
@@ -262,7 +256,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ks = 0; ks < 8; ++ks) {
           const uint64_t dk = desc_add(dK, (uint32_t)(ks >> 2) * kHalfBytes + (uint32_t)(ks & 3) * 32u);
           umma_bf16(d, desc_add(dQh, ks * 256u), dk, idesc, ks ? 1u : 0u);
-          umma_bf16(d, desc_add(dQl, ks * 256u), dk, idesc, 1u);
         }
         umma_commit(&sfull[kt % kSBufs]);
         umma_commit(&kempty[s]);
@@ -333,7 +326,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < 4; ++k) m4[k] = __uint_as_float(v[k]);
 #pragma unroll
       for (int j = 4; j < 64; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
-      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      const float sl = a.scale_log2;  // raw q.k scores -> log2 domain
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl;
       if (kt > 0) asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // partner read the last maxima
       sRed[half * kTcTile + row] = mx;
       asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
@@ -362,8 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pk[32];
 #pragma unroll
       for (int j = 0; j < 64; j += 2) {
-        const float p0 = ex2(__uint_as_float(v[j]) - msub);
-        const float p1 = ex2(__uint_as_float(v[j + 1]) - msub);
+        const float p0 = ex2(fmaf(__uint_as_float(v[j]), sl, -msub));
+        const float p1 = ex2(fmaf(__uint_as_float(v[j + 1]), sl, -msub));
         ps[(j >> 1) & 3] += p0 + p1;
         pk[j >> 1] = cvt_bf2(p0, p1);
       }
@@ -444,7 +438,7 @@ cudaError_t prefill_attn_tc_launch(const PrefillAttnArgs& a, cudaStream_t stream
     map_bytes = a.arena_bytes;
   }
   const int qtiles = (a.n + kTcTile - 1) / kTcTile;
-  const size_t smem = kCtrlBytes + 1024 + (size_t)(2 + kKStages + kVStages) * kOpBytes;
+  const size_t smem = kCtrlBytes + 1024 + (size_t)(1 + kKStages + kVStages) * kOpBytes;
   if (smem > 227 * 1024) return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {

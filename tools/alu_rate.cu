@@ -30,6 +30,14 @@ __global__ void rate_kernel(uint32_t* out, int iters, uint32_t seed) {
         v[i] = __float_as_uint(__uint_as_float(v[i]) * __uint_as_float(s));
       } else if (kMode == 3) {  // LOP3
         asm("lop3.b32 %0, %0, %1, %2, 0xEA;" : "+r"(v[i]) : "r"(0x000F000Fu), "r"(s));
+      } else if (kMode == 5) {  // MUFU ex2 f32
+        float x = __uint_as_float(v[i] & 0x3fffffffu) * -0.5f;
+        asm("ex2.approx.ftz.f32 %0, %0;" : "+f"(x));
+        v[i] = __float_as_uint(x);
+      } else if (kMode == 6) {  // MUFU ex2 f16x2
+        uint32_t x = v[i] | 0x80008000u;
+        asm("ex2.approx.f16x2 %0, %0;" : "+r"(x));
+        v[i] = x;
       } else if (kMode == 4) {  // dequant word: shf + lop3 + hsub2 + hmul2 (bf16)
         uint32_t x;
         asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(v[i] >> 4), "r"(0x000F000Fu), "r"(0x43004300u));
@@ -57,7 +65,7 @@ void run(const char* name, int warps) {
   cudaDeviceSynchronize();
   uint32_t cyc;
   cudaMemcpy(&cyc, d + blocks * threads, 4, cudaMemcpyDeviceToHost);
-  const int per_iter = kMode == 4 ? 5 : 1;  // warp-instructions per chain step (mode 4: shf, lop3, hadd2, hmul2, xor)
+  const int per_iter = kMode == 4 ? 5 : (kMode == 5 ? 3 : (kMode == 6 ? 2 : 1));  // warp-instructions per chain step (mode 4: shf, lop3, hadd2, hmul2, xor)
   const double instr_per_smsp = (double)iters * 8 * per_iter * warps / 4.0;
   printf("%-28s warps %2d: %.2f cycles per warp-instruction per SMSP\n", name, warps, cyc / instr_per_smsp);
   cudaFree(d);
@@ -70,6 +78,8 @@ int main() {
     run<2>("FMUL", w);
     run<3>("LOP3", w);
     run<4>("dequant word (5 instr)", w);
+    run<5>("ex2.f32 (+lop, fmul)", w);
+    run<6>("ex2.f16x2 (+lop)", w);
   }
   return 0;
 }
