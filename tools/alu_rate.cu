@@ -38,6 +38,12 @@ __global__ void rate_kernel(uint32_t* out, int iters, uint32_t seed) {
         uint32_t x = v[i] | 0x80008000u;
         asm("ex2.approx.f16x2 %0, %0;" : "+r"(x));
         v[i] = x;
+      } else if (kMode == 7) {  // software exp2 (round-to-nearest split, degree-3 polynomial)
+        const float x = __uint_as_float(v[i] & 0x3fffffffu) * -0.5f;
+        const float j = x + 12582912.0f;                 // 1.5 * 2^23: nearest integer in the mantissa
+        const float f = x - (j - 12582912.0f);           // [-0.5, 0.5]
+        float p = fmaf(fmaf(fmaf(0.0555041f, f, 0.2402265f), f, 0.6931472f), f, 1.0f);
+        v[i] = __float_as_uint(p) + (__float_as_uint(j) << 23);
       } else if (kMode == 4) {  // dequant word: shf + lop3 + hsub2 + hmul2 (bf16)
         uint32_t x;
         asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(v[i] >> 4), "r"(0x000F000Fu), "r"(0x43004300u));
@@ -65,7 +71,7 @@ void run(const char* name, int warps) {
   cudaDeviceSynchronize();
   uint32_t cyc;
   cudaMemcpy(&cyc, d + blocks * threads, 4, cudaMemcpyDeviceToHost);
-  const int per_iter = kMode == 4 ? 5 : (kMode == 5 ? 3 : (kMode == 6 ? 2 : 1));  // warp-instructions per chain step (mode 4: shf, lop3, hadd2, hmul2, xor)
+  const int per_iter = kMode == 4 ? 5 : (kMode == 5 ? 3 : (kMode == 6 ? 2 : (kMode == 7 ? 10 : 1)));  // warp-instructions per chain step (mode 4: shf, lop3, hadd2, hmul2, xor)
   const double instr_per_smsp = (double)iters * 8 * per_iter * warps / 4.0;
   printf("%-28s warps %2d: %.2f cycles per warp-instruction per SMSP\n", name, warps, cyc / instr_per_smsp);
   cudaFree(d);
@@ -80,6 +86,7 @@ int main() {
     run<4>("dequant word (5 instr)", w);
     run<5>("ex2.f32 (+lop, fmul)", w);
     run<6>("ex2.f16x2 (+lop)", w);
+    run<7>("soft exp2 (10 instr)", w);
   }
   return 0;
 }
