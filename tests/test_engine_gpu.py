@@ -208,3 +208,35 @@ def test_swap_commit_keeps_captured_graphs():
     finally:
         ref.close()
         dev.close()
+
+
+@pytest.mark.parametrize("bits", [8, 3])
+def test_engine_swaps_to_q8_and_q3_levels(tmp_path, bits):
+    """Controller target_bits 8 / 3 (reference controller.cpp:21-23,
+    toy_model.hpp:26): the engine's swaps upload real Q8 / Q3 images; the event
+    log stays byte-identical to the CPU-only run and every generated token is
+    what the oracle predicts at that precision."""
+    from paper_2506_02006_b200 import morphsim as M
+    from paper_2506_02006_b200.device import DeviceModel, layer_pages
+    trace = tmp_path / "trace.csv"
+    trace.write_text("".join(f"{i * 3},{40 + (i % 3) * 8},{24 + (i % 4) * 4}\n" for i in range(14)))
+    seq = str(tmp_path / "seq.json")
+    M.save_sequence(M.baseline_sequence("back_to_front", 4), seq)
+    cfg = tiny_config(str(trace), seq)
+    cfg["model"]["layer_bytes"] = {k: layer_pages(TINY, b) * PB for k, b in
+                                   (("full", 16), ("q8", 8), ("q4", 4), ("q3", 3))}
+    for mode in ("performance", "accuracy"):
+        cfg["controller"][mode]["target_bits"] = bits
+    dev = DeviceModel(TINY, max_batch=32, max_prefill_tokens=128, max_pos=128,
+                      arena_pages=(4 * 48 + 40 + 40) + 32, variants=(16, bits, 4))
+    try:
+        dev.weights_synthetic(7)
+        rep_cpu, log_cpu, _ = M.run_arm_full(cfg, "morph-performance")
+        rep, log, _ = M.run_arm_full(cfg, "morph-performance", device=dev, record=True)
+        assert log == log_cpu
+        calls = rep.pop("device_calls")
+        assert rep["morph"]["swap_events"] >= 1
+        assert any(b == bits for c in calls for b in c["bits"])
+        _replay_on_oracle(cfg, dev, calls, min_checked=150)
+    finally:
+        dev.close()
