@@ -36,7 +36,7 @@ def tiny_config(trace_path, seq_path, static_blocks=40):
     }
 
 
-def _replay_on_oracle(cfg, dev, calls, min_checked=300):
+def _replay_on_oracle(cfg, dev, calls, min_checked=300, shape=TINY):
     """Replays every recorded device launch on the CPU oracle with the same
     per-layer precision; every generated token must match (near ties allowed)."""
     from paper_2506_02006_b200 import morphsim as M
@@ -48,8 +48,8 @@ def _replay_on_oracle(cfg, dev, calls, min_checked=300):
             for r in range(n_req)}
     for r in range(n_req):
         P = trace.events[r].prompt_tokens
-        assert np.array_equal(hist[r][:P], np.array(_core.synthetic_prompt(cfg["seed"], r, P, TINY["V"])))
-    model = O.RefModel(dict(TINY, max_pos=256), 7)
+        assert np.array_equal(hist[r][:P], np.array(_core.synthetic_prompt(cfg["seed"], r, P, shape["V"])))
+    model = O.RefModel(dict(shape, max_pos=256), 7)
     seqs, checked, ties = {}, 0, []
     bits_now = [16] * 4
 
@@ -212,31 +212,39 @@ def test_swap_commit_keeps_captured_graphs():
 
 @pytest.mark.parametrize("bits", [8, 3])
 def test_engine_swaps_to_q8_and_q3_levels(tmp_path, bits):
-    """Controller target_bits 8 / 3 (reference controller.cpp:21-23,
-    toy_model.hpp:26): the engine's swaps upload real Q8 / Q3 images; the event
-    log stays byte-identical to the CPU-only run and every generated token is
-    what the oracle predicts at that precision."""
+    """Controller target_bits 8 / 3 (config quant_bits, reference
+    experiment.cpp:92,139-140; toy_model.hpp:26): the engine's swaps upload
+    real Q8 / Q3 images and carve what they free into KV blocks; the event log
+    stays byte-identical to the CPU-only run and every generated token is what
+    the oracle predicts at that precision.  Tiny shape with 4 KV heads: 64 KiB
+    pages hold three 16640-B Q8 chunks, so a Q8 layer is smaller than BF16."""
     from paper_2506_02006_b200 import morphsim as M
-    from paper_2506_02006_b200.device import DeviceModel, layer_pages
+    from paper_2506_02006_b200.device import DeviceModel, layer_pages, page_bytes
+    shape = dict(TINY, KVH=4)
+    pb = page_bytes(shape)
+    pages = {b: layer_pages(shape, b) for b in (16, 8, 4, 3)}
+    assert pages[16] > pages[8] > pages[4] == pages[3]
     trace = tmp_path / "trace.csv"
-    trace.write_text("".join(f"{i * 3},{40 + (i % 3) * 8},{24 + (i % 4) * 4}\n" for i in range(14)))
+    trace.write_text("".join(f"{i * 3},{40 + (i % 3) * 8},{24 + (i % 4) * 4}\n" for i in range(14)) +
+                     "".join(f"{400 + i * 40},{32},{16}\n" for i in range(6)))
     seq = str(tmp_path / "seq.json")
     M.save_sequence(M.baseline_sequence("back_to_front", 4), seq)
-    cfg = tiny_config(str(trace), seq)
-    cfg["model"]["layer_bytes"] = {k: layer_pages(TINY, b) * PB for k, b in
-                                   (("full", 16), ("q8", 8), ("q4", 4), ("q3", 3))}
-    for mode in ("performance", "accuracy"):
-        cfg["controller"][mode]["target_bits"] = bits
-    dev = DeviceModel(TINY, max_batch=32, max_prefill_tokens=128, max_pos=128,
-                      arena_pages=(4 * 48 + 40 + 40) + 32, variants=(16, bits, 4))
+    static = 40
+    cfg = tiny_config(str(trace), seq, static_blocks=static)
+    cfg["quant_bits"] = bits  # both controller modes' target_bits
+    cfg["model"]["layer_bytes"] = {k: pages[b] * pb for k, b in (("full", 16), ("q8", 8), ("q4", 4), ("q3", 3))}
+    cfg["kv"]["block_bytes"] = pb
+    cfg["budget"] = {"device_bytes": (4 * pages[16] + static + 40) * pb, "reserve_bytes": 40 * pb}
+    dev = DeviceModel(shape, max_batch=32, max_prefill_tokens=128, max_pos=128,
+                      arena_pages=4 * pages[16] + static + 40 + 64, variants=(16, bits, 4))
     try:
         dev.weights_synthetic(7)
         rep_cpu, log_cpu, _ = M.run_arm_full(cfg, "morph-performance")
         rep, log, _ = M.run_arm_full(cfg, "morph-performance", device=dev, record=True)
         assert log == log_cpu
         calls = rep.pop("device_calls")
-        assert rep["morph"]["swap_events"] >= 1
+        assert rep["morph"]["swap_events"] >= 1 and "KV_ATTACH" in log
         assert any(b == bits for c in calls for b in c["bits"])
-        _replay_on_oracle(cfg, dev, calls, min_checked=150)
+        _replay_on_oracle(cfg, dev, calls, min_checked=150, shape=shape)
     finally:
         dev.close()
