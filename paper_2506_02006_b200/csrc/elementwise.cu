@@ -274,19 +274,35 @@ __global__ void silu_mul_kernel(const float* __restrict__ part, GemmPlanDev plan
   const float4* p4 = reinterpret_cast<const float4*>(part);
   const int m_end = min(M, (int)(blockIdx.y + 1) * rows);
   const size_t col = act_col_off(j4 * 4, TM);
-  // silu(g) = g / (1 + e^-g) with the fast exp / divide (a few ulp of fp32,
-  // far below the bf16 rounding of the result)
-  auto silu = [](float g) { return __fdividef(g, 1.0f + __expf(-g)); };
+  // columns 4 j4 .. +3: gate / up interleaved (gate_col), 8 consecutive floats
+  const int n0 = gate_col(j4 * 4);
 #pragma unroll 2
   for (int m = blockIdx.y * rows; m < m_end; ++m) {
-    const size_t base = (size_t)m * 2 * f4 + j4;
-    const float4 g = part_ld4(plan, p4 + base, stride4, m, j4 * 4);
-    const float4 u = part_ld4(plan, p4 + base + f4, stride4, m, ffn + j4 * 4);
+    const size_t base = ((size_t)m * 2 * ffn + n0) >> 2;
+    const float4 a = part_ld4(plan, p4 + base, stride4, m, n0);      // g0 u0 g1 u1
+    const float4 b = part_ld4(plan, p4 + base + 1, stride4, m, n0);  // g2 u2 g3 u3
     uint2 o;
-    o.x = pack_bf2(silu(g.x) * u.x, silu(g.y) * u.y);
-    o.y = pack_bf2(silu(g.z) * u.z, silu(g.w) * u.w);
+    o.x = pack_bf2(silu_f(a.x) * a.y, silu_f(a.z) * a.w);
+    o.y = pack_bf2(silu_f(b.x) * b.y, silu_f(b.z) * b.w);
     *reinterpret_cast<uint2*>(x + act_row_off(m, ffn, TM) + col) = o;
   }
+}
+
+// gate_up rows -> the interleaved storage order (gate_col); run before packing
+__global__ void interleave_gate_up_kernel(const uint16_t* __restrict__ w, int ffn, int K, uint16_t* __restrict__ out) {
+  const int64_t total = (int64_t)2 * ffn * K / 8;  // 16-B chunks
+  const int kc = K / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / kc), c = (int)(i - (int64_t)r * kc);
+    const int blk = r >> 7, t = r & 127;
+    const int src = (t & 1) * ffn + blk * 64 + (t >> 1);
+    reinterpret_cast<uint4*>(out)[i] = reinterpret_cast<const uint4*>(w)[(int64_t)src * kc + c];
+  }
+}
+cudaError_t interleave_gate_up_launch(const uint16_t* w, int ffn, int K, uint16_t* out, cudaStream_t s) {
+  if (ffn % 64 || K % 8) return cudaErrorInvalidValue;
+  interleave_gate_up_kernel<<<148 * 8, 256, 0, s>>>(w, ffn, K, out);
+  return cudaGetLastError();
 }
 
 cudaError_t silu_mul_launch(const float* part, const GemmPlanDev& plan, int M, int ffn, uint16_t* x_packed, int TM,

@@ -54,7 +54,7 @@ namespace ms {
 // (chunk sizes, ChunkCursor, SegIter, nib_magic: gemm_common.cuh)
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                float* __restrict__ out, int stages) {
+                float* __restrict__ out, int stages, GemmEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -186,14 +186,37 @@ __global__ void __launch_bounds__(192, 1)
       const int n = n_tile * 128 + quad * 32 + lane;
       float* o = out + (size_t)slot * M * N;
       const uint32_t d = tmem_base + acc * tm_cols + ((uint32_t)(quad * 32) << 16);
-      for (int c0 = 0; c0 < TM; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(d + (uint32_t)c0, v);
-        tmem_ld_wait();
+      if (epi.silu_out) {
+        // fused SiLU: lanes 2i / 2i+1 hold gate / up of FFN column
+        // j = 64 n_tile + (row >> 1) (interleaved storage, gate_col); per
+        // token pair the even lane computes token 2t, the odd lane 2t + 1
+        const int j = n_tile * 64 + ((quad * 32 + lane) >> 1);
+        const bool odd = lane & 1;
+        const size_t col = act_col_off(j, epi.TMo);
+        for (int c0 = 0; c0 < TM; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(d + (uint32_t)c0, v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = m_tile * TM + c0 + j;
-          if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
+          for (int t = 0; t < 8; ++t) {
+            const float ve = __uint_as_float(v[2 * t]), vo = __uint_as_float(v[2 * t + 1]);
+            const float mine = odd ? vo : ve, send = odd ? ve : vo;
+            const float other = __shfl_xor_sync(0xffffffffu, send, 1);
+            const float g = odd ? other : mine, up = odd ? mine : other;
+            const int m = m_tile * TM + c0 + 2 * t + (odd ? 1 : 0);
+            if (m < M) epi.silu_out[act_row_off(m, epi.ffn, epi.TMo) + col] = f2bf(silu_f(g) * up);
+          }
+        }
+      } else {
+        for (int c0 = 0; c0 < TM; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(d + (uint32_t)c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int m = m_tile * TM + c0 + j;
+            if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
+          }
         }
       }
       tc_fence_before();
@@ -681,7 +704,9 @@ static cudaError_t launch_q_groups(const GemmWeights& w, const uint16_t* x, int 
 }
 
 cudaError_t gemm_launch(const GemmWeights& w, int wkind, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                        float* out, cudaStream_t stream) {
+                        float* out, cudaStream_t stream, const GemmEpi& epi) {
+  // the fused SiLU epilogue needs whole tiles (one slot) of the BF16 kernel
+  if (epi.silu_out && (wkind != 16 || !plan.aligned)) return cudaErrorInvalidValue;
   if (wkind == 8) return launch_q_groups<1, 8>(w, x, M, TM, plan, out, stream);
   if (wkind == 4) {
     // the plan fixed the unit: K / nk = 256 -> two K groups per pipeline unit
@@ -702,7 +727,7 @@ cudaError_t gemm_launch(const GemmWeights& w, int wkind, const uint16_t* x, int 
     cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  return launch_pdl(gemm_kernel, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, st);
+  return launch_pdl(gemm_kernel, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, st, epi);
 }
 
 }  // namespace ms

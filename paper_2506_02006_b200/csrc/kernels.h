@@ -93,8 +93,24 @@ __host__ __device__ inline int part_slots(const GemmPlanDev& p, int m, int n) {
 
 GemmPlanDev gemm_plan(int N, int K, int M, int TM, int wkind, int num_sms, size_t part_elems);
 
+// The gate_up matrix is stored with gate and up rows interleaved per 64
+// output columns: packed row 128 c + 2 i = gate row 64 c + i, row 128 c + 2 i + 1
+// = up row 64 c + i.  A 128-row weight tile then holds gate AND up of the same
+// 64 FFN columns, in adjacent TMEM lanes, so SiLU(gate) * up is tile-local.
+__host__ __device__ inline int gate_col(int j) { return ((j >> 6) << 7) + ((j & 63) << 1); }  // up: + 1
+cudaError_t interleave_gate_up_launch(const uint16_t* w, int ffn, int K, uint16_t* out, cudaStream_t s);
+
+// Optional fused epilogue of the BF16 GEMM (whole-tile plans, one slot):
+// silu_out != nullptr -> the tile's (gate, up) lane pairs become
+// bf16(silu(gate) * up) in the packed activation image [M x ffn] (token tile TMo)
+// instead of fp32 partials.
+struct GemmEpi {
+  uint16_t* silu_out = nullptr;
+  int ffn = 0, TMo = 0;
+};
+
 cudaError_t gemm_launch(const GemmWeights& w, int wkind, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                        float* out, cudaStream_t stream);
+                        float* out, cudaStream_t stream, const GemmEpi& epi = GemmEpi());
 
 // Paged KV geometry.  Page p holds one logical KV block (block_tokens tokens of
 // every layer): [layer][kv_head][K|V][token][head_dim] bf16.

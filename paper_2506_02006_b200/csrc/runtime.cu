@@ -204,6 +204,7 @@ struct ms_ctx {
   int max_rows = 0;
   float* h = nullptr;
   uint16_t* x = nullptr;
+  uint16_t* x2 = nullptr;  // SiLU output of a fused gate_up GEMM (its input x is still being read)
   float* part = nullptr;
   size_t part_elems = 0;
   float* q = nullptr;
@@ -374,6 +375,13 @@ int round16(int m) { return (m + 15) / 16 * 16; }
 
 void build_images(ms_ctx* c, int l, uint16_t* w_dev[kMats], uint8_t* tmp) {
   Layer& L = c->layers[l];
+  // gate_up rows into the interleaved storage order (kernels.h gate_col) once,
+  // before any variant is packed: tmp <- raw, raw <- interleave(tmp)
+  {
+    const ms_model_desc& D = c->desc;
+    CK(cudaMemcpyAsync(tmp, w_dev[2], (size_t)2 * D.ffn * D.hidden * 2, cudaMemcpyDeviceToDevice, c->compute));
+    CK(ms::interleave_gate_up_launch(reinterpret_cast<const uint16_t*>(tmp), D.ffn, D.hidden, w_dev[2], c->compute));
+  }
   for (int bi = 0; bi < kVariants; ++bi) {
     if (!c->variant_on[bi]) continue;
     const ImageGeom& g = c->geom[bi];
@@ -419,10 +427,31 @@ ms::GemmWeights mat_weights(ms_ctx* c, int l, int mat) {
 // Quantised layers (Q8 / Q4 / Q3) at every M run the fused kernel (codes ->
 // bf16 dequantised into TMEM in the GEMM's staging path); no dequantised copy
 // of a matrix exists.  wkind: 16 BF16, 8 int8 codes, 4 int4 containers.
-ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, int wkind, int M, int TM) {
+// MS_FUSED_SILU=0 (experiments / A-B): keep the separate SiLU kernel at long prefills
+bool fused_silu_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MS_FUSED_SILU");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// fuse_silu (the gate_up GEMM): when the plan takes whole tiles and the layer
+// is BF16, the epilogue writes bf16(silu(gate) * up) straight into the next
+// GEMM's activation image and *fused is set (no fp32 output, no SiLU launch).
+ms::GemmPlanDev gemm(ms_ctx* c, const ms::GemmWeights& w, int wkind, int M, int TM, bool fuse_silu = false,
+                     bool* fused = nullptr, const uint16_t* x_in = nullptr) {
   if ((size_t)M * w.N > c->part_elems) fail(MS_EVALIDATION, "GEMM rows x N exceed the partial buffer");
   const ms::GemmPlanDev plan = ms::gemm_plan(w.N, w.K, M, TM, wkind, c->num_sms, c->part_elems);
-  CK(ms::gemm_launch(w, wkind, c->x, M, TM, plan, c->part, c->compute));
+  ms::GemmEpi epi;
+  const bool fuse = fuse_silu && wkind == 16 && plan.aligned && fused_silu_enabled();
+  if (fuse) {
+    epi.silu_out = c->x2;
+    epi.ffn = w.N / 2;
+    epi.TMo = TM;
+  }
+  if (fused) *fused = fuse;
+  CK(ms::gemm_launch(w, wkind, x_in ? x_in : c->x, M, TM, plan, c->part, c->compute, epi));
   c->launches += 1;
   return plan;
 }
@@ -572,12 +601,15 @@ void forward(ms_ctx* c, int M, int TM, const int32_t* d_slot, const int32_t* d_p
     CK(ms::residual_norm_launch(c->part, s, M, d, c->h, n2, D.rms_eps, c->x, TM, c->compute));
     c->launches += 1;
     pk_mark(c, MS_PK_NORM);
-    s = gemm(c, mat_weights(c, l, 2), wk, M, TM);
+    bool silu_done = false;
+    s = gemm(c, mat_weights(c, l, 2), wk, M, TM, true, &silu_done);
     pk_mark(c, w4 ? MS_PK_GEMM_GU_W4 : MS_PK_GEMM_GU);
-    CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
-    c->launches += 1;
-    pk_mark(c, MS_PK_SILU);
-    s = gemm(c, mat_weights(c, l, 3), wk, M, TM);
+    if (!silu_done) {
+      CK(ms::silu_mul_launch(c->part, s, M, D.ffn, c->x, TM, c->compute));
+      c->launches += 1;
+      pk_mark(c, MS_PK_SILU);
+    }
+    s = gemm(c, mat_weights(c, l, 3), wk, M, TM, false, nullptr, silu_done ? c->x2 : c->x);
     pk_mark(c, w4 ? MS_PK_GEMM_DOWN_W4 : MS_PK_GEMM_DOWN);
     CK(ms::residual_norm_rows_launch(c->part, s, M, d, c->h, nw, D.rms_eps, c->x, tm_out, row_begin, c->compute));
     c->launches += 1;
@@ -721,6 +753,10 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       CK(cudaMalloc(&c->h, (size_t)c->max_rows * d * sizeof(float)));
       CK(cudaMalloc(&c->x, (size_t)rows_pad * kmax * sizeof(uint16_t)));
       CK(cudaMemset(c->x, 0, (size_t)rows_pad * kmax * sizeof(uint16_t)));
+      // second image for the fused gate_up -> SiLU output (whole-tile plans)
+      const size_t x2_elems = (size_t)rows_pad * desc->ffn;
+      CK(cudaMalloc(&c->x2, x2_elems * sizeof(uint16_t)));
+      CK(cudaMemset(c->x2, 0, x2_elems * sizeof(uint16_t)));
       c->part_elems = std::max((size_t)desc->max_prefill_tokens * std::max(qkv_n, 2 * desc->ffn),
                                (size_t)std::min(desc->max_batch * 16, 4096) * nmax);
       c->part_elems = std::max(c->part_elems, (size_t)std::min(desc->max_prefill_tokens, 256) * desc->vocab);
@@ -802,7 +838,7 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
-                 c->h, c->x, c->part, c->q, c->attn_ws, c->am_key, c->am_cnt, c->next, c->logits, c->hist};
+                 c->h, c->x, c->x2, c->part, c->q, c->attn_ws, c->am_key, c->am_cnt, c->next, c->logits, c->hist};
   for (void* p : dev) cudaFree(p);
   cudaFreeHost(c->h_next);
   cudaFreeHost(c->h_logits);
