@@ -52,6 +52,47 @@
 namespace ms {
 
 // (chunk sizes, ChunkCursor, SegIter, nib_magic: gemm_common.cuh)
+
+// Epilogue of one accumulator (128 weight rows x TM tokens, this warp's 32
+// lanes at TMEM address d): fp32 partials out[m][n], or -- fused SiLU
+// (GemmEpi) -- bf16(silu(gate) * up) into the packed activation image: lanes
+// 2i / 2i+1 hold gate / up of FFN column j = 64 n_tile + (row >> 1)
+// (interleaved storage, gate_col); per token pair the even lane computes token
+// 2t and the odd lane token 2t + 1.
+__device__ __forceinline__ void epilogue_tile(uint32_t d, int quad, int lane, int n_tile, int m_tile, int M, int N,
+                                              int TM, float* __restrict__ o, const GemmEpi& epi) {
+  if (epi.silu_out) {
+    const int j = n_tile * 64 + ((quad * 32 + lane) >> 1);
+    const bool odd = lane & 1;
+    const size_t col = act_col_off(j, epi.TMo);
+    for (int c0 = 0; c0 < TM; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(d + (uint32_t)c0, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float ve = __uint_as_float(v[2 * t]), vo = __uint_as_float(v[2 * t + 1]);
+        const float mine = odd ? vo : ve, send = odd ? ve : vo;
+        const float other = __shfl_xor_sync(0xffffffffu, send, 1);
+        const float g = odd ? other : mine, up = odd ? mine : other;
+        const int m = m_tile * TM + c0 + 2 * t + (odd ? 1 : 0);
+        if (m < M) epi.silu_out[act_row_off(m, epi.ffn, epi.TMo) + col] = f2bf(silu_f(g) * up);
+      }
+    }
+    return;
+  }
+  const int n = n_tile * 128 + quad * 32 + lane;
+  for (int c0 = 0; c0 < TM; c0 += 16) {
+    uint32_t v[16];
+    tmem_ld16(d + (uint32_t)c0, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int m = m_tile * TM + c0 + j;
+      if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
+    }
+  }
+}
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
                 float* __restrict__ out, int stages, GemmEpi epi) {
@@ -183,42 +224,9 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
       const int slot = plan.aligned ? 0 : cta - plan_cta_of(plan, (int64_t)t * nk);
-      const int n = n_tile * 128 + quad * 32 + lane;
       float* o = out + (size_t)slot * M * N;
       const uint32_t d = tmem_base + acc * tm_cols + ((uint32_t)(quad * 32) << 16);
-      if (epi.silu_out) {
-        // fused SiLU: lanes 2i / 2i+1 hold gate / up of FFN column
-        // j = 64 n_tile + (row >> 1) (interleaved storage, gate_col); per
-        // token pair the even lane computes token 2t, the odd lane 2t + 1
-        const int j = n_tile * 64 + ((quad * 32 + lane) >> 1);
-        const bool odd = lane & 1;
-        const size_t col = act_col_off(j, epi.TMo);
-        for (int c0 = 0; c0 < TM; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(d + (uint32_t)c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float ve = __uint_as_float(v[2 * t]), vo = __uint_as_float(v[2 * t + 1]);
-            const float mine = odd ? vo : ve, send = odd ? ve : vo;
-            const float other = __shfl_xor_sync(0xffffffffu, send, 1);
-            const float g = odd ? other : mine, up = odd ? mine : other;
-            const int m = m_tile * TM + c0 + 2 * t + (odd ? 1 : 0);
-            if (m < M) epi.silu_out[act_row_off(m, epi.ffn, epi.TMo) + col] = f2bf(silu_f(g) * up);
-          }
-        }
-      } else {
-        for (int c0 = 0; c0 < TM; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(d + (uint32_t)c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int m = m_tile * TM + c0 + j;
-            if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
-          }
-        }
-      }
+      epilogue_tile(d, quad, lane, n_tile, m_tile, M, N, TM, o, epi);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -280,7 +288,7 @@ __device__ __forceinline__ uint32_t w8_pair(uint32_t word, int e, float s) {
 template <int kG, int kGPS, int kBits>
 __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
-                        float* __restrict__ out, int bstages, int rstages, int astages, int dbg) {
+                        float* __restrict__ out, int bstages, int rstages, int astages, int dbg, GemmEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -495,19 +503,9 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
       tc_fence_after();
       const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
       const int slot = plan.aligned ? 0 : cta - plan_cta_of(plan, (int64_t)t * nk);
-      const int n = n_tile * 128 + quad * 32 + lane;
       float* o = out + (size_t)slot * M * N;
       const uint32_t d = tmem_base + acc * tm_cols + ((uint32_t)(quad * 32) << 16);
-      for (int c0 = 0; c0 < TM; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(d + (uint32_t)c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = m_tile * TM + c0 + j;
-          if (m < M) o[(size_t)m * N + n] = __uint_as_float(v[j]);
-        }
-      }
+      epilogue_tile(d, quad, lane, n_tile, m_tile, M, N, TM, o, epi);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -677,7 +675,7 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, int wkind, int num_sms, size_
 
 template <int kG, int kGPS, int kBits>
 static cudaError_t launch_q_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                 float* out, cudaStream_t stream) {
+                                 float* out, cudaStream_t stream, const GemmEpi& epi) {
   int rs = 0, as = 0;
   size_t sm = 0;
   const int bs = pick_q_stages(TM, kGPS, kBits, &rs, &as, &sm);
@@ -688,30 +686,30 @@ static cudaError_t launch_q_tmem(const GemmWeights& w, const uint16_t* x, int M,
     attr = true;
   }
   return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS, kBits>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M,
-                    TM, plan, out, bs, rs, as, gemm_debug());
+                    TM, plan, out, bs, rs, as, gemm_debug(), epi);
 }
 
 // Three dequantiser groups (fastest in the 7B step), two when TMEM holds only
 // two A stages (a group holds one stage).
 template <int kGPS, int kBits>
 static cudaError_t launch_q_groups(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
-                                   float* out, cudaStream_t stream) {
+                                   float* out, cudaStream_t stream, const GemmEpi& epi) {
   int rs = 0, as = 0;
   size_t sm = 0;
   pick_q_stages(TM, kGPS, kBits, &rs, &as, &sm);
-  if (as >= 3) return launch_q_tmem<3, kGPS, kBits>(w, x, M, TM, plan, out, stream);
-  return launch_q_tmem<2, kGPS, kBits>(w, x, M, TM, plan, out, stream);
+  if (as >= 3) return launch_q_tmem<3, kGPS, kBits>(w, x, M, TM, plan, out, stream, epi);
+  return launch_q_tmem<2, kGPS, kBits>(w, x, M, TM, plan, out, stream, epi);
 }
 
 cudaError_t gemm_launch(const GemmWeights& w, int wkind, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                         float* out, cudaStream_t stream, const GemmEpi& epi) {
-  // the fused SiLU epilogue needs whole tiles (one slot) of the BF16 kernel
-  if (epi.silu_out && (wkind != 16 || !plan.aligned)) return cudaErrorInvalidValue;
-  if (wkind == 8) return launch_q_groups<1, 8>(w, x, M, TM, plan, out, stream);
+  // the fused SiLU epilogue needs whole tiles (one slot)
+  if (epi.silu_out && !plan.aligned) return cudaErrorInvalidValue;
+  if (wkind == 8) return launch_q_groups<1, 8>(w, x, M, TM, plan, out, stream, epi);
   if (wkind == 4) {
     // the plan fixed the unit: K / nk = 256 -> two K groups per pipeline unit
-    if (w.K / plan.nk == 256) return launch_q_groups<2, 4>(w, x, M, TM, plan, out, stream);
-    return launch_q_groups<1, 4>(w, x, M, TM, plan, out, stream);
+    if (w.K / plan.nk == 256) return launch_q_groups<2, 4>(w, x, M, TM, plan, out, stream, epi);
+    return launch_q_groups<1, 4>(w, x, M, TM, plan, out, stream, epi);
   }
   if (wkind != 16) return cudaErrorInvalidValue;
   static const int max_st = [] {  // (experiments) ring depth cap

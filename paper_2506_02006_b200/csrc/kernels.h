@@ -100,7 +100,7 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, int wkind, int num_sms, size_
 __host__ __device__ inline int gate_col(int j) { return ((j >> 6) << 7) + ((j & 63) << 1); }  // up: + 1
 cudaError_t interleave_gate_up_launch(const uint16_t* w, int ffn, int K, uint16_t* out, cudaStream_t s);
 
-// Optional fused epilogue of the BF16 GEMM (whole-tile plans, one slot):
+// Optional fused epilogue of the GEMMs (whole-tile plans, one slot):
 // silu_out != nullptr -> the tile's (gate, up) lane pairs become
 // bf16(silu(gate) * up) in the packed activation image [M x ffn] (token tile TMo)
 // instead of fp32 partials.
