@@ -107,6 +107,13 @@ int ms_variant_export(ms_ctx* ctx, int layer, int bits, void* host_out, int64_t 
  * compute-stream fence).  Validation mirrors begin_swap (range, double swap,
  * no-op) with MS_EVALIDATION. */
 int ms_swap_begin(ms_ctx* ctx, int layer, int bits, uint64_t* ticket);
+/* Peer fetch: the same swap, with the image copied from
+ * `src`, another context of this process with the same model geometry that
+ * holds `layer` committed at `bits` (device to device, cudaMemcpyPeerAsync --
+ * NVLink 5 between B200s -- instead of the pinned host store over PCIe).
+ * src's copy of the layer stays resident until the fetch completes (a later
+ * commit on src waits for it).  Poll / wait / commit with the ticket as usual. */
+int ms_swap_begin_peer(ms_ctx* ctx, int layer, int bits, ms_ctx* src, uint64_t* ticket);
 int ms_swap_poll(ms_ctx* ctx, uint64_t ticket, int* done);
 int ms_swap_wait(ms_ctx* ctx, uint64_t ticket, float* upload_ms);
 int ms_swap_commit(ms_ctx* ctx, uint64_t ticket, int64_t* pages_freed);

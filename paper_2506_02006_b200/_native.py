@@ -64,6 +64,7 @@ SIGNATURES = [
     ("ms_variant_export", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64]),
     ("ms_variant_register", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64, C.c_int]),
     ("ms_swap_begin", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
+    ("ms_swap_begin_peer", C.c_int, [_P, C.c_int, C.c_int, _P, C.POINTER(C.c_uint64)]),
     ("ms_swap_poll", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int)]),
     ("ms_swap_wait", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_float)]),
     ("ms_swap_commit", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int64)]),

@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -30,6 +32,10 @@
 namespace {
 
 thread_local std::string g_err;
+
+// live contexts of this process (peer fetches reference each other's layers)
+std::mutex g_ctx_mu;
+std::set<ms_ctx*> g_ctxs;
 
 struct MsError {
   int code;
@@ -147,6 +153,10 @@ struct Layer {
   uint64_t ticket = 0;
   std::vector<int32_t> new_pages;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  // peer fetches reading this layer's resident image (ms_swap_begin_peer on
+  // another context): its pages are not released before these complete
+  // (event owned by the reading context; dropped when that context dies)
+  std::vector<std::pair<cudaEvent_t, const ms_ctx*>> peer_reads;
   // pinned host variant store
   uint8_t* host_img[kVariants] = {};  // by variant_of(bits)
   // caller-registered images (ms_variant_register): not freed here; `ready`
@@ -806,6 +816,10 @@ int ms_ctx_create(int device, const ms_model_desc* desc, ms_ctx** out) {
       ms_ctx_destroy(c);
       throw;
     }
+    {
+      std::lock_guard<std::mutex> lk(g_ctx_mu);
+      g_ctxs.insert(c);
+    }
     *out = c;
   });
 }
@@ -815,6 +829,20 @@ int ms_ctx_destroy(ms_ctx* c) {
   cudaSetDevice(c->device);
   if (c->compute) cudaStreamSynchronize(c->compute);
   if (c->copy) cudaStreamSynchronize(c->copy);
+  {
+    // peer fetches: this context's copies are done (copy stream synced); drop
+    // its read events from the layers it read, and wait for other contexts
+    // still reading this context's layers
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    g_ctxs.erase(c);
+    for (ms_ctx* o : g_ctxs)
+      for (auto& L : o->layers)
+        L.peer_reads.erase(std::remove_if(L.peer_reads.begin(), L.peer_reads.end(),
+                                          [c](const std::pair<cudaEvent_t, const ms_ctx*>& pr) { return pr.second == c; }),
+                           L.peer_reads.end());
+    for (auto& L : c->layers)
+      for (auto& pr : L.peer_reads) cudaEventSynchronize(pr.first);
+  }
   for (auto& L : c->layers) {
     for (int s = 0; s < kVariants; ++s) {
       cudaFree(L.d_table[s]);
@@ -1059,6 +1087,60 @@ int ms_swap_begin(ms_ctx* c, int layer, int bits, uint64_t* ticket) {
   });
 }
 
+// LayerSwapper, peer fetch: the variant image is copied
+// from another context that holds this layer committed at `bits` (device to
+// device, cudaMemcpyPeerAsync: NVLink between GPUs of one process) instead of
+// uploaded from pinned host memory.  Poll / wait / commit as for ms_swap_begin.
+int ms_swap_begin_peer(ms_ctx* c, int layer, int bits, ms_ctx* src, uint64_t* ticket) {
+  return guard([&] {
+    if (!src || src == c) fail(MS_EVALIDATION, "begin_swap_peer: bad source context");
+    if (layer < 0 || layer >= c->desc.num_layers) fail(MS_EVALIDATION, "begin_swap_peer: layer out of range");
+    const ms_model_desc &a = c->desc, &b = src->desc;
+    if (a.num_layers != b.num_layers || a.hidden != b.hidden || a.num_heads != b.num_heads ||
+        a.num_kv_heads != b.num_kv_heads || a.head_dim != b.head_dim || a.ffn != b.ffn ||
+        a.block_tokens != b.block_tokens || c->page_bytes != src->page_bytes)
+      fail(MS_EVALIDATION, "begin_swap_peer: source context has a different model geometry");
+    Layer& L = c->layers[layer];
+    Layer& S = src->layers[layer];
+    if (L.in_flight) fail(MS_EVALIDATION, "begin_swap: swap already in flight on layer");
+    if (!valid_bits(bits)) fail(MS_EVALIDATION, "begin_swap: bits must be 16, 8, 4 or 3");
+    if (L.bits == bits) fail(MS_EVALIDATION, "begin_swap: layer already at target precision");
+    if (!c->weights_ready || !src->weights_ready) fail(MS_EVALIDATION, "weights not initialised");
+    if (S.in_flight || S.bits != bits)
+      fail(MS_EVALIDATION, "begin_swap_peer: source layer is not committed at " + std::to_string(bits) + " bits");
+    CK(cudaSetDevice(c->device));
+    if (src->device != c->device) {
+      int ok = 0;
+      CK(cudaDeviceCanAccessPeer(&ok, c->device, src->device));
+      if (!ok) fail(MS_ERUNTIME, "begin_swap_peer: no peer access between the devices");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else CK(e);
+    }
+    const ImageGeom& g = geom_of(c, bits);
+    if (L.last_release) CK(cudaStreamWaitEvent(c->copy, L.last_release, 0));
+    L.new_pages = take_pages(c, g.pages, c->copy);
+    CK(cudaEventRecord(L.ev_start, c->copy));
+    write_table(c, L, variant_of(bits), L.new_pages, c->copy);
+    for (int64_t p = 0; p < g.pages; ++p) {
+      const int64_t bytes = std::min<int64_t>(g.cpp, g.total_chunks - p * g.cpp) * g.chunk_bytes;
+      CK(cudaMemcpyPeerAsync(c->arena + (int64_t)L.new_pages[p] * c->page_bytes, c->device,
+                             src->arena + (int64_t)S.pages[p] * src->page_bytes, src->device, (size_t)bytes, c->copy));
+    }
+    CK(cudaEventRecord(L.ev_done, c->copy));
+    cudaEvent_t rd = new_event(c);
+    CK(cudaEventRecord(rd, c->copy));
+    {
+      std::lock_guard<std::mutex> lk(g_ctx_mu);
+      S.peer_reads.push_back({rd, c});
+    }
+    L.in_flight = true;
+    L.to_bits = bits;
+    L.ticket = (c->next_ticket++ << 16) | (uint64_t)layer;
+    *ticket = L.ticket;
+  });
+}
+
 namespace {
 Layer& ticket_layer(ms_ctx* c, uint64_t ticket) {
   const int layer = (int)(ticket & 0xFFFF);
@@ -1099,6 +1181,11 @@ int ms_swap_commit(ms_ctx* c, uint64_t ticket, int64_t* pages_freed) {
     // Token-boundary flip: steps launched from now on use the new image; the
     // compute stream orders them after the upload (no host sync, no flush).
     CK(cudaStreamWaitEvent(c->compute, L.ev_done, 0));
+    {  // another context may still be copying the old image
+      std::lock_guard<std::mutex> lk(g_ctx_mu);
+      for (auto& pr : L.peer_reads) CK(cudaEventSynchronize(pr.first));
+      L.peer_reads.clear();
+    }
     cudaEvent_t fence = compute_fence(c);  // after every step that read the old image
     const int64_t freed = (int64_t)L.pages.size();
     give_pages(c, L.pages, fence);

@@ -121,6 +121,13 @@ class DeviceModel:
         N.check(self.lib.ms_swap_begin(self.h, layer, bits, C.byref(t)))
         return SwapTicket(layer, bits, t.value)
 
+    def swap_begin_peer(self, layer: int, bits: int, src: "DeviceModel") -> SwapTicket:
+        """Swap with the image copied from another context that holds the layer at
+        `bits` (ms_swap_begin_peer: device to device / NVLink instead of host PCIe)."""
+        t = C.c_uint64()
+        N.check(self.lib.ms_swap_begin_peer(self.h, layer, bits, src.h, C.byref(t)))
+        return SwapTicket(layer, bits, t.value)
+
     def swap_done(self, t: SwapTicket) -> bool:
         d = C.c_int()
         N.check(self.lib.ms_swap_poll(self.h, t.ticket, C.byref(d)))

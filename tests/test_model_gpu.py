@@ -248,3 +248,59 @@ def test_multilevel_variants_decode_matches_oracle():
     finally:
         ref.close()
         m.close()
+
+
+def test_peer_fetch_swap_matches_host_upload():
+    """LayerSwapper peer fetch (ms_swap_begin_peer): a
+    context takes layer 1's W4 image from another context that holds it
+    committed, device to device (two contexts on the one B200 here; between
+    GPUs the same call goes over NVLink), and decodes exactly like the oracle
+    at that precision; validation refuses a source not at the target
+    precision, and the source keeps serving while it is read."""
+    from paper_2506_02006_b200 import _native as N
+    from paper_2506_02006_b200.device import DeviceModel, layer_pages
+    kw = dict(max_batch=4, max_prefill_tokens=64, max_pos=128, arena_pages=300)
+    src, dst = DeviceModel(TINY, **kw), DeviceModel(TINY, **kw)
+    ref = O.RefModel(dict(TINY, max_pos=128), 7)
+    try:
+        src.weights_synthetic(7)
+        dst.weights_synthetic(7)
+        with pytest.raises(N.MsError):
+            dst.swap_begin_peer(1, 4, src)  # source layer still BF16
+        t = src.swap_begin(1, 4)
+        src.swap_wait(t)
+        src.swap_commit(t)
+        t = dst.swap_begin_peer(1, 4, src)
+        dst.swap_wait(t)
+        assert dst.swap_commit(t) == layer_pages(TINY, 16)
+        assert dst.layer_bits(1) == 4
+        ref.set_precision(1, 4)
+        # the source swaps the layer back while nothing reads it any more
+        t = src.swap_begin(1, 16)
+        src.swap_wait(t)
+        src.swap_commit(t)
+        dst.hist_reserve(2, 128)
+        dst.kv_attach(0, 16)
+        table = np.arange(16, dtype=np.int64).reshape(2, 8)
+        prompts = (np.arange(2 * 16, dtype=np.int32).reshape(2, 16) * 71) % TINY["V"]
+        seqs = [ref.new_seq(128) for _ in range(2)]
+        toks = []
+        for b in range(2):
+            dst.hist_write(b, 0, prompts[b])
+            tk, lg = dst.prefill(b, 16, table[b], want_logits=True)
+            _, rl = ref.prefill(seqs[b], prompts[b])
+            _check_logits(lg, rl)
+            toks.append(tk)
+        toks = np.array(toks, np.int32)
+        pos = np.full(2, 16, np.int32)
+        for _ in range(6):
+            got, lg = dst.decode(np.arange(2), pos, table, want_logits=True)
+            _, rl = ref.forward(seqs, toks)
+            for b in range(2):
+                _check_logits(lg[b], rl[b])
+            toks = got
+            pos += 1
+    finally:
+        ref.close()
+        dst.close()
+        src.close()
