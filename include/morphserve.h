@@ -160,6 +160,13 @@ typedef struct {
   int32_t max_blocks;
 } ms_decode_batch;
 int ms_decode_step(ms_ctx* ctx, const ms_decode_batch* batch, int32_t* next_out, float* logits_out);
+/* Caller-supplied stream: from now on every decode step and
+ * prefill is ordered after the work already enqueued on `stream` (a
+ * cudaStream_t of the context's device; NULL = none), and `stream` waits for
+ * the step's completion, so caller kernels before / after a step see its
+ * inputs / outputs without a host synchronisation.  The steps themselves run
+ * on the context's compute stream (their CUDA graphs are captured there). */
+int ms_set_stream(ms_ctx* ctx, void* stream);
 /* Pipelined form of ms_decode_step: submit enqueues the step (its inputs are
  * staged at once, its next tokens copied back asynchronously) and returns; the
  * host may run one step ahead.  collect waits for the OLDEST submitted step and

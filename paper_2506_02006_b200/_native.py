@@ -79,6 +79,7 @@ SIGNATURES = [
     ("ms_hist_reserve", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("ms_hist_write", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]),
     ("ms_hist_read", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]),
+    ("ms_set_stream", C.c_int, [_P, _P]),
     ("ms_decode_step", C.c_int, [_P, C.POINTER(DecodeBatch), C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
     ("ms_decode_submit", C.c_int, [_P, C.POINTER(DecodeBatch)]),
     ("ms_decode_collect", C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),

@@ -248,6 +248,10 @@ struct ms_ctx {
   int32_t* h_next = nullptr;   // pinned
   float* h_logits = nullptr;   // pinned
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
+  // caller stream (ms_set_stream): steps order after its prior work and it
+  // waits for each step's completion
+  cudaStream_t user = nullptr;
+  cudaEvent_t ev_user_in = nullptr, ev_user_out = nullptr;
 
   int32_t* hist = nullptr;
   int32_t hist_slots = 0, hist_len = 0;
@@ -867,6 +871,8 @@ int ms_ctx_destroy(ms_ctx* c) {
   if (c->trace_h) cudaFree(c->trace_h);
   if (c->tm0) cudaEventDestroy(c->tm0);
   if (c->tm1) cudaEventDestroy(c->tm1);
+  if (c->ev_user_in) cudaEventDestroy(c->ev_user_in);
+  if (c->ev_user_out) cudaEventDestroy(c->ev_user_out);
   if (c->ev_step0) cudaEventDestroy(c->ev_step0);
   if (c->ev_step1) cudaEventDestroy(c->ev_step1);
   void* dev[] = {c->arena, c->embed, c->normf, c->norms, c->lm_packed, c->lm_table, c->rope_cos, c->rope_sin,
@@ -1323,6 +1329,18 @@ int ms_hist_read(ms_ctx* c, int32_t slot, int32_t offset, int32_t* host_out, int
 // -------------------------------------------------------------------- steps
 namespace {
 // Enqueue one decode step; returns the staging slot used.
+// caller-stream ordering around a step (no-ops without ms_set_stream)
+void user_enter(ms_ctx* c) {
+  if (!c->user) return;
+  CK(cudaEventRecord(c->ev_user_in, c->user));
+  CK(cudaStreamWaitEvent(c->compute, c->ev_user_in, 0));
+}
+void user_leave(ms_ctx* c) {
+  if (!c->user) return;
+  CK(cudaEventRecord(c->ev_user_out, c->compute));
+  CK(cudaStreamWaitEvent(c->user, c->ev_user_out, 0));
+}
+
 int decode_enqueue(ms_ctx* c, const ms_decode_batch* b, bool want_logits) {
     check_ready(c);
     const int n = b->n;
@@ -1348,6 +1366,7 @@ int decode_enqueue(ms_ctx* c, const ms_decode_batch* b, bool want_logits) {
       for (int j = 0; j < nb; ++j) row[j] = page_of(c, b->block_ids[(size_t)i * b->max_blocks + j]);
     }
     CK(cudaSetDevice(c->device));
+    user_enter(c);
     CK(cudaEventRecord(c->ev_step0, c->compute));
     stage_in(c, st, (size_t)n * (4 + mb));
     CK(cudaEventRecord(st.used, c->compute));
@@ -1417,9 +1436,21 @@ int decode_enqueue(ms_ctx* c, const ms_decode_batch* b, bool want_logits) {
       forward(c, n, TM, d_slot, d_pos, d_ctx, nullptr, d_pages, nullptr, mb, max_ctx, 0, want_logits);
     }
     CK(cudaEventRecord(c->ev_step1, c->compute));
+    user_leave(c);
     return (int)(&st - c->ring);
 }
 }  // namespace
+
+int ms_set_stream(ms_ctx* c, void* stream) {
+  return guard([&] {
+    CK(cudaSetDevice(c->device));
+    if (!c->ev_user_in) {
+      CK(cudaEventCreateWithFlags(&c->ev_user_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_user_out, cudaEventDisableTiming));
+    }
+    c->user = static_cast<cudaStream_t>(stream);
+  });
+}
 
 int ms_decode_step(ms_ctx* c, const ms_decode_batch* b, int32_t* next_out, float* logits_out) {
   return guard([&] {
@@ -1488,6 +1519,7 @@ int ms_prefill(ms_ctx* c, int32_t slot, int32_t n_tokens, const int64_t* block_i
     int32_t* row = hs + 4 * n;
     for (int j = 0; j < nb; ++j) row[j] = page_of(c, block_ids[j]);
     CK(cudaSetDevice(c->device));
+    user_enter(c);
     CK(cudaEventRecord(c->ev_step0, c->compute));
     stage_in(c, st, (size_t)n * 4 + mb);
     CK(cudaEventRecord(st.used, c->compute));
@@ -1496,6 +1528,7 @@ int ms_prefill(ms_ctx* c, int32_t slot, int32_t n_tokens, const int64_t* block_i
     forward(c, n, TM, st.d, st.d + n, st.d + 2 * n, nullptr, st.d + 4 * n, st.d + 3 * n, 0, n, n - 1,
             logits_out != nullptr);
     CK(cudaEventRecord(c->ev_step1, c->compute));
+    user_leave(c);
     if (next_out || logits_out) {
       if (next_out) CK(cudaMemcpyAsync(c->h_next, c->next, 4, cudaMemcpyDeviceToHost, c->compute));
       if (logits_out)

@@ -121,6 +121,10 @@ class DeviceModel:
         N.check(self.lib.ms_swap_begin(self.h, layer, bits, C.byref(t)))
         return SwapTicket(layer, bits, t.value)
 
+    def set_stream(self, stream_ptr: int | None):
+        """Order steps after / before the caller's CUDA stream (ms_set_stream)."""
+        N.check(self.lib.ms_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
     def swap_begin_peer(self, layer: int, bits: int, src: "DeviceModel") -> SwapTicket:
         """Swap with the image copied from another context that holds the layer at
         `bits` (ms_swap_begin_peer: device to device / NVLink instead of host PCIe)."""

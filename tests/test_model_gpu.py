@@ -304,3 +304,43 @@ def test_peer_fetch_swap_matches_host_upload():
         ref.close()
         dst.close()
         src.close()
+
+
+def test_caller_stream_orders_steps():
+    """ms_set_stream (SURVEY 8(b) caller-supplied stream): a decode step submitted
+    after work on the caller's stream starts only when that work is done, and
+    the caller's stream waits for the step; results equal the unbound run."""
+    torch = pytest.importorskip("torch")
+    from paper_2506_02006_b200.device import DeviceModel
+    dev = DeviceModel(TINY, max_batch=4, max_prefill_tokens=64, max_pos=128, arena_pages=300)
+    try:
+        dev.weights_synthetic(7)
+        dev.hist_reserve(2, 128)
+        dev.kv_attach(0, 16)
+        table = np.arange(16, dtype=np.int64).reshape(2, 8)
+        prompts = (np.arange(2 * 16, dtype=np.int32).reshape(2, 16) * 29) % TINY["V"]
+        for b in range(2):
+            dev.hist_write(b, 0, prompts[b])
+            dev.prefill(b, 16, table[b])
+        pos = np.full(2, 16, np.int32)
+        want = dev.decode(np.arange(2), pos, table, want_next=True, tokens=np.array([5, 7], np.int32))[0]
+        s = torch.cuda.Stream()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        dev.set_stream(s.cuda_stream)
+        with torch.cuda.stream(s):
+            e0.record()
+            torch.cuda._sleep(40_000_000)  # ~20 ms of caller work
+            e1.record()
+        dev.decode_submit(np.arange(2), pos, table, tokens=np.array([5, 7], np.int32))
+        with torch.cuda.stream(s):
+            e2.record()  # after the step (the caller stream waits for it)
+        got = dev.decode_collect()
+        torch.cuda.synchronize()
+        dev.set_stream(None)
+        assert np.array_equal(got[:2], want)
+        sleep_ms, total_ms = e0.elapsed_time(e1), e0.elapsed_time(e2)
+        assert sleep_ms > 5.0 and total_ms > sleep_ms
+        t0 = dev.last_step_ms()
+        assert total_ms >= sleep_ms + 0.5 * t0
+    finally:
+        dev.close()
