@@ -38,6 +38,7 @@ SHAPE = dict(L=32, d=4096, H=32, KVH=32, hd=128, ffn=11008, V=32000)
 BATCH = 64
 CTX = 2048
 W4_LAYERS = [24, 14, 10, 20, 4, 19, 11, 5]  # reference LIS order[0..7]
+VARIANTS = (16, 4)  # precision levels of the variant store (tools/step_ab.py --bits 8 adds Q8)
 METRIC = "decode tok/s/GPU + P95 TTFT, 7B mixed W4A16/BF16, bursty trace, 1-8 B200"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
@@ -191,7 +192,7 @@ def build_model(local_rank: int, world: int, extra_steps: int):
     # N > 1: one box-wide host copy of the variant store
     dev, store = replica_device(SHAPE, local_rank=local_rank, world=world, barrier=lambda: dist_barrier(world),
                                 key="7b", max_batch=128, max_prefill_tokens=1024, max_pos=CTX + extra_steps + 32,
-                                arena_pages=kv_pages + w_pages + staging)
+                                arena_pages=kv_pages + w_pages + staging, variants=VARIANTS)
     dev.variant_store = store
     dev.hist_reserve(BATCH, CTX + extra_steps + 33)
     dev.kv_attach(0, kv_pages)

@@ -16,10 +16,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def child(steps, w4s, shape, prof, order_kind, reps):
+def child(steps, w4s, shape, prof, order_kind, reps, bits=4):
     import numpy as np
 
     import bench
+    if bits != 4:
+        bench.VARIANTS = (16, bits, 4)
     if shape == "8b":
         from paper_2506_02006_b200.device import LLAMA3_8B
         bench.SHAPE = dict(LLAMA3_8B)
@@ -43,7 +45,7 @@ def child(steps, w4s, shape, prof, order_kind, reps):
                 dev.swap_wait(t)
                 dev.swap_commit(t)
             for l in sorted(want - cur):
-                t = dev.swap_begin(l, 4)
+                t = dev.swap_begin(l, bits)
                 dev.swap_wait(t)
                 dev.swap_commit(t)
             cur = want
@@ -79,11 +81,12 @@ def main():
     ap.add_argument("--child", action="store_true")
     ap.add_argument("--order", default="lis", help="lis | seq | comma-separated layer list")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--bits", type=int, default=4, help="level of the swapped layers (8, 4, 3)")
     ap.add_argument("configs", nargs="*", default=["base:"])
     a = ap.parse_args()
     w4s = [int(x) for x in a.w4.split(",")]
     if a.child:
-        child(a.steps, w4s, a.shape, a.prof, a.order, a.reps)
+        child(a.steps, w4s, a.shape, a.prof, a.order, a.reps, a.bits)
         return
     for cfg in a.configs:
         name, _, kv = cfg.partition(":")
@@ -92,7 +95,7 @@ def main():
             k, _, v = item.partition("=")
             env[k] = v
         cmd = [sys.executable, __file__, "--child", "--steps", str(a.steps), "--w4", a.w4, "--shape", a.shape,
-               "--order", a.order, "--reps", str(a.reps)]
+               "--order", a.order, "--reps", str(a.reps), "--bits", str(a.bits)]
         if a.prof:
             cmd.append("--prof")
         r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
