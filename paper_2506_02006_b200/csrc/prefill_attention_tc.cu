@@ -368,14 +368,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 128; ++j)
           if (key0 + j > qrow || key0 + j >= n) v[j] = __float_as_uint(-INFINITY);
       }
-      float m4[4];  // four independent chains
+      // One pass while the running max holds: exp2 against the current max
+      // (lazy rescaling keeps it unless a tile's max exceeds it by 2^8),
+      // tracking this tile's max alongside.  A row whose max moved (the first
+      // tile always) takes the second pass below with the new max, reloading
+      // its scores from TMEM (P has not been stored yet).
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if (kt > 0) {
+        const float msub = m_run;  // finite after the first tile
 #pragma unroll
-      for (int k = 0; k < 4; ++k) m4[k] = __uint_as_float(v[k]);
+        for (int j = 0; j < 128; j += 2) {
+          const float s0 = __uint_as_float(v[j]), s1 = __uint_as_float(v[j + 1]);
+          m4[(j >> 1) & 3] = fmaxf(m4[(j >> 1) & 3], fmaxf(s0, s1));
+          const float p0 = ex2(fmaf(s0, sl, -msub));
+          const float p1 = ex2(fmaf(s1, sl, -msub));
+          ps[(j >> 1) & 3] += p0 + p1;
+          v[j >> 1] = cvt_bf2(p0, p1);  // packed P, in place (index j/2 <= j)
+        }
+      } else {
 #pragma unroll
-      for (int j = 4; j < 128; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
+        for (int j = 0; j < 128; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
+      }
       const float m_tile = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl;
-      const bool move = m_tile > m_run + kRescaleLog2;  // false while both are -inf
-      const float m_new = move ? m_tile : m_run;
+      const bool move = kt == 0 || m_tile > m_run + kRescaleLog2;
+      const float m_new = move ? (m_tile > m_run ? m_tile : m_run) : m_run;
       const float corr = (move && m_run != -INFINITY) ? ex2(m_run - m_new) : 1.f;
       if (kt > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
         // O_X holds PV_X(0 .. kt-1), all complete (covered by this S's commit)
@@ -389,16 +406,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32p(ocol + c0, o);
         }
       }
-      m_run = m_new;
-      const float msub = m_new == -INFINITY ? 0.f : m_new;
-      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      if (__any_sync(0xffffffffu, move)) {
+        // second pass (rows whose max moved, e.g. every row of the first
+        // tile): the scores again from TMEM, 64 columns at a time (registers)
+        const float msub = m_new == -INFINITY ? 0.f : m_new;
+        if (move) {
 #pragma unroll
-      for (int j = 0; j < 128; j += 2) {
-        const float p0 = ex2(fmaf(__uint_as_float(v[j]), sl, -msub));
-        const float p1 = ex2(fmaf(__uint_as_float(v[j + 1]), sl, -msub));
-        ps[(j >> 1) & 3] += p0 + p1;
-        v[j >> 1] = cvt_bf2(p0, p1);  // packed P, in place (index j/2 <= j)
+          for (int k = 0; k < 4; ++k) ps[k] = 0.f;
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t w[64];
+          tmem_ld32(scol + hh * 64, w);
+          tmem_ld32(scol + hh * 64 + 32, w + 32);
+          tmem_ld_wait();
+          if (move) {
+            if (kt == nk - 1) {
+              const int key0 = kt * kTcTile + hh * 64;
+#pragma unroll
+              for (int j = 0; j < 64; ++j)
+                if (key0 + j > qrow || key0 + j >= n) w[j] = __float_as_uint(-INFINITY);
+            }
+#pragma unroll
+            for (int j = 0; j < 64; j += 2) {
+              const float p0 = ex2(fmaf(__uint_as_float(w[j]), sl, -msub));
+              const float p1 = ex2(fmaf(__uint_as_float(w[j + 1]), sl, -msub));
+              ps[(j >> 1) & 3] += p0 + p1;
+              v[hh * 32 + (j >> 1)] = cvt_bf2(p0, p1);
+            }
+          }
+        }
       }
+      m_run = m_new;
       l_run = l_run * corr + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
       tmem_st32p(scol, v);  // P over S: 64 columns of bf16 pairs
       tmem_st32p(scol + 32, v + 32);
