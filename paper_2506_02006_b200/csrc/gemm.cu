@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // MS_GEMM_DEBUG (experiments only): bit0 skip activation loads, bit1 skip MMAs,
+// bit3 CTA-0 timeline, bit4 producer stamps, bit5 one raw-chunk producer,
 // bit2 (W4 TMEM) skip the dequant ALU work and TMEM stores.
 static int gemm_debug() {
   static const int v = [] {
@@ -258,7 +259,11 @@ static int gemm_debug() {
 //   warps 2..5      epilogue (TMEM accumulators -> fp32 partials)
 //   warp 6 lane 0   activation (B) ring, after the grid dependency (own warp:
 //                   two spin-waiting roles in one warp serialise each other)
-//   warps 7..       kG dequantiser groups of 4 warps: warp w writes TMEM lanes
+//   warp 7 lane 0   second raw-chunk producer: warps 0 and 7 issue alternate
+//                   units (one thread's issue rate -- cursor arithmetic and
+//                   the bulk-copy instruction under the dequantisers' issue
+//                   pressure, ~0.5 us per unit -- capped the weight stream)
+//   warps 8..       kG dequantiser groups of 4 warps: warp w writes TMEM lanes
 //                   32*(w%4).. (its rows); bf16(code*scale) via the 0x4300
 //                   magic, tcgen05.st.32x32b.x32, wait::st, arrive.
 // TMEM: [acc_bufs x TM columns of fp32 accumulators][astages x 64 columns of
@@ -266,6 +271,8 @@ static int gemm_debug() {
 // kG dequantiser groups of 4 warps each keep kG chunks in flight, so the
 // dequant ALU work (~4 instructions per bf16x2) is latency-hidden.
 constexpr int kMaxAStages = 8;
+constexpr int kDqWarp0 = 8;  // first dequantiser warp
+constexpr int kProducers = 2;  // raw-chunk producer threads (warps 0 and 7)
 
 
 // kGPS = 128-wide K groups per pipeline unit (1 or 2): two groups per unit
@@ -286,7 +293,7 @@ __device__ __forceinline__ uint32_t w8_pair(uint32_t word, int e, float s) {
 }
 
 template <int kG, int kGPS, int kBits>
-__global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
+__global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
     gemm_w4_tmem_kernel(GemmWeights W, const uint16_t* __restrict__ X, int M, int TM, GemmPlanDev plan,
                         float* __restrict__ out, int bstages, int rstages, int astages, int dbg, GemmEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -355,16 +362,18 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   ChunkCursor cur(W, (int)chunkB);
   // one unit's kGPS consecutive chunks into raw stage r (one copy when they
   // are contiguous in the same page); leaves the cursor at the next unit
-  auto issue_unit = [&](int r) {
-    mbar_expect_tx(&rfull[r], raw_bytes);
+  auto issue_unit = [&](int r, uint32_t dit) {
     const uint8_t* c0 = cur.get();
     cur.advance();
+    const uint8_t* c1 = kGPS == 1 ? c0 : cur.get();
+    if (kGPS != 1) cur.advance();
+    if (dbg & 16) stamp(1, dit);
+    mbar_expect_tx(&rfull[r], raw_bytes);
+    if (dbg & 16) stamp(2, dit);
     if (kGPS == 1) {
       bulk_g2s(sRaw(r), c0, chunkB, &rfull[r]);
       return;
     }
-    const uint8_t* c1 = cur.get();
-    cur.advance();
     if (c1 == c0 + chunkB) {
       bulk_g2s(sRaw(r), c0, 2 * chunkB, &rfull[r]);
     } else {
@@ -372,19 +381,24 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
       bulk_g2s(sRaw(r) + chunkB, c1, chunkB, &rfull[r]);
     }
   };
+  // decode tiles: only two units ahead of the pipeline start -- the first
+  // chunks then arrive ~1 us sooner (every SM's initial burst queues in HBM
+  // together) and the dequantisers start earlier; measured 2-5% per W4 decode
+  // GEMM isolated, neutral in the step.  Long prefills (compute bound) fill
+  // the whole ring.  Both producer threads need the count.
+  const uint32_t pre_cap = TM <= 128 ? (uint32_t)min(rstages, 2) : (uint32_t)rstages;
+  if (threadIdx.x == (kDqWarp0 - 1) * 32) {
+    SegIter pre(plan, cta);
+    int t, k0, k1;
+    while (npre < pre_cap && pre.next(t, k0, k1)) npre += min((uint32_t)(k1 - k0), pre_cap - npre);
+  }
   if (threadIdx.x == 0) {
     SegIter pre(plan, cta);
     int t, k0, k1;
-    // decode tiles: only two units ahead of the pipeline start -- the first
-    // chunks then arrive ~1 us sooner (every SM's initial burst queues in
-    // HBM together) and the dequantisers start earlier; measured 2-5% per W4
-    // decode GEMM isolated, neutral in the step.  Long prefills (compute
-    // bound) fill the whole ring.
-    const uint32_t pre_cap = TM <= 128 ? (uint32_t)min(rstages, 2) : (uint32_t)rstages;
     while (npre < pre_cap && pre.next(t, k0, k1)) {
       cur.seek(W.first_chunk + (int64_t)(t % plan.n_tiles) * gpr + (int64_t)k0 * kGPS);
       for (int k = k0; k < k1 && npre < pre_cap; ++k, ++npre) {
-        issue_unit((int)npre);
+        issue_unit((int)npre, 64);
         stamp(0, npre);
       }
     }
@@ -397,29 +411,44 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
   const int64_t kb_per_mtile = W.K / 64;
   pdl_trigger();
 
-  if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ producer
+  // (debug, dbg bit5) a single producer thread, for A/B timing
+  const uint32_t nprod = (dbg & 32) ? 1u : (uint32_t)kProducers;
+  if (warp == 0 || warp == kDqWarp0 - 1) {
+    if (lane == 0 && (warp == 0 || nprod > 1)) {
+      // ----------------------------------------------------------- producers
       // raw int4 chunks (independent of the activation ring, so the weight
-      // stream runs `rstages` ahead; weights need no grid dependency)
+      // stream runs `rstages` ahead; weights need no grid dependency).
+      // Producer p issues the units it = p, p + kProducers, ... (after the
+      // pre-issued ones); ring slot / phase kept incrementally.
+      const uint32_t p = warp == 0 ? 0u : 1u;
       SegIter seg(plan, cta);
       int t, k0, k1;
       uint32_t it = 0;
       while (seg.next(t, k0, k1)) {
-        if (it + (uint32_t)(k1 - k0) <= npre) {  // whole segment already issued
-          it += (uint32_t)(k1 - k0);
+        const uint32_t end = it + (uint32_t)(k1 - k0);
+        uint32_t u = it > npre ? it : npre;
+        u += (p + nprod - u % nprod) % nprod;  // first unit of this producer
+        if (u >= end) {
+          it = end;
           continue;
         }
         const int n_tile = t % plan.n_tiles;
-        const int skip = it < npre ? (int)(npre - it) : 0;  // units of this segment already issued
-        it += (uint32_t)skip;
-        cur.seek(W.first_chunk + (int64_t)n_tile * gpr + (int64_t)(k0 + skip) * kGPS);
-        for (int k = k0 + skip; k < k1; ++k, ++it) {
-          const int r = it % rstages;
-          mbar_wait(&rempty[r], ((it / rstages) & 1) ^ 1);
-          issue_unit(r);
-          stamp(0, it);
+        cur.seek(W.first_chunk + (int64_t)n_tile * gpr + (int64_t)(k0 + (int)(u - it)) * kGPS);
+        uint32_t r = u % (uint32_t)rstages, ph = ((u / (uint32_t)rstages) & 1) ^ 1;
+        for (; u < end; u += nprod) {
+          if (dbg & 16) stamp(5, u);
+          mbar_wait(&rempty[r], ph);
+          if (dbg & 16) stamp(3, u);
+          issue_unit((int)r, u);
+          stamp(0, u);
+          for (uint32_t i = 0; i < (nprod - 1) * kGPS; ++i) cur.advance();  // the other producer's units
+          r += nprod;
+          while (r >= (uint32_t)rstages) {
+            r -= (uint32_t)rstages;
+            ph ^= 1;
+          }
         }
+        it = end;
       }
     }
   } else if (warp == 1) {
@@ -479,19 +508,23 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
       SegIter seg(plan, cta);
       int t, k0, k1;
       uint32_t it = 0;
+      uint32_t s = 0, ph = 1;
       while (seg.next(t, k0, k1)) {
         const int m_tile = t / plan.n_tiles;
         const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
         for (int k = k0; k < k1; ++k, ++it) {
-          const int s = it % bstages;
-          if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ((it / bstages) & 1) ^ 1);
+          if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ph);
           if (dbg & 1) {  // (debug) no activation traffic: complete the stage empty
             mbar_expect_tx(&bfull[s], 0);
-            continue;
+          } else {
+            mbar_expect_tx(&bfull[s], 2 * kGPS * b_bytes);
+            bulk_g2s(sB(s), xb + (size_t)(2 * kGPS * k) * b_bytes, 2 * kGPS * b_bytes, &bfull[s]);
           }
-          mbar_expect_tx(&bfull[s], 2 * kGPS * b_bytes);
-          bulk_g2s(sB(s), xb + (size_t)(2 * kGPS * k) * b_bytes, 2 * kGPS * b_bytes, &bfull[s]);
-          stamp(5, it);
+          if (!(dbg & 16)) stamp(5, it);
+          if (++s == (uint32_t)bstages) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
@@ -523,21 +556,35 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
     // chunks are in flight); warp quadrant q owns TMEM lanes / weight rows
     // 32q..32q+31 and dequantises the whole 128-wide group of its row: 64
     // packed bf16x2 columns, two tcgen05.st.32x32b.x32.
-    const int quad = warp & 3, grp = (warp - 7) >> 2;
+    const int quad = warp & 3, grp = (warp - kDqWarp0) >> 2;
     const int row = quad * 32 + lane;
     const __nv_bfloat162 bias = __floats2bfloat162_rn(136.0f, 136.0f);
     const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16) + a_col0;
     SegIter seg(plan, cta);
     int t, k0, k1;
     uint32_t it = 0;
+    // this group's units are it = grp, grp + kG, ...: ring slots and phases
+    // advance by kG (< rstages, astages) per unit, no division in the loop
+    uint32_t rs = (uint32_t)grp, rph = 0, a = (uint32_t)grp, aph = 0;
+    auto adv = [&] {
+      rs += kG;
+      while (rs >= (uint32_t)rstages) {
+        rs -= (uint32_t)rstages;
+        rph ^= 1;
+      }
+      a += kG;
+      if (a >= (uint32_t)astages) {  // kG <= astages (launch_q_groups)
+        a -= (uint32_t)astages;
+        aph ^= 1;
+      }
+    };
     while (seg.next(t, k0, k1)) {
       // first k-step of this segment owned by this group
       int k = k0 + (int)((grp - (int)(it % kG) + kG) % kG);
       it += (uint32_t)(k - k0);
       for (; k < k1; k += kG, it += kG) {
-        const int rs = it % rstages, a = it % astages;
-        mbar_wait(&rfull[rs], (it / rstages) & 1);
-        if (lane == 0 && quad == 0) stamp(1, it);
+        mbar_wait(&rfull[rs], rph);
+        if (lane == 0 && quad == 0 && !(dbg & 16)) stamp(1, it);
         const uint8_t* raw = sRaw(rs);
         constexpr int kQ = kBits == 8 ? 8 : 4;  // uint4 of codes per row per K group
         __nv_bfloat162 sc[kGPS];
@@ -555,12 +602,13 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[rs]);
-        if (it >= (uint32_t)astages) mbar_wait(&aempty[a], ((it / astages) & 1) ^ 1);
-        if (lane == 0 && quad == 0) stamp(2, it);
+        if (it >= (uint32_t)astages) mbar_wait(&aempty[a], aph ^ 1);
+        if (lane == 0 && quad == 0 && !(dbg & 16)) stamp(2, it);
         tc_fence_after();
         if (dbg & 4) {  // (debug) no dequant ALU / TMEM stores: hand the stage straight on
           __syncwarp();
           if (lane == 0) mbar_arrive(&afull[a]);
+          adv();
           continue;
         }
 #pragma unroll
@@ -602,7 +650,8 @@ __global__ void __launch_bounds__((7 + 4 * kG) * 32, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[a]);
-        if (lane == 0 && quad == 0) stamp(3, it);
+        if (lane == 0 && quad == 0 && !(dbg & 16)) stamp(3, it);
+        adv();
       }
       it -= (uint32_t)(k - k1);  // back to the segment end
     }
@@ -691,7 +740,7 @@ static cudaError_t launch_q_tmem(const GemmWeights& w, const uint16_t* x, int M,
                          227 * 1024);
     attr = true;
   }
-  return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS, kBits>, dim3(plan.C), dim3((7 + 4 * kG) * 32), sm, stream, w, x, M,
+  return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS, kBits>, dim3(plan.C), dim3((kDqWarp0 + 4 * kG) * 32), sm, stream, w, x, M,
                     TM, plan, out, bs, rs, as, gemm_debug(), epi);
 }
 
