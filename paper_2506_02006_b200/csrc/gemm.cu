@@ -664,21 +664,33 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
 }
 
 // Ring sizes of the quantised kernel: activation (B) stages, raw chunk
-// stages (the rest of the shared-memory budget), TMEM A stages.
-static int pick_q_stages(int TM, int gps, int bits, int* rstages, int* astages, size_t* smem_out) {
+// stages (the rest of the shared-memory budget), TMEM A stages, dequantiser
+// groups (*groups).  Parity waits are only sound while a barrier is at most
+// one phase behind its waiter, which the sizes guarantee by construction:
+//  - raw stages are even, so with the two producers issuing alternate units
+//    each raw stage is always filled by the same producer (which issued the
+//    stage's previous round itself before waiting on its release);
+//  - raw stages >= groups + A stages: a group starts waiting for unit u
+//    only after finishing u - groups, which needed the MMA of
+//    u - groups - astages, so every unit <= u - rstages has landed.
+static int pick_q_stages(int TM, int gps, int bits, int* rstages, int* astages, int* groups, size_t* smem_out) {
   const size_t budget = 215 * 1024;
   const size_t bst = (size_t)TM * 128 * 2 * gps;
   const size_t raw_stage = bits == 8 ? 16640 : (gps == 1 ? 8576 : 16896);
-  const int bs = gps == 1 ? (TM <= 64 ? 6 : (TM <= 128 ? 4 : 2)) : (TM <= 64 ? 3 : (TM <= 128 ? 2 : 1));
+  const int bs = gps == 1 ? (TM <= 64 ? (bits == 8 ? 4 : 6) : (TM <= 128 ? 4 : 2)) : (TM <= 64 ? 3 : (TM <= 128 ? 2 : 1));
   int rs = (int)((budget - bs * bst) / raw_stage);
   if (rs > 16) rs = 16;
-  if (rs < 2) rs = 2;
-  *rstages = rs;
+  rs &= ~1;
   const int tm_cols = TM <= 32 ? 32 : TM <= 64 ? 64 : TM <= 128 ? 128 : 256;
   const int acc = (TM <= 128 ? 2 : 1) * tm_cols;
-  *astages = std::min(kMaxAStages, (512 - acc) / (64 * gps));
+  const int as_max = std::min(kMaxAStages, (512 - acc) / (64 * gps));
+  // three groups when three A stages and six raw stages fit, else two
+  const int g = as_max >= 3 && rs >= 6 ? 3 : 2;
+  *groups = g;
+  *rstages = rs;
+  *astages = std::min(as_max, rs - g);
   *smem_out = bs * bst + (size_t)rs * raw_stage + (2 * bs + 2 * rs + 2 * kMaxAStages + 4) * 8 + 64;
-  return bs;
+  return *astages >= g && rs >= 2 * g ? bs : -1;
 }
 
 void gemm_inline_pages(GemmWeights& w, int wkind, const uint64_t* host_pages) {
@@ -731,9 +743,10 @@ GemmPlanDev gemm_plan(int N, int K, int M, int TM, int wkind, int num_sms, size_
 template <int kG, int kGPS, int kBits>
 static cudaError_t launch_q_tmem(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                                  float* out, cudaStream_t stream, const GemmEpi& epi) {
-  int rs = 0, as = 0;
+  int rs = 0, as = 0, g = 0;
   size_t sm = 0;
-  const int bs = pick_q_stages(TM, kGPS, kBits, &rs, &as, &sm);
+  const int bs = pick_q_stages(TM, kGPS, kBits, &rs, &as, &g, &sm);
+  if (bs < 0 || g != kG) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG, kGPS, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -744,15 +757,15 @@ static cudaError_t launch_q_tmem(const GemmWeights& w, const uint16_t* x, int M,
                     TM, plan, out, bs, rs, as, gemm_debug(), epi);
 }
 
-// Three dequantiser groups (fastest in the 7B step), two when TMEM holds only
-// two A stages (a group holds one stage).
+// Three dequantiser groups (fastest in the 7B step), two when TMEM or the raw
+// ring holds fewer stages (pick_q_stages).
 template <int kGPS, int kBits>
 static cudaError_t launch_q_groups(const GemmWeights& w, const uint16_t* x, int M, int TM, const GemmPlanDev& plan,
                                    float* out, cudaStream_t stream, const GemmEpi& epi) {
-  int rs = 0, as = 0;
+  int rs = 0, as = 0, g = 0;
   size_t sm = 0;
-  pick_q_stages(TM, kGPS, kBits, &rs, &as, &sm);
-  if (as >= 3) return launch_q_tmem<3, kGPS, kBits>(w, x, M, TM, plan, out, stream, epi);
+  pick_q_stages(TM, kGPS, kBits, &rs, &as, &g, &sm);
+  if (g == 3) return launch_q_tmem<3, kGPS, kBits>(w, x, M, TM, plan, out, stream, epi);
   return launch_q_tmem<2, kGPS, kBits>(w, x, M, TM, plan, out, stream, epi);
 }
 
