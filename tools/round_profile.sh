@@ -13,4 +13,6 @@ ncu --set full --import-source on --clock-control none -k regex:attn_decode_kern
   -o gpurun_out/${TAG}_attn $DEC > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gemm -s 300 -c 8 \
   -o gpurun_out/${TAG}_gemm $DEC > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:gemm_w4 -s 8 -c 4 \
+  -o gpurun_out/${TAG}_gemm_w4 $DEC > /dev/null 2>&1
 ls -la gpurun_out/${TAG}_*
