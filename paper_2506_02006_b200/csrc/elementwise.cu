@@ -5,6 +5,7 @@
 // quantiser/packer).  Each output is written directly in the layout its
 // consumer wants (packed activation images for the next GEMM, KV pages for
 // attention) so no separate layout pass runs per step.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -178,11 +179,15 @@ cudaError_t qkv_post_launch(const float* part, const GemmPlanDev& plan, int M, i
 // One CTA per row; each thread keeps its (up to 8) float4 of the row in
 // registers between the sum of squares and the normalised write, which goes
 // straight into the packed activation image of the next GEMM.
-constexpr int kNormPer = 8;
-__global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __restrict__ part, GemmPlanDev plan, int M,
-                                                             int d, float* __restrict__ h,
-                                                             const uint16_t* __restrict__ w, float eps,
-                                                             uint16_t* __restrict__ x, int TM, int norm_row_begin) {
+// kNormPer float4 per thread at most: 2 for decode-sized CTAs (up to 1024
+// threads, one float4 each at d <= 4096), 4 (8 for d > 8192) for long
+// prefills (<= 512 threads, registers for all of a thread's loads in flight
+// at once).
+template <int kNormPer>
+__global__ void __launch_bounds__(kNormPer <= 2 ? 1024 : 512)
+    residual_norm_kernel(const float* __restrict__ part, GemmPlanDev plan, int M, int d, float* __restrict__ h,
+                         const uint16_t* __restrict__ w, float eps, uint16_t* __restrict__ x, int TM,
+                         int norm_row_begin) {
   __shared__ float red[32];
   pdl_wait();
   pdl_trigger();
@@ -191,18 +196,38 @@ __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __rest
   const int d4 = d >> 2;
   float4* hr = reinterpret_cast<float4*>(h + (size_t)m * d);
   const float4* pr = reinterpret_cast<const float4*>(part + (size_t)m * d);
-  float4 v[kNormPer];
+  float4 v[kNormPer], a[kNormPer];
   float ss = 0.f;
+  // every load of the row first, then the adds and stores: a store between
+  // them keeps the compiler from hoisting the next cache-global loads, which
+  // had serialised a thread's float4s into one DRAM round trip each
+  if (plan.aligned) {  // one partial slot (long prefills): plain loads, nothing dependent in between
+#pragma unroll
+    for (int k = 0; k < kNormPer; ++k) {
+      const int i4 = threadIdx.x + k * blockDim.x;
+      if (i4 < d4) {
+        v[k] = hr[i4];
+        a[k] = __ldcg(pr + i4);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kNormPer; ++k) {
+      const int i4 = threadIdx.x + k * blockDim.x;
+      if (i4 < d4) {
+        v[k] = hr[i4];
+        a[k] = part_ld4(plan, pr + i4, stride / 4, m, i4 * 4);
+      }
+    }
+  }
 #pragma unroll
   for (int k = 0; k < kNormPer; ++k) {
     const int i4 = threadIdx.x + k * blockDim.x;
     if (i4 < d4) {
-      v[k] = hr[i4];
-      const float4 a = part_ld4(plan, pr + i4, stride / 4, m, i4 * 4);
-      v[k].x += a.x;
-      v[k].y += a.y;
-      v[k].z += a.z;
-      v[k].w += a.w;
+      v[k].x += a[k].x;
+      v[k].y += a[k].y;
+      v[k].z += a[k].z;
+      v[k].w += a[k].w;
       hr[i4] = v[k];
       ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
     }
@@ -238,25 +263,34 @@ __global__ void __launch_bounds__(1024) residual_norm_kernel(const float* __rest
 
 // A long prefill (thousands of rows) wants 4 float4 per thread; a decode step
 // (tens of rows) wants the widest CTA: one float4 per thread.
-static int norm_threads(int d, int M) {
-  int t = M >= 1024 ? (d / 4 + 3) / 4 : d / 4;
-  if (t > 1024) t = 1024;
-  return (t + 31) / 32 * 32;
+static cudaError_t norm_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h,
+                               const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM, int norm_row_begin,
+                               cudaStream_t s) {
+  const int d4 = d / 4;
+  int t = M >= 1024 ? (d4 + 3) / 4 : d4;
+  t = (std::min(t, 1024) + 31) / 32 * 32;
+  if (t <= 1024 && d4 <= 2 * t)
+    return launch_pdl(residual_norm_kernel<2>, dim3(M), dim3(t), 0, s, part, plan, M, d, h, norm_w, eps, x_packed,
+                      TM, norm_row_begin);
+  t = ((d4 + 3) / 4 + 31) / 32 * 32;
+  if (t <= 512)
+    return launch_pdl(residual_norm_kernel<4>, dim3(M), dim3(t), 0, s, part, plan, M, d, h, norm_w, eps, x_packed,
+                      TM, norm_row_begin);
+  t = ((d4 + 7) / 8 + 31) / 32 * 32;
+  if (t > 512) return cudaErrorInvalidValue;
+  return launch_pdl(residual_norm_kernel<8>, dim3(M), dim3(t), 0, s, part, plan, M, d, h, norm_w, eps, x_packed, TM,
+                    norm_row_begin);
 }
 
 cudaError_t residual_norm_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h, const uint16_t* norm_w,
                                  float eps, uint16_t* x_packed, int TM, cudaStream_t s) {
-  if (d / 4 > kNormPer * 1024) return cudaErrorInvalidValue;
-  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d, M)), 0, s, part, plan, M, d, h, norm_w, eps,
-                    x_packed, TM, 0);
+  return norm_launch(part, plan, M, d, h, norm_w, eps, x_packed, TM, 0, s);
 }
 
 cudaError_t residual_norm_rows_launch(const float* part, const GemmPlanDev& plan, int M, int d, float* h,
                                       const uint16_t* norm_w, float eps, uint16_t* x_packed, int TM,
                                       int norm_row_begin, cudaStream_t s) {
-  if (d / 4 > kNormPer * 1024) return cudaErrorInvalidValue;
-  return launch_pdl(residual_norm_kernel, dim3(M), dim3(norm_threads(d, M)), 0, s, part, plan, M, d, h, norm_w, eps,
-                    x_packed, TM, norm_row_begin);
+  return norm_launch(part, plan, M, d, h, norm_w, eps, x_packed, TM, norm_row_begin, s);
 }
 
 // ------------------------------------------------------------- SiLU(gate)*up
