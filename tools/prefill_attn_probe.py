@@ -25,19 +25,22 @@ def main():
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--H", type=int, default=40)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--layers", type=int, default=1, help="layers per KV page (40 = the 13B serving geometry)")
     a = ap.parse_args()
-    n, H, hd, L = a.n, a.H, 128, 1
+    n, H, hd, L = a.n, a.H, 128, a.layers
     page_bytes = 16 * L * H * 2 * hd * 2
     nb = (n + 15) // 16
-    arena = torch.randint(-16000, 16000, (nb * page_bytes // 2,), dtype=torch.int16, device="cuda")
-    arena = (arena.view(torch.bfloat16).float().clamp(-1, 1) * 0.5).to(torch.bfloat16).view(torch.int16)
+    arena = torch.empty((nb * page_bytes // 2,), dtype=torch.int16, device="cuda")
+    for c in arena.split(1 << 28):
+        r = torch.randint(-16000, 16000, c.shape, dtype=torch.int16, device="cuda")
+        c.copy_((r.view(torch.bfloat16).float().clamp(-1, 1) * 0.5).to(torch.bfloat16).view(torch.int16))
     pages = torch.randperm(nb, dtype=torch.int32, device="cuda")
     q = torch.randn(n * H * hd, dtype=torch.float32, device="cuda")
     out = torch.empty(n * H * hd, dtype=torch.int16, device="cuda")
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def run():
-        N.check(N.lib().ms_k_attn_prefill(C.c_void_p(q.data_ptr()), C.c_void_p(arena.data_ptr()), page_bytes, L, 0,
+        N.check(N.lib().ms_k_attn_prefill(C.c_void_p(q.data_ptr()), C.c_void_p(arena.data_ptr()), page_bytes, L, L // 2,
                                           H, H, hd, C.c_void_p(pages.data_ptr()), n, C.c_void_p(out.data_ptr()), st))
     run()
     torch.cuda.synchronize()
@@ -51,7 +54,7 @@ def main():
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
     flops = 4.0 * H * hd * n * (n + 1) / 2
-    print(json.dumps({"n": n, "H": H, "ms": ms, "tflops": flops / ms / 1e9, "each": [round(t, 4) for t in ts]}))
+    print(json.dumps({"n": n, "H": H, "layers_per_page": L, "ms": ms, "tflops": flops / ms / 1e9, "each": [round(t, 4) for t in ts]}))
 
 
 
