@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // MS_GEMM_DEBUG (experiments only): bit0 skip activation loads, bit1 skip MMAs,
-// bit3 CTA-0 timeline, bit4 producer stamps, bit5 one raw-chunk producer,
+// bit3 CTA-0 timeline, bit4 producer stamps, bit5 one raw-chunk producer, bit6 per-CTA start/end,
 // bit2 (W4 TMEM) skip the dequant ALU work and TMEM stores.
 static int gemm_debug() {
   static const int v = [] {
@@ -322,6 +322,8 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
     }
   };
 
+  uint64_t t0_dbg = 0;
+  if (dbg & 64) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0_dbg));
   uint8_t* bbase = smem;
   uint8_t* rbase = smem + (size_t)bstages * 2 * kGPS * b_bytes;
   uint64_t* bfull = reinterpret_cast<uint64_t*>(rbase + (size_t)rstages * raw_stage);
@@ -660,6 +662,13 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
   tc_fence_before();
   __syncthreads();
   stamp(6, threadIdx.x == 0 ? 1 : 64);
+  if ((dbg & 64) && threadIdx.x == 0) {  // (debug) per-CTA start / end globaltimer after the CTA-0 timeline
+    uint64_t* ce = reinterpret_cast<uint64_t*>(out + (size_t)150 * M * N) + 1024 + 2 * blockIdx.x;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    ce[0] = t0_dbg;
+    ce[1] = t;
+  }
   if (warp == 1) tmem_dealloc(tmem_base, 512);
 }
 

@@ -60,6 +60,14 @@ def main():
             continue
         rows.append({"unit": i, **{f"e{e}": (ev[e] - t0 if ev[e] else None) for e in range(8) if e != 6}})
     print(json.dumps({"name": args.name, "M": M, "end_ns": int(tl[6, 1]) - t0 if int(tl[6, 1]) else None}))
+    if int(os.environ.get("MS_GEMM_DEBUG", "0")) & 64:  # per-CTA start / end (ns from the earliest start)
+        ce = out.view(-1)[150 * M * Nn:150 * M * Nn + 2 * (1024 + 2 * 148)].view(torch.int64)[1024:].view(148, 2).cpu()
+        ce = ce[ce[:, 1] > 0]
+        s0 = int(ce[:, 0].min())
+        st, en = (ce[:, 0] - s0).tolist(), (ce[:, 1] - s0).tolist()
+        q = lambda v, f: sorted(v)[int(f * (len(v) - 1))]
+        print(json.dumps({"ctas": len(en), "start_ns": [q(st, f) for f in (0, .5, 1)],
+                          "end_ns": [q(en, f) for f in (0, .1, .5, .9, 1)]}))
     for r in rows:
         print(json.dumps(r))
 
