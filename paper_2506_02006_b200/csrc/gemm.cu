@@ -299,7 +299,8 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta = blockIdx.x;
+  // (debug, dbg bits 8..15) rotate the CTA -> work map, to tell per-SM from per-range effects apart
+  const int cta = (dbg >> 8) ? (int)((blockIdx.x + (unsigned)(dbg >> 8)) % gridDim.x) : (int)blockIdx.x;
   const int nk = plan.nk;
   const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk; a B stage holds 2 * kGPS
   static_assert(kBits == 4 || (kBits == 8 && kGPS == 1), "Q8 units hold one K group");
@@ -666,7 +667,9 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
     uint64_t* ce = reinterpret_cast<uint64_t*>(out + (size_t)150 * M * N) + 1024 + 2 * blockIdx.x;
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    ce[0] = t0_dbg;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    ce[0] = (t0_dbg & 0xFFFFFFFFFFFFull) | ((uint64_t)smid << 48);  // start (low 48 bits) | SM id
     ce[1] = t;
   }
   if (warp == 1) tmem_dealloc(tmem_base, 512);

@@ -63,11 +63,19 @@ def main():
     if int(os.environ.get("MS_GEMM_DEBUG", "0")) & 64:  # per-CTA start / end (ns from the earliest start)
         ce = out.view(-1)[150 * M * Nn:150 * M * Nn + 2 * (1024 + 2 * 148)].view(torch.int64)[1024:].view(148, 2).cpu()
         ce = ce[ce[:, 1] > 0]
+        sm = (ce[:, 0] >> 48).tolist()
+        ce[:, 0] &= (1 << 48) - 1
+        ce[:, 1] &= (1 << 48) - 1
         s0 = int(ce[:, 0].min())
         st, en = (ce[:, 0] - s0).tolist(), (ce[:, 1] - s0).tolist()
         q = lambda v, f: sorted(v)[int(f * (len(v) - 1))]
         print(json.dumps({"ctas": len(en), "start_ns": [q(st, f) for f in (0, .5, 1)],
                           "end_ns": [q(en, f) for f in (0, .1, .5, .9, 1)]}))
+        if os.environ.get("W4_PROBE_SM"):
+            rot = int(os.environ.get("MS_GEMM_DEBUG", "0")) >> 8
+            work = [(b + rot) % 148 for b in range(len(en))]  # rows are in blockIdx order
+            print(json.dumps({"sm_end": dict(zip(sm, [e - s for s, e in zip(st, en)])),
+                              "work_end": dict(zip(work, [e - s for s, e in zip(st, en)]))}))
     for r in rows:
         print(json.dumps(r))
 
