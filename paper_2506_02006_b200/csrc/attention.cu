@@ -712,11 +712,8 @@ static cudaError_t launch_gqa(const AttnArgs& a_in, cudaStream_t stream) {
   }
   const size_t smem = 1024 + (size_t)stages * 8192 + 2 * stages * 8 +
                       ((size_t)4 * G * 128 + 8 * G + (size_t)G * 128) * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_gqa_mma_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  max_smem_once(attn_gqa_mma_kernel<G>, 200 * 1024, attr);
   attn_item_map(a);
   const int ctas = a.whole_items + (a.rows * a.KVH - a.whole_items) * a.tail_splits;
   cudaError_t e = launch_pdl(attn_gqa_mma_kernel<G>, dim3(ctas), dim3(160), smem, stream, a, tmap);
@@ -742,11 +739,8 @@ static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
   a.stages = stages;
   size_t smem = (size_t)stages * BT * HD * 4 + 2 * stages * 8 + (size_t)4 * G * (HD + 2) * 4 + (size_t)G * HD * 4;
   if (ctas_per_sm > 0) smem = std::max(smem, (size_t)(220 * 1024) / ctas_per_sm);  // cap residency
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_decode_kernel<HD, G, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  max_smem_once(attn_decode_kernel<HD, G, BT>, 200 * 1024, attr);
   attn_item_map(a);
   const int ctas = a.whole_items + (a.rows * a.KVH - a.whole_items) * a.tail_splits;
   cudaError_t e = launch_pdl(attn_decode_kernel<HD, G, BT>, dim3(ctas), dim3(160), smem, stream, a);

@@ -759,12 +759,8 @@ static cudaError_t launch_q_tmem(const GemmWeights& w, const uint16_t* x, int M,
   size_t sm = 0;
   const int bs = pick_q_stages(TM, kGPS, kBits, &rs, &as, &g, &sm);
   if (bs < 0 || g != kG) return cudaErrorInvalidConfiguration;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_w4_tmem_kernel<kG, kGPS, kBits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  max_smem_once(gemm_w4_tmem_kernel<kG, kGPS, kBits>, 227 * 1024, attr);
   return launch_pdl(gemm_w4_tmem_kernel<kG, kGPS, kBits>, dim3(plan.C), dim3((kDqWarp0 + 4 * kG) * 32), sm, stream, w, x, M,
                     TM, plan, out, bs, rs, as, gemm_debug(), epi);
 }
@@ -800,11 +796,8 @@ cudaError_t gemm_launch(const GemmWeights& w, int wkind, const uint16_t* x, int 
   int st = (int)((size_t)(215 * 1024) / stage);
   st = std::max(2, std::min(st, max_st));
   const size_t smem = st * stage + (2 * st + 4) * 8 + 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  max_smem_once(gemm_kernel, 227 * 1024, attr);
   return launch_pdl(gemm_kernel, dim3(plan.C), dim3(192), smem, stream, w, x, M, TM, plan, out, st, epi);
 }
 

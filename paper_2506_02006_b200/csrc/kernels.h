@@ -1,6 +1,7 @@
 // kernels.h -- internal launch interface between the runtime (runtime.cu) and
 // the CUDA kernels.  Not part of the public C ABI (include/morphserve.h).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -8,6 +9,19 @@
 #include <utility>
 
 namespace ms {
+
+// Dynamic shared-memory opt-in for `fn` on the current device.  The attribute
+// is per device, so a process driving several GPUs (peer fetch between
+// contexts) sets it once per (kernel, device); `done` is the kernel's bit set.
+template <typename F>
+inline void max_smem_once(F* fn, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_release);
+}
 
 // Every hot-path kernel is launched with programmatic dependent launch so its
 // launch latency and prologue overlap the tail of the previous kernel

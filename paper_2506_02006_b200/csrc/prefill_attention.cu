@@ -257,20 +257,14 @@ cudaError_t prefill_attn_launch(const PrefillAttnArgs& a, cudaStream_t stream) {
   auto smem_for = [&](int hd) { return (size_t)kQTile * hd * 2 + (size_t)2 * 2 * kKTile * hd * 2 + max_blocks * 4 + 16; };
   if (a.kv.head_dim == 128) {
     const size_t sm = smem_for(128);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(prefill_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    max_smem_once(prefill_attn_kernel<128>, 227 * 1024, attr);
     return launch_pdl(prefill_attn_kernel<128>, dim3(qtiles, a.H), dim3(128), sm, stream, a);
   }
   if (a.kv.head_dim == 64) {
     const size_t sm = smem_for(64);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(prefill_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    max_smem_once(prefill_attn_kernel<64>, 227 * 1024, attr);
     return launch_pdl(prefill_attn_kernel<64>, dim3(qtiles, a.H), dim3(128), sm, stream, a);
   }
   return cudaErrorInvalidValue;

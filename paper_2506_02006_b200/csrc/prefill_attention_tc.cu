@@ -516,11 +516,8 @@ cudaError_t prefill_attn_tc_launch(const PrefillAttnArgs& a, cudaStream_t stream
   const int qpairs = (a.n + 2 * kTcTile - 1) / (2 * kTcTile);
   const size_t smem = kCtrlBytes + 1024 + (size_t)(2 + kKStages + kVStages) * kOpBytes;
   if (smem > 227 * 1024) return cudaErrorNotSupported;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  max_smem_once(prefill_attn_tc_kernel, 227 * 1024, attr);
   return launch_pdl(prefill_attn_tc_kernel, dim3(a.H * qpairs), dim3(kThreads), smem, stream, a, tmap);
 }
 
