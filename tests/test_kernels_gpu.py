@@ -162,7 +162,12 @@ def test_gemm_q8_q3(bits, Nn, K, M, TM, splits):
     (32, 32, 128, [4100], 16),
     # MHA hd 128: warp-per-block consumer, long rows (many ring wraps)
     (32, 32, 128, [2048, 1, 1500, 17, 4096], 1),
-    (8, 1, 128, [64, 129, 16, 17], 3)])
+    (8, 1, 128, [64, 129, 16, 17], 3),
+    # persistent GQA: > 32 rows (prefix scan over several rows per lane), items
+    # cut across CTAs next to 1-block items, and the 16-piece cap
+    (32, 8, 128, [2048] * 3 + [1] * 40 + [513, 31, 16, 17], 1),
+    (16, 4, 128, [int(x) for x in np.random.default_rng(5).integers(1, 1200, 70)], 1),
+    (32, 8, 128, [3000], 1)])
 def test_paged_attention(H, KVH, hd, ctxs, splits):
     N = _native()
     L, layer = 3, 1
