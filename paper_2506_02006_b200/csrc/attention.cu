@@ -128,10 +128,15 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
   const int kAttnStages = a.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAttnStages * kStageBytes);
   uint64_t* empty = full + kAttnStages;
-  float* scratch = reinterpret_cast<float*>(empty + kAttnStages);  // [4][G][HD] acc + [4][G][2] m,l
+  uint64_t* kv_ready = empty + kAttnStages;  // the new token's K/V is in the cache (fused QKV); 16 B slot
+  float* scratch = reinterpret_cast<float*>(kv_ready + 2);  // [4][G][HD] acc + [4][G][2] m,l
 
-  pdl_wait();
-  pdl_trigger();
+  // No grid-dependency wait before the producer starts: the K/V of earlier
+  // tokens, the block table and ctx_len were written by kernels that completed
+  // before this grid launched (the previous kernel -- the QKV GEMM -- writes
+  // only its fp32 partials, and every row kernel waits before it triggers),
+  // so the ring fills while the QKV GEMM drains and the consumers wait for it.
+  // Only the block receiving the new token waits, for the consumers' append.
   int kvh, row, split, nsplit;
   attn_item(a, kvh, row, split, nsplit);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -147,13 +152,23 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kWarpPerBlock ? 1 : 4);
     }
+    mbar_init(kv_ready, 1);
     fence_mbar_init();
   }
+  __syncthreads();
   // q source: fused QKV post-processing into shared memory, or the q buffer
   float* qsm = scratch + (size_t)4 * G * HD + 8 * G;  // [G][HD] fp32
   const bool fused = a.qkv_part != nullptr;
-  if (fused) attn_qkv_fused<HD, G>(a, kvh, row, b1 == nb, qsm, threadIdx.x, blockDim.x);
-  __syncthreads();
+  const bool append = fused && b1 == nb;  // this CTA writes (then streams) the new token's block
+  if (warp != 4) {  // consumers (named barrier 1): after the QKV GEMM, q into smem, new K/V into the cache
+    pdl_wait();
+    pdl_trigger();
+    if (fused) {
+      attn_qkv_fused<HD, G>(a, kvh, row, append, qsm, threadIdx.x, 128);  // ends with a generic->async proxy fence
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0 && append) mbar_arrive(kv_ready);
+    }
+  }
   const float* qsrc = fused ? qsm : a.q + ((size_t)row * a.H + kvh * G) * HD;
 
   float m[G], l[G], acc[G][VEC];
@@ -167,6 +182,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
       if (lane == 0) {
         const int s = it % kAttnStages;
         if (it >= kAttnStages) mbar_wait(&empty[s], ((it / kAttnStages) & 1) ^ 1);
+        if (append && b0 + it == nb - 1) mbar_wait(kv_ready, 0);
         const char* src = a.kv.arena + (int64_t)page * a.kv.page_bytes + kv_off;
         mbar_expect_tx(&full[s], kStageBytes);
         bulk_g2s(smem + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
@@ -478,8 +494,7 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
   uint64_t* kv_ready = empty + S;  // the new token's K/V is in the cache (fused QKV)
   float* scratch = reinterpret_cast<float*>(kv_ready + 1);  // [4][G][HD] acc + [4][G][2] m,l, then q [G][HD]
 
-  pdl_wait();
-  pdl_trigger();
+  // producer streams before the grid-dependency wait (see attn_decode_kernel)
   int kvh, row, split, nsplit;
   attn_item(a, kvh, row, split, nsplit);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -530,6 +545,8 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
     return;
   }
   // ------------------------------------------------------------- consumers
+  pdl_wait();
+  pdl_trigger();
   if (fused) {  // consumers only (named barrier 1): q into smem, new K/V into the cache
     attn_qkv_fused<HD, G>(a, kvh, row, append, qsm, threadIdx.x, 128);  // ends with a generic->async proxy fence
     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -737,7 +754,7 @@ static cudaError_t launch_g(const AttnArgs& a_in, cudaStream_t stream) {
   static const int ctas_per_sm = attn_env("MS_ATTN_CTAS", 0);
   AttnArgs a = a_in;
   a.stages = stages;
-  size_t smem = (size_t)stages * BT * HD * 4 + 2 * stages * 8 + (size_t)4 * G * (HD + 2) * 4 + (size_t)G * HD * 4;
+  size_t smem = (size_t)stages * BT * HD * 4 + 2 * stages * 8 + 16 + (size_t)4 * G * (HD + 2) * 4 + (size_t)G * HD * 4;
   if (ctas_per_sm > 0) smem = std::max(smem, (size_t)(220 * 1024) / ctas_per_sm);  // cap residency
   static std::atomic<uint64_t> attr{0};
   max_smem_once(attn_decode_kernel<HD, G, BT>, 200 * 1024, attr);
