@@ -54,6 +54,18 @@ def run(H, KVH, rows=64, ctx=2048, L=32, hd=128, iters=10):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "tlb":
+        # MHA kernel, 2048 items each: the per-layer slice of a page that one
+        # 2 MB translation serves (256 KB vs 64 KB) at equal page size
+        for H, KVH, rows, L in [(32, 32, 64, 32), (32, 32, 64, 8), (8, 8, 256, 32), (8, 8, 256, 8)]:
+            r = run(H, KVH, rows=rows, L=L)
+            r.update(rows=rows, L=L, slice_KB=KVH * 2 * 128 * 16 * 2 // 1024)
+            print(json.dumps(r), flush=True)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "gqa":  # run under MS_ATTN_GQA_MMA=0 / 1
+        for rows in (64, 16):
+            print(json.dumps(dict(run(32, 8, rows=rows), rows=rows)), flush=True)
+        sys.exit(0)
     for H, KVH in [(32, 8), (8, 8), (32, 32)]:
         print(json.dumps(run(H, KVH)), flush=True)
     # 8B GQA with a 4x longer context per row (fewer rows in flight per byte)
