@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(192, 1)
 
 // MS_GEMM_DEBUG (experiments only): bit0 skip activation loads, bit1 skip MMAs,
 // bit3 CTA-0 timeline, bit4 producer stamps, bit5 one raw-chunk producer, bit6 per-CTA start/end,
-// bit2 (W4 TMEM) skip the dequant ALU work and TMEM stores.
+// bit2 (W4 TMEM) skip the dequant ALU work and TMEM stores, bits 16..19 (W4) pre-issued raw units.
 static int gemm_debug() {
   static const int v = [] {
     const char* e = std::getenv("MS_GEMM_DEBUG");
@@ -300,7 +300,8 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
   const int N = W.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // (debug, dbg bits 8..15) rotate the CTA -> work map, to tell per-SM from per-range effects apart
-  const int cta = (dbg >> 8) ? (int)((blockIdx.x + (unsigned)(dbg >> 8)) % gridDim.x) : (int)blockIdx.x;
+  const int rot = (dbg >> 8) & 255;
+  const int cta = rot ? (int)((blockIdx.x + (unsigned)rot) % gridDim.x) : (int)blockIdx.x;
   const int nk = plan.nk;
   const uint32_t b_bytes = (uint32_t)TM * 128u;  // one 64-wide activation chunk; a B stage holds 2 * kGPS
   static_assert(kBits == 4 || (kBits == 8 && kGPS == 1), "Q8 units hold one K group");
@@ -389,7 +390,9 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
   // together) and the dequantisers start earlier; measured 2-5% per W4 decode
   // GEMM isolated, neutral in the step.  Long prefills (compute bound) fill
   // the whole ring.  Both producer threads need the count.
-  const uint32_t pre_cap = TM <= 128 ? (uint32_t)min(rstages, 2) : (uint32_t)rstages;
+  // (debug, dbg bits 16..19: pre-issued unit count override, A/B only)
+  const uint32_t pre_cap = ((dbg >> 16) & 15) ? (uint32_t)min(rstages, (dbg >> 16) & 15)
+                         : TM <= 128 ? (uint32_t)min(rstages, 2) : (uint32_t)rstages;
   if (threadIdx.x == (kDqWarp0 - 1) * 32) {
     SegIter pre(plan, cta);
     int t, k0, k1;
