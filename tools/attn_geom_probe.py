@@ -21,8 +21,8 @@ import torch  # noqa: E402
 from paper_2506_02006_b200 import _native as N  # noqa: E402
 
 
-def run(H, KVH, rows=64, ctx=2048, L=32, hd=128, iters=10):
-    page_bytes = 16 * L * KVH * 2 * hd * 2
+def run(H, KVH, rows=64, ctx=2048, L=32, hd=128, iters=10, pad=0):
+    page_bytes = 16 * L * KVH * 2 * hd * 2 + pad  # pad: page stride beyond one block's bytes
     nb = (ctx + 15) // 16
     n_pages = rows * nb
     arena = torch.empty(n_pages * page_bytes // 2, dtype=torch.int16, device="cuda").random_(-2000, 2000)
@@ -61,6 +61,12 @@ if __name__ == "__main__":
             r = run(H, KVH, rows=rows, L=L)
             r.update(rows=rows, L=L, slice_KB=KVH * 2 * 128 * 16 * 2 // 1024)
             print(json.dumps(r), flush=True)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "pad":
+        # same pages, stride padded: concurrent reads no longer share their offset modulo 2 MiB
+        for H, KVH in [(32, 8), (8, 8)]:
+            for pad in (0, 8192, 65536, 262144):
+                print(json.dumps(dict(run(H, KVH, pad=pad), pad=pad)), flush=True)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "gqa":  # run under MS_ATTN_GQA_MMA=0 / 1
         for rows in (64, 16):
