@@ -21,13 +21,16 @@ import torch  # noqa: E402
 from paper_2506_02006_b200 import _native as N  # noqa: E402
 
 
-def run(H, KVH, rows=64, ctx=2048, L=32, hd=128, iters=10, pad=0):
+def run(H, KVH, rows=64, ctx=2048, L=32, hd=128, iters=10, pad=0, spread=1, perm=False):
     page_bytes = 16 * L * KVH * 2 * hd * 2 + pad  # pad: page stride beyond one block's bytes
     nb = (ctx + 15) // 16
     n_pages = rows * nb
-    arena = torch.empty(n_pages * page_bytes // 2, dtype=torch.int16, device="cuda").random_(-2000, 2000)
+    # spread: the same pages placed every `spread`-th page of a larger arena
+    arena = torch.empty(n_pages * spread * page_bytes // 2, dtype=torch.int16, device="cuda").random_(-2000, 2000)
     # interleaved ids as in bench.build_model: row r's block j -> page j * rows + r
-    pages = torch.arange(n_pages, dtype=torch.int32, device="cuda").reshape(nb, rows).t().contiguous()
+    ids = torch.randperm(n_pages, device="cuda").to(torch.int32) if perm else torch.arange(n_pages, dtype=torch.int32,
+                                                                                          device="cuda")
+    pages = (ids * spread).reshape(nb, rows).t().contiguous()
     q = torch.randn(rows, H, hd, device="cuda")
     d_ctx = torch.full((rows,), ctx, dtype=torch.int32, device="cuda")
     out = torch.empty(rows * H * hd, dtype=torch.int16, device="cuda")
@@ -67,6 +70,12 @@ if __name__ == "__main__":
         for H, KVH in [(32, 8), (8, 8)]:
             for pad in (0, 8192, 65536, 262144):
                 print(json.dumps(dict(run(H, KVH, pad=pad), pad=pad)), flush=True)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "spread":
+        # same bytes, pages spread over a 1x / 2x / 4x larger arena, or randomly permuted
+        for H, KVH in [(32, 8), (8, 8)]:
+            for sp, pm in ((1, False), (2, False), (4, False), (1, True), (4, True)):
+                print(json.dumps(dict(run(H, KVH, spread=sp, perm=pm), spread=sp, perm=pm)), flush=True)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "gqa":  # run under MS_ATTN_GQA_MMA=0 / 1
         for rows in (64, 16):
