@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
 
   float m[G], l[G], acc[G][VEC];
   if (warp == 4) {
+    pdl_trigger();  // every thread of the CTA signals (the consumers after their wait)
     // page ids of the next 32 blocks in one warp-wide load, handed to lane 0
     // by shuffle (no dependent global load in front of each copy)
     int pid = 0;
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(160) attn_gqa_mma_kernel(AttnArgs a, const __g
     // ------------------------------------------------------------ producer
     // streams from the start; only the block holding the new token waits for
     // the consumers' fused QKV append
+    pdl_trigger();
     int pid = 0;  // page ids of the next 32 blocks, one warp-wide load
     for (int it = 0; it < b1 - b0; ++it) {
       if ((it & 31) == 0) pid = it + lane < b1 - b0 ? __ldg(ptab + b0 + it + lane) : 0;
