@@ -180,10 +180,12 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(AttnArgs a) {
     for (int it = 0; it < b1 - b0; ++it) {
       if ((it & 31) == 0) pid = it + lane < b1 - b0 ? __ldg(ptab + b0 + it + lane) : 0;
       const int page = __shfl_sync(0xffffffffu, pid, it & 31);
+      const int s = it % kAttnStages;
+      // the whole warp waits on the ring (measured on the GQA producer: lane-0-only
+      // waits were 1.5% slower per 8B step)
+      if (it >= kAttnStages) mbar_wait(&empty[s], ((it / kAttnStages) & 1) ^ 1);
+      if (append && b0 + it == nb - 1) mbar_wait(kv_ready, 0);
       if (lane == 0) {
-        const int s = it % kAttnStages;
-        if (it >= kAttnStages) mbar_wait(&empty[s], ((it / kAttnStages) & 1) ^ 1);
-        if (append && b0 + it == nb - 1) mbar_wait(kv_ready, 0);
         const char* src = a.kv.arena + (int64_t)page * a.kv.page_bytes + kv_off;
         mbar_expect_tx(&full[s], kStageBytes);
         bulk_g2s(smem + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
