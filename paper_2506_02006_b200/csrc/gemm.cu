@@ -154,27 +154,31 @@ __global__ void __launch_bounds__(192, 1)
   pdl_trigger();
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ producer
-      pdl_wait();
-      SegIter seg(plan, cta);
-      int t, k0, k1;
-      uint32_t it = 0;
-      while (seg.next(t, k0, k1)) {
-        const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
-        const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
-        cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
-        for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
-          if (it < npre) {  // weight chunk already in flight: only the activations remain
-            bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
-            continue;
-          }
-          const int s = it % stages;
-          if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+    // ------------------------------------------------------------ producer
+    // the whole warp walks the ring and waits on it; lane 0 issues the copies
+    // (a lone spinning lane was measured slower in the attention producers)
+    npre = __shfl_sync(0xffffffffu, npre, 0);
+    pdl_wait();
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t it = 0;
+    while (seg.next(t, k0, k1)) {
+      const int n_tile = t % plan.n_tiles, m_tile = t / plan.n_tiles;
+      const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
+      cur.seek(W.first_chunk + (int64_t)n_tile * nk + k0);
+      for (int k = k0; k < k1; ++k, ++it, cur.advance()) {
+        if (it < npre) {  // weight chunk already in flight: only the activations remain
+          if (lane == 0) bulk_g2s(sB(it), xb + (size_t)k * b_bytes, b_bytes, &full[it]);
+          continue;
+        }
+        const int s = it % stages;
+        if (it >= (uint32_t)stages) mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+        if (lane == 0) {
           mbar_expect_tx(&full[s], a_bytes + b_bytes);
           bulk_g2s(sA(s), cur.get(), a_bytes, &full[s]);
           bulk_g2s(sB(s), xb + (size_t)k * b_bytes, b_bytes, &full[s]);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
