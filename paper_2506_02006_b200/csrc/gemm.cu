@@ -424,7 +424,9 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
   // (debug, dbg bit5) a single producer thread, for A/B timing
   const uint32_t nprod = (dbg & 32) ? 1u : (uint32_t)kProducers;
   if (warp == 0 || warp == kDqWarp0 - 1) {
-    if (lane == 0 && (warp == 0 || nprod > 1)) {
+    // the whole warp waits on the ring, lane 0 issues and moves the cursor
+    npre = __shfl_sync(0xffffffffu, npre, 0);
+    if (warp == 0 || nprod > 1) {
       // ----------------------------------------------------------- producers
       // raw int4 chunks (independent of the activation ring, so the weight
       // stream runs `rstages` ahead; weights need no grid dependency).
@@ -446,12 +448,15 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
         cur.seek(W.first_chunk + (int64_t)n_tile * gpr + (int64_t)(k0 + (int)(u - it)) * kGPS);
         uint32_t r = u % (uint32_t)rstages, ph = ((u / (uint32_t)rstages) & 1) ^ 1;
         for (; u < end; u += nprod) {
-          if (dbg & 16) stamp(5, u);
+          if ((dbg & 16) && lane == 0) stamp(5, u);
           mbar_wait(&rempty[r], ph);
-          if (dbg & 16) stamp(3, u);
-          issue_unit((int)r, u);
-          stamp(0, u);
-          for (uint32_t i = 0; i < (nprod - 1) * kGPS; ++i) cur.advance();  // the other producer's units
+          if (lane == 0) {
+            if (dbg & 16) stamp(3, u);
+            issue_unit((int)r, u);
+            stamp(0, u);
+            for (uint32_t i = 0; i < (nprod - 1) * kGPS; ++i) cur.advance();  // the other producer's units
+          }
+          __syncwarp();
           r += nprod;
           while (r >= (uint32_t)rstages) {
             r -= (uint32_t)rstages;
@@ -511,19 +516,20 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
       ++u;
     }
   } else if (warp == 6) {
-    if (lane == 0) {
-      // activation (B) chunks: own warp (a spin-wait here must not hold up the
-      // weight producer), after the grid dependency
-      pdl_wait();
-      SegIter seg(plan, cta);
-      int t, k0, k1;
-      uint32_t it = 0;
-      uint32_t s = 0, ph = 1;
-      while (seg.next(t, k0, k1)) {
-        const int m_tile = t / plan.n_tiles;
-        const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
-        for (int k = k0; k < k1; ++k, ++it) {
-          if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ph);
+    // activation (B) chunks: own warp (a spin-wait here must not hold up the
+    // weight producer), after the grid dependency; the whole warp waits on
+    // the ring, lane 0 issues
+    pdl_wait();
+    SegIter seg(plan, cta);
+    int t, k0, k1;
+    uint32_t it = 0;
+    uint32_t s = 0, ph = 1;
+    while (seg.next(t, k0, k1)) {
+      const int m_tile = t / plan.n_tiles;
+      const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + (size_t)m_tile * kb_per_mtile * b_bytes;
+      for (int k = k0; k < k1; ++k, ++it) {
+        if (it >= (uint32_t)bstages) mbar_wait(&bempty[s], ph);
+        if (lane == 0) {
           if (dbg & 1) {  // (debug) no activation traffic: complete the stage empty
             mbar_expect_tx(&bfull[s], 0);
           } else {
@@ -531,10 +537,11 @@ __global__ void __launch_bounds__((kDqWarp0 + 4 * kG) * 32, 1)
             bulk_g2s(sB(s), xb + (size_t)(2 * kGPS * k) * b_bytes, 2 * kGPS * b_bytes, &bfull[s]);
           }
           if (!(dbg & 16)) stamp(5, it);
-          if (++s == (uint32_t)bstages) {
-            s = 0;
-            ph ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++s == (uint32_t)bstages) {
+          s = 0;
+          ph ^= 1;
         }
       }
     }
