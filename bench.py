@@ -625,7 +625,9 @@ def main():
         sys.exit(spawn_ranks(args.gpus))
     if args.ranks_probe:
         rank, local_rank, world = dist_env()
-        print(json.dumps({"rank": rank, "local_rank": local_rank, "world": world}), flush=True)
+        # one write(2) per line: the ranks share the parent's stdout pipe, and a
+        # print() may split the text and its newline into two writes that interleave
+        os.write(1, (json.dumps({"rank": rank, "local_rank": local_rank, "world": world}) + "\n").encode())
         return
     if args.impl == "reference":
         run_reference(args)
